@@ -1,0 +1,26 @@
+"""paper_1912_10877_b200 — a B200-native (sm_100a) state-vector engine for Yao-style
+differentiable quantum circuits (arXiv 1912.10877), behind the reference's register / block
+API.  Compute runs only in ``libqbg.so`` (CUDA, built in-tree); this package is the host
+mirror of the reference interface (qblock register.hpp / gates.hpp and SPEC.md blocks /
+autodiff) over its C-ABI (include/qbg.h)."""
+from . import errors
+from ._capi import LIB_PATH, lib
+from .ad import GradResult, backward, expect, expect_grad, obs_apply
+from .blocks import (CNOT, CZ, SWAP, Add, Block, Chain, Control, Daggered, GeneralMatrix, H, I2, Kron, P0, P1,
+                     Pd, Phase, Program, Pu, Put, Repeat, Rotation, Rx, Ry, Rz, S, Scale, Sdag, Shift, T, Tdag,
+                     Toffoli, X, Y, Z, apply, chain, compile_block, compile_observable, control, dagger,
+                     define_const_gate, dispatch, gatecount, kron, mat, matblock, nparameters, parameters,
+                     pauli_terms, phase, put, repeat, rot, shift)
+from .circuits import heisenberg, variational_circuit
+from .register import (Register, Rng, instruct, measure, measure_collapse, probabilities, product_state, qubit_cap,
+                       rand_state, set_qubit_cap, state_alloc_counter, to_text, zero_state)
+
+
+def set_fusion(enabled: bool) -> None:
+    """Tiled multi-gate passes (default) or one kernel per gate."""
+    lib().qbg_set_fusion(1 if enabled else 0)
+
+
+def synchronize() -> None:
+    from ._capi import check
+    check(lib().qbg_synchronize())

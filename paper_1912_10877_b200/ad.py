@@ -1,0 +1,75 @@
+"""Expectation values and reversible-AD gradients (Yao.AD) on the device.
+
+``expect_grad(obs, (reg, circuit))`` runs forward once, seeds φ̄ = O|ψ⟩ and walks the
+circuit backwards uncomputing ψ and back-propagating φ̄, with at most
+two extra full states live regardless of depth."""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import errors
+from ._capi import check, lib
+from .blocks import Block, apply, compile_block, compile_observable
+from .register import Register
+
+
+@dataclass
+class GradResult:
+    energies: np.ndarray     # per batch <O>
+    param_grads: np.ndarray  # summed over the batch, parameters() order
+    state_grad: Register | None = None  # adjoint of the input state
+
+
+def _pair(reg_or_pair):
+    if isinstance(reg_or_pair, tuple):
+        return reg_or_pair
+    return reg_or_pair, None
+
+
+def expect(obs: Block, reg_or_pair) -> np.ndarray:
+    """expect(O, reg) or expect(O, (reg, circuit)) -> per-batch real <O>."""
+    reg, circuit = _pair(reg_or_pair)
+    if circuit is not None:
+        reg = reg.copy()
+        apply(reg, circuit)
+    o = compile_observable(obs)
+    out = np.empty(reg.nbatch)
+    check(lib().qbg_expect(reg._h, o._h, out.ctypes.data))
+    return out
+
+
+def obs_apply(obs: Block, reg: Register, out: Register | None = None) -> Register:
+    """|out> = O |reg> for a Pauli-sum observable."""
+    o = compile_observable(obs)
+    if out is None:
+        out = Register(reg.nqubits, reg.nbatch, dtype=reg.dtype)
+    check(lib().qbg_obs_apply(reg._h, o._h, out._h))
+    return out
+
+
+def expect_grad(obs: Block, pair, want_state_grad: bool = False, inplace: bool = False) -> GradResult:
+    """expect'(O, reg => circuit).  ``inplace`` runs on ``reg`` itself (it
+    is uncomputed back to the input up to rounding) and saves one full-state copy."""
+    reg, circuit = pair
+    if circuit.nqubits != reg.nactive or obs.nqubits != reg.nactive:
+        raise errors.ShapeError("expect': block qubit count differs from active qubits")
+    p = compile_block(circuit)
+    o = compile_observable(obs)
+    energies = np.empty(reg.nbatch)
+    grads = np.zeros(max(1, p.nparams))
+    sg = Register(reg.nqubits, reg.nbatch, dtype=reg.dtype) if want_state_grad else None
+    check(lib().qbg_expect_grad(reg._h, p._h, o._h, 1 if inplace else 0, energies.ctypes.data, grads.ctypes.data,
+                                sg._h if sg is not None else None))
+    return GradResult(energies, grads[: p.nparams], sg)
+
+
+def backward(psi: Register, adj: Register, circuit: Block, grads: np.ndarray | None = None) -> np.ndarray:
+    """apply_back through a whole circuit: uncomputes psi, back-propagates
+    adj, and adds the parameter gradient into ``grads``."""
+    p = compile_block(circuit)
+    g = np.zeros(max(1, p.nparams)) if grads is None else np.ascontiguousarray(grads, dtype=np.float64)
+    check(lib().qbg_backward(psi._h, adj._h, p._h, g.ctypes.data))
+    return g[: p.nparams]

@@ -1,0 +1,1110 @@
+// capi.cu — the extern "C" boundary (include/qbg.h) over the device engine.
+//
+// Replaces the reference's register "instruction set" (register.hpp:58-493) and the SPEC's
+// apply / expect / expect_grad.  All device work is issued on
+// one stream per process (qbg_set_stream); calls that return host values synchronise it.
+// There is no CPU fallback: without a CUDA device every call fails with QBG_ERR_CUDA.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <numbers>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "engine.h"
+#include "program.h"
+
+// ---- opaque handles ---------------------------------------------------------------------------
+struct qbg_rng {
+    uint64_t state;
+    std::mt19937_64 eng;
+    explicit qbg_rng(uint64_t seed);
+};
+
+struct qbg_reg {
+    qbg::DevState s;
+    int nactive = 0;
+    qbg_rng rng{42};
+    std::vector<std::vector<int32_t>> focus_stack;
+};
+
+struct qbg_prog {
+    qbg::Program p;
+};
+struct qbg_obs {
+    qbg::Observable o;
+};
+
+namespace qbg {
+
+// ---- library state ---------------------------------------------------------------------------
+namespace {
+thread_local std::string g_err;
+std::atomic<int32_t> g_cap{30};
+std::atomic<uint64_t> g_allocs{0};
+std::atomic<uint64_t> g_launches{0};
+cudaStream_t g_stream = nullptr;
+int g_device = 0;
+int g_sms = 0;
+bool g_fusion = true;
+bool g_profile = false;
+
+struct ProfRec {
+    const char* name;
+    cudaEvent_t a, b;
+    double bytes;
+};
+std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_event_pool;
+
+cudaEvent_t get_event() {
+    if (!g_event_pool.empty()) {
+        cudaEvent_t e = g_event_pool.back();
+        g_event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    QBG_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+struct Scratch {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+Scratch g_scratch[16];
+
+uint64_t mix(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return QBG_OK;
+    } catch (const Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return QBG_ERR_RESOURCE;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return QBG_ERR_INTERNAL;
+    }
+}
+
+void ensure_device() {
+    static bool init = false;
+    if (init) return;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+        raise(QBG_ERR_CUDA, std::string("no CUDA device available (") + cudaGetErrorString(e) +
+                                "); the qbg engine has no CPU fallback");
+    QBG_CUDA(cudaSetDevice(g_device));
+    QBG_CUDA(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, g_device));
+    init = true;
+}
+
+void* dev_alloc(size_t bytes, bool state) {
+    ensure_device();
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        raise(QBG_ERR_RESOURCE, "device allocation of " + std::to_string(bytes) + " bytes failed: " +
+                                    cudaGetErrorString(e));
+    }
+    if (state) g_allocs.fetch_add(1);
+    return p;
+}
+
+void stream_sync() { QBG_CUDA(cudaStreamSynchronize(g_stream)); }
+
+qbg_reg* new_reg(int n, int64_t B, int dtype) {
+    if (n < 1) raise(QBG_ERR_VALIDATION, "Register: need at least one qubit");
+    if (n > g_cap.load())
+        raise(QBG_ERR_RESOURCE, "Register: " + std::to_string(n) + " qubits exceeds the cap of " +
+                                    std::to_string(g_cap.load()));
+    if (B < 1) raise(QBG_ERR_VALIDATION, "Register: batch count must be positive");
+    if (dtype != QBG_C128 && dtype != QBG_C64) raise(QBG_ERR_VALIDATION, "Register: unknown dtype");
+    auto* r = new qbg_reg;
+    r->s.n = n;
+    r->s.B = B;
+    r->s.dtype = dtype;
+    r->nactive = n;
+    try {
+        r->s.ptr = dev_alloc(r->s.bytes(), true);
+    } catch (...) {
+        delete r;
+        throw;
+    }
+    return r;
+}
+
+void check_reg(const qbg_reg* r) {
+    if (!r || !r->s.ptr) raise(QBG_ERR_VALIDATION, "null register");
+}
+
+void same_shape(const qbg_reg* a, const qbg_reg* b, const char* what) {
+    check_reg(a);
+    check_reg(b);
+    if (a->s.n != b->s.n || a->s.B != b->s.B || a->s.dtype != b->s.dtype)
+        raise(QBG_ERR_SHAPE, std::string(what) + ": shape mismatch");
+}
+
+// ---- gate table (gates.hpp:32-94) on the host -------------------------------------------
+using cd = std::complex<double>;
+
+struct HostGate {
+    int kind;
+    int dim;
+    std::vector<cd> v;
+    std::vector<int> perm;
+};
+
+HostGate H_diag(std::vector<cd> d) { return HostGate{QBG_MAT_DIAGONAL, static_cast<int>(d.size()), d, {}}; }
+HostGate H_perm(std::vector<int> p, std::vector<cd> v) {
+    return HostGate{QBG_MAT_PERMUTATION, static_cast<int>(p.size()), v, p};
+}
+HostGate H_dense(int dim, std::vector<cd> a) { return HostGate{QBG_MAT_DENSE, dim, a, {}}; }
+
+HostGate gate_by_tag(const std::string& tag, const double* params, int nparams) {
+    const cd i1(0.0, 1.0);
+    if (tag == "Rx" || tag == "Ry" || tag == "Rz" || tag == "shift" || tag == "phase") {
+        if (nparams != 1) raise(QBG_ERR_DISPATCH, "gate " + tag + " expects one parameter");
+        double th = params[0];
+        if (tag == "Rx") {
+            cd c = std::cos(th / 2), ms = -i1 * std::sin(th / 2);
+            return H_dense(2, {c, ms, ms, c});
+        }
+        if (tag == "Ry") {
+            double c = std::cos(th / 2), s = std::sin(th / 2);
+            return H_dense(2, {c, s, -s, c});
+        }
+        if (tag == "Rz") return H_diag({std::polar(1.0, -th / 2), std::polar(1.0, th / 2)});
+        if (tag == "shift") return H_diag({1.0, std::polar(1.0, th)});
+        return H_diag({std::polar(1.0, th), std::polar(1.0, th)});
+    }
+    if (nparams != 0) {
+        static const char* known[] = {"X",  "Y",    "Z",  "H",  "I2", "S",  "Sdag", "T",  "Tdag",
+                                      "SWAP", "CNOT", "CZ", "Toffoli", "P0", "P1", "Pu", "Pd"};
+        for (auto* k : known)
+            if (tag == k) raise(QBG_ERR_DISPATCH, "gate " + tag + " takes no parameters");
+    }
+    double s = 1.0 / std::numbers::sqrt2;
+    if (tag == "X") return H_perm({1, 0}, {1.0, 1.0});
+    if (tag == "Y") return H_perm({1, 0}, {-i1, i1});
+    if (tag == "Z") return H_diag({1.0, -1.0});
+    if (tag == "H") return H_dense(2, {s, s, s, -s});
+    if (tag == "I2") return HostGate{QBG_MAT_IDENTITY, 2, {}, {}};
+    if (tag == "S") return H_diag({1.0, i1});
+    if (tag == "Sdag") return H_diag({1.0, -i1});
+    if (tag == "T") return H_diag({1.0, std::polar(1.0, std::numbers::pi / 4)});
+    if (tag == "Tdag") return H_diag({1.0, std::polar(1.0, -std::numbers::pi / 4)});
+    if (tag == "SWAP") return H_perm({0, 2, 1, 3}, {1.0, 1.0, 1.0, 1.0});
+    if (tag == "CNOT") return H_perm({0, 1, 3, 2}, {1.0, 1.0, 1.0, 1.0});
+    if (tag == "CZ") return H_perm({0, 1, 2, 3}, {1.0, 1.0, 1.0, -1.0});
+    if (tag == "Toffoli") return H_perm({0, 1, 2, 3, 4, 5, 7, 6}, std::vector<cd>(8, 1.0));
+    // projectors (SparseColumns in the reference, densified by its generic path)
+    if (tag == "P0") return H_dense(2, {1.0, 0.0, 0.0, 0.0});
+    if (tag == "P1") return H_dense(2, {0.0, 0.0, 0.0, 1.0});
+    if (tag == "Pu") return H_dense(2, {0.0, 0.0, 1.0, 0.0});
+    if (tag == "Pd") return H_dense(2, {0.0, 1.0, 0.0, 0.0});
+    raise(QBG_ERR_DISPATCH, "unknown gate tag: " + tag);
+}
+
+std::vector<cdbl> to_cdbl(const std::vector<cd>& v) {
+    std::vector<cdbl> o(v.size());
+    for (size_t k = 0; k < v.size(); ++k) o[k] = cdbl{v[k].real(), v[k].imag()};
+    return o;
+}
+
+}  // namespace
+
+// ---- shared helpers used by the other translation units -----------------------------------
+cudaStream_t stream() { return g_stream; }
+int num_sms() {
+    ensure_device();
+    return g_sms;
+}
+
+void* scratch(size_t bytes, int slot) {
+    Scratch& s = g_scratch[slot];
+    if (s.bytes < bytes) {
+        if (s.p) {
+            QBG_CUDA(cudaStreamSynchronize(g_stream));
+            QBG_CUDA(cudaFree(s.p));
+        }
+        s.p = dev_alloc(bytes, false);
+        s.bytes = bytes;
+    }
+    return s.p;
+}
+
+LaunchScope::LaunchScope(const char* n, double b) : name(n), bytes(b) {
+    g_launches.fetch_add(1);
+    if (g_profile) {
+        cudaEvent_t a = get_event();
+        QBG_CUDA(cudaEventRecord(a, g_stream));
+        g_prof.push_back(ProfRec{n, a, nullptr, b});
+    }
+}
+LaunchScope::~LaunchScope() {
+    if (g_profile && !g_prof.empty() && g_prof.back().name == name && g_prof.back().b == nullptr) {
+        cudaEvent_t e = get_event();
+        cudaEventRecord(e, g_stream);
+        g_prof.back().b = e;
+    }
+}
+
+// make_plan's validation order (register.hpp:301-323)
+void validate_op(int nactive, const qbg_op& op) {
+    if (op.ntarget < 1) raise(QBG_ERR_VALIDATION, "instruct: need at least one target qubit");
+    if (op.ntarget > QBG_MAX_TARGETS) raise(QBG_ERR_UNSUPPORTED, "instruct: more than 5 targets");
+    if (op.nctrl < 0 || op.nctrl > QBG_MAX_CTRLS)
+        raise(QBG_ERR_VALIDATION, "instruct: control locations and configuration differ in length");
+    uint64_t lm = 0, cm = 0;
+    for (int k = 0; k < op.ntarget; ++k) {
+        int l = op.targets[k];
+        if (l < 1 || l > nactive) raise(QBG_ERR_RANGE, "instruct: target qubit out of range");
+        uint64_t b = uint64_t{1} << (l - 1);
+        if (lm & b) raise(QBG_ERR_VALIDATION, "instruct: duplicate target qubit");
+        lm |= b;
+    }
+    for (int k = 0; k < op.nctrl; ++k) {
+        int l = op.ctrls[k];
+        if (l < 1 || l > nactive) raise(QBG_ERR_RANGE, "instruct: control qubit out of range");
+        if (op.ctrl_cfg[k] != 0 && op.ctrl_cfg[k] != 1)
+            raise(QBG_ERR_VALIDATION, "instruct: control configuration must be 0 or 1");
+        uint64_t b = uint64_t{1} << (l - 1);
+        if ((lm | cm) & b) raise(QBG_ERR_VALIDATION, "instruct: control qubit overlaps another location");
+        cm |= b;
+    }
+    if (op.dim != (1 << op.ntarget)) raise(QBG_ERR_SHAPE, "instruct: gate dimension does not match target count");
+}
+
+Gate place_gate(const qbg_op& op, int kind, int dim, const std::vector<cdbl>& m, const std::vector<int>& perm) {
+    Gate g;
+    g.kind = kind;
+    g.t = op.ntarget;
+    g.dim = dim;
+    for (int q = 0; q < op.ntarget; ++q) {
+        g.tbit[q] = static_cast<uint8_t>(op.targets[q] - 1);
+        g.tmask |= uint64_t{1} << (op.targets[q] - 1);
+    }
+    for (int k = 0; k < op.nctrl; ++k) {
+        uint64_t b = uint64_t{1} << (op.ctrls[k] - 1);
+        g.cmask |= b;
+        if (op.ctrl_cfg[k]) g.cval |= b;
+    }
+    g.m = m;
+    g.perm = perm;
+    return g;
+}
+
+// rot(G, θ) with the exact arithmetic sequence of gates.hpp:79-92
+void realise(Program& p) {
+    const cd I(0.0, 1.0);
+    p.real.resize(p.ops.size());
+    for (size_t k = 0; k < p.ops.size(); ++k) {
+        const qbg_op& op = p.ops[k];
+        int dim = op.dim;
+        std::vector<cd> pay;
+        std::vector<int> perm;
+        const cdbl* src = p.vals.data() + op.data;
+        if (op.kind == QBG_MAT_DIAGONAL || op.kind == QBG_MAT_PERMUTATION)
+            for (int r = 0; r < dim; ++r) pay.emplace_back(src[r].re, src[r].im);
+        if (op.kind == QBG_MAT_DENSE)
+            for (int r = 0; r < dim * dim; ++r) pay.emplace_back(src[r].re, src[r].im);
+        if (op.kind == QBG_MAT_PERMUTATION)
+            for (int r = 0; r < dim; ++r) perm.push_back(static_cast<int>(p.perms[op.perm + r]));
+        RealOp ro;
+        ro.param = op.gen == QBG_GEN_NONE ? -1 : op.param;
+        if (op.gen == QBG_GEN_NONE) {
+            ro.u = place_gate(op, op.kind, dim, to_cdbl(pay), perm);
+        } else if (op.gen == QBG_GEN_ROTATION) {
+            double th = p.theta[op.param];
+            double c = std::cos(th / 2), s = std::sin(th / 2);
+            if (op.kind == QBG_MAT_IDENTITY || op.kind == QBG_MAT_DIAGONAL) {
+                std::vector<cd> d(dim);
+                for (int r = 0; r < dim; ++r) {
+                    cd g = op.kind == QBG_MAT_IDENTITY ? cd(1.0) : pay[r];
+                    d[r] = cd(c) - I * cd(s) * g;
+                }
+                ro.u = place_gate(op, QBG_MAT_DIAGONAL, dim, to_cdbl(d), {});
+                std::vector<cd> kd(dim);
+                for (int r = 0; r < dim; ++r) kd[r] = op.kind == QBG_MAT_IDENTITY ? cd(1.0) : pay[r];
+                ro.k = place_gate(op, QBG_MAT_DIAGONAL, dim, to_cdbl(kd), {});
+            } else {
+                std::vector<cd> dn(static_cast<size_t>(dim) * dim, cd(0.0));
+                if (op.kind == QBG_MAT_PERMUTATION)
+                    for (int r = 0; r < dim; ++r) dn[perm[r] * dim + r] += pay[r];
+                else
+                    dn = pay;
+                std::vector<cd> u = dn;
+                cd f = -I * s;
+                for (auto& e : u) e *= f;
+                for (int r = 0; r < dim; ++r) u[r * dim + r] += c;
+                ro.u = place_gate(op, QBG_MAT_DENSE, dim, to_cdbl(u), {});
+                ro.k = op.kind == QBG_MAT_PERMUTATION ? place_gate(op, QBG_MAT_PERMUTATION, dim, to_cdbl(pay), perm)
+                                                      : place_gate(op, QBG_MAT_DENSE, dim, to_cdbl(dn), {});
+            }
+        } else if (op.gen == QBG_GEN_SHIFT) {
+            double th = p.theta[op.param];
+            ro.u = place_gate(op, QBG_MAT_DIAGONAL, dim, to_cdbl({cd(1.0), std::polar(1.0, th)}), {});
+            ro.k = place_gate(op, QBG_MAT_DIAGONAL, dim, to_cdbl({cd(0.0), cd(-2.0)}), {});
+        } else {
+            double th = p.theta[op.param];
+            ro.u = place_gate(op, QBG_MAT_DIAGONAL, dim, to_cdbl(std::vector<cd>(dim, std::polar(1.0, th))), {});
+            ro.k = place_gate(op, QBG_MAT_DIAGONAL, dim, to_cdbl(std::vector<cd>(dim, cd(-2.0))), {});
+        }
+        ro.udag = adjoint(ro.u);
+        p.real[k] = std::move(ro);
+    }
+    p.realised = true;
+}
+
+namespace {
+
+void run_program(const DevState& s, Program& p, bool adjoint) {
+    if (!p.realised) realise(p);
+    if (g_fusion && fused_forward(s, p, adjoint)) return;
+    size_t N = p.real.size();
+    for (size_t q = 0; q < N; ++q) {
+        size_t k = adjoint ? N - 1 - q : q;
+        launch_gate(s, adjoint ? p.real[k].udag : p.real[k].u);
+    }
+}
+
+void run_obs(const DevState& psi, const DevState& phi, Observable& o, double* d_energy) {
+    if (g_fusion && fused_obs_apply(psi, phi, o, d_energy)) return;
+    if (o.terms.empty()) {
+        QBG_CUDA(cudaMemsetAsync(phi.ptr, 0, phi.bytes(), g_stream));
+    }
+    for (size_t t = 0; t < o.terms.size(); ++t)
+        launch_pauli_axpy(psi, phi, o.terms[t].xmask, o.terms[t].zmask, o.terms[t].coef_re, o.terms[t].coef_im,
+                          t == 0);
+    if (d_energy) {
+        double* ip = static_cast<double*>(scratch(2 * psi.B * sizeof(double), 2));
+        reduce_inner(psi, &phi, ip);
+        // keep only the real parts: energies are read back by the caller from ip
+        QBG_CUDA(cudaMemcpy2DAsync(d_energy, sizeof(double), ip, 2 * sizeof(double), sizeof(double), psi.B,
+                                   cudaMemcpyDeviceToDevice, g_stream));
+    }
+}
+
+// reverse pass; d_grads (device, nparams) receives the accumulated gradient
+void run_backward(const DevState& psi, const DevState& adj, Program& p, double* d_grads) {
+    if (!p.realised) realise(p);
+    if (g_fusion && fused_backward(psi, adj, p, d_grads)) return;
+    size_t N = p.real.size();
+    int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+    int64_t nparam_ops = 0;
+    for (auto& r : p.real) nparam_ops += r.param >= 0;
+    double* part = static_cast<double*>(scratch(std::max<int64_t>(1, nparam_ops) * cap * sizeof(double), 3));
+    QBG_CUDA(cudaMemsetAsync(part, 0, std::max<int64_t>(1, nparam_ops) * cap * sizeof(double), g_stream));
+    std::vector<int> slot_param;
+    for (size_t q = 0; q < N; ++q) {
+        size_t k = N - 1 - q;
+        const RealOp& r = p.real[k];
+        int used = 0;
+        if (r.param >= 0) {
+            launch_gate_back(psi, adj, r.udag, &r.k, part + slot_param.size() * cap, cap, &used);
+            slot_param.push_back(r.param);
+        } else {
+            launch_gate_back(psi, adj, r.udag, nullptr, nullptr, cap, &used);
+        }
+    }
+    if (slot_param.empty()) return;
+    int* dmap = static_cast<int*>(scratch(slot_param.size() * sizeof(int), 4));
+    QBG_CUDA(cudaMemcpyAsync(dmap, slot_param.data(), slot_param.size() * sizeof(int), cudaMemcpyHostToDevice,
+                             g_stream));
+    accumulate_grads(part, static_cast<int64_t>(slot_param.size()), cap, dmap, d_grads);
+    stream_sync();  // slot_param (host) must outlive the async copy
+}
+
+}  // namespace
+}  // namespace qbg
+
+using namespace qbg;
+
+qbg_rng::qbg_rng(uint64_t seed) : state(qbg::mix(seed)), eng(qbg::mix(seed)) {}
+
+extern "C" {
+
+const char* qbg_last_error(void) { return g_err.c_str(); }
+const char* qbg_version(void) { return "qbg 0.1 (sm_100a)"; }
+
+int qbg_set_qubit_cap(int32_t cap) {
+    return guarded([&] {
+        if (cap < 1 || cap > 62) raise(QBG_ERR_VALIDATION, "qubit cap must be in 1..62");
+        g_cap.store(cap);
+    });
+}
+int32_t qbg_get_qubit_cap(void) { return g_cap.load(); }
+uint64_t qbg_alloc_count(void) { return g_allocs.load(); }
+
+int qbg_set_device(int32_t device) {
+    return guarded([&] {
+        g_device = device;
+        QBG_CUDA(cudaSetDevice(device));
+        QBG_CUDA(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, device));
+    });
+}
+int qbg_set_stream(void* s) {
+    g_stream = static_cast<cudaStream_t>(s);
+    return QBG_OK;
+}
+int qbg_synchronize(void) {
+    return guarded([&] {
+        ensure_device();
+        stream_sync();
+    });
+}
+int qbg_set_fusion(int32_t on) {
+    g_fusion = on != 0;
+    return QBG_OK;
+}
+int qbg_profile_enable(int32_t on) {
+    g_profile = on != 0;
+    return QBG_OK;
+}
+int qbg_profile_reset(void) {
+    return guarded([&] {
+        for (auto& r : g_prof) {
+            g_event_pool.push_back(r.a);
+            if (r.b) g_event_pool.push_back(r.b);
+        }
+        g_prof.clear();
+    });
+}
+int qbg_profile_report(char* buf, int64_t cap) {
+    return guarded([&] {
+        stream_sync();
+        struct Agg {
+            int64_t n = 0;
+            double ms = 0, bytes = 0;
+        };
+        std::map<std::string, Agg> agg;
+        for (auto& r : g_prof) {
+            if (!r.b) continue;
+            float ms = 0;
+            QBG_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+            auto& a = agg[r.name];
+            a.n++;
+            a.ms += ms;
+            a.bytes += r.bytes;
+        }
+        std::string out;
+        char line[256];
+        for (auto& [k, a] : agg) {
+            std::snprintf(line, sizeof(line), "%s\t%lld\t%.6f\t%.6e\n", k.c_str(), static_cast<long long>(a.n), a.ms,
+                          a.bytes);
+            out += line;
+        }
+        if (cap > 0) {
+            std::strncpy(buf, out.c_str(), static_cast<size_t>(cap - 1));
+            buf[cap - 1] = 0;
+        }
+    });
+}
+uint64_t qbg_launch_count(void) { return g_launches.load(); }
+int qbg_launch_count_reset(void) {
+    g_launches.store(0);
+    return QBG_OK;
+}
+
+// ---- rng ---------------------------------------------------------------------------------------
+int qbg_rng_create(uint64_t seed, qbg_rng** out) {
+    return guarded([&] { *out = new qbg_rng(seed); });
+}
+int qbg_rng_destroy(qbg_rng* r) {
+    delete r;
+    return QBG_OK;
+}
+int qbg_rng_split_label(const qbg_rng* r, const char* label, qbg_rng** out) {
+    return guarded([&] {
+        uint64_t h = r->state;
+        for (const char* c = label; *c; ++c) h = mix(h ^ static_cast<uint64_t>(static_cast<unsigned char>(*c)));
+        *out = new qbg_rng(h);
+    });
+}
+int qbg_rng_split_salt(const qbg_rng* r, uint64_t salt, qbg_rng** out) {
+    return guarded([&] { *out = new qbg_rng(mix(r->state ^ salt)); });
+}
+double qbg_rng_uniform(qbg_rng* r) { return std::uniform_real_distribution<double>(0.0, 1.0)(r->eng); }
+double qbg_rng_uniform_range(qbg_rng* r, double lo, double hi) {
+    return std::uniform_real_distribution<double>(lo, hi)(r->eng);
+}
+double qbg_rng_gauss(qbg_rng* r) { return std::normal_distribution<double>(0.0, 1.0)(r->eng); }
+uint64_t qbg_rng_bits(qbg_rng* r) { return r->eng(); }
+
+// ---- registers ----------------------------------------------------------------------------------
+int qbg_reg_create(int32_t nqubits, int64_t nbatch, int32_t dtype, uint64_t seed, qbg_reg** out) {
+    return guarded([&] {
+        qbg_reg* r = new_reg(nqubits, nbatch, dtype);
+        r->rng = qbg_rng(seed);
+        QBG_CUDA(cudaMemsetAsync(r->s.ptr, 0, r->s.bytes(), g_stream));
+        *out = r;
+    });
+}
+int qbg_reg_destroy(qbg_reg* r) {
+    return guarded([&] {
+        if (!r) return;
+        if (r->s.ptr) {
+            QBG_CUDA(cudaStreamSynchronize(g_stream));
+            QBG_CUDA(cudaFree(r->s.ptr));
+        }
+        delete r;
+    });
+}
+int qbg_reg_clone(const qbg_reg* src, qbg_reg** out) {
+    return guarded([&] {
+        check_reg(src);
+        qbg_reg* r = new_reg(src->s.n, src->s.B, src->s.dtype);
+        r->nactive = src->nactive;
+        r->rng = src->rng;
+        r->focus_stack = src->focus_stack;
+        QBG_CUDA(cudaMemcpyAsync(r->s.ptr, src->s.ptr, src->s.bytes(), cudaMemcpyDeviceToDevice, g_stream));
+        *out = r;
+    });
+}
+int qbg_reg_copy(qbg_reg* dst, const qbg_reg* src) {
+    return guarded([&] {
+        same_shape(dst, src, "Register::operator=");
+        if (dst == src) return;
+        dst->nactive = src->nactive;
+        dst->rng = src->rng;
+        dst->focus_stack = src->focus_stack;
+        QBG_CUDA(cudaMemcpyAsync(dst->s.ptr, src->s.ptr, src->s.bytes(), cudaMemcpyDeviceToDevice, g_stream));
+    });
+}
+int qbg_reg_info(const qbg_reg* r, int32_t* nq, int32_t* na, int64_t* nb, int32_t* dt) {
+    return guarded([&] {
+        check_reg(r);
+        if (nq) *nq = r->s.n;
+        if (na) *na = r->nactive;
+        if (nb) *nb = r->s.B;
+        if (dt) *dt = r->s.dtype;
+    });
+}
+void* qbg_reg_device_ptr(qbg_reg* r) { return r ? r->s.ptr : nullptr; }
+qbg_rng* qbg_reg_rng(qbg_reg* r) { return r ? &r->rng : nullptr; }
+
+int qbg_set_zero(qbg_reg* r) {
+    uint64_t z = 0;
+    return qbg_set_product(r, &z, 1);
+}
+int qbg_set_product(qbg_reg* r, const uint64_t* bits, int64_t nbits) {
+    return guarded([&] {
+        check_reg(r);
+        if (nbits != 1 && nbits != r->s.B) raise(QBG_ERR_SHAPE, "product_state: one basis index per batch");
+        for (int64_t k = 0; k < nbits; ++k)
+            if (bits[k] >> r->s.n) raise(QBG_ERR_VALIDATION, "BitStr value does not fit in the register");
+        uint64_t* d = static_cast<uint64_t*>(scratch(nbits * sizeof(uint64_t), 5));
+        QBG_CUDA(cudaMemcpyAsync(d, bits, nbits * sizeof(uint64_t), cudaMemcpyHostToDevice, g_stream));
+        launch_set_basis(r->s, d, nbits);
+    });
+}
+int qbg_set_rand(qbg_reg* r, uint64_t seed) {
+    return guarded([&] {
+        check_reg(r);
+        // rand_state, register.hpp:266-280: host Gaussians from Rng(seed).split("rand_state")
+        qbg_rng root(seed);
+        uint64_t h = root.state;
+        for (const char* c = "rand_state"; *c; ++c) h = mix(h ^ static_cast<uint64_t>(static_cast<unsigned char>(*c)));
+        qbg_rng g(h);
+        uint64_t len = r->s.rows();
+        std::vector<std::complex<double>> host(len * r->s.B);
+        for (int64_t b = 0; b < r->s.B; ++b) {
+            auto* sl = host.data() + b * len;
+            double nrm2 = 0.0;
+            for (uint64_t i = 0; i < len; ++i) {
+                double im = std::normal_distribution<double>(0.0, 1.0)(g.eng);  // g++ evaluates right to left
+                double re = std::normal_distribution<double>(0.0, 1.0)(g.eng);
+                sl[i] = std::complex<double>(re, im);
+                nrm2 += std::norm(sl[i]);
+            }
+            double inv = 1.0 / std::sqrt(nrm2);
+            for (uint64_t i = 0; i < len; ++i) sl[i] *= inv;
+        }
+        int rc = qbg_upload(r, reinterpret_cast<const double*>(host.data()), static_cast<int64_t>(host.size()));
+        if (rc) raise(rc, g_err);
+        stream_sync();
+    });
+}
+
+int qbg_upload(qbg_reg* r, const double* host, int64_t n) {
+    return guarded([&] {
+        check_reg(r);
+        if (static_cast<uint64_t>(n) != r->s.count()) raise(QBG_ERR_SHAPE, "upload: element count mismatch");
+        if (r->s.dtype == QBG_C64) {
+            std::vector<float> f(2 * n);
+            for (int64_t k = 0; k < 2 * n; ++k) f[k] = static_cast<float>(host[k]);
+            if (r->s.B == 1) {
+                QBG_CUDA(cudaMemcpyAsync(r->s.ptr, f.data(), r->s.bytes(), cudaMemcpyHostToDevice, g_stream));
+            } else {
+                void* tmp = scratch(r->s.bytes(), 6);
+                QBG_CUDA(cudaMemcpyAsync(tmp, f.data(), r->s.bytes(), cudaMemcpyHostToDevice, g_stream));
+                launch_transpose(tmp, r->s.ptr, r->s.rows(), r->s.B, r->s.dtype, true);
+            }
+            stream_sync();
+            return;
+        }
+        if (r->s.B == 1) {
+            QBG_CUDA(cudaMemcpyAsync(r->s.ptr, host, r->s.bytes(), cudaMemcpyHostToDevice, g_stream));
+        } else {
+            void* tmp = scratch(r->s.bytes(), 6);
+            QBG_CUDA(cudaMemcpyAsync(tmp, host, r->s.bytes(), cudaMemcpyHostToDevice, g_stream));
+            launch_transpose(tmp, r->s.ptr, r->s.rows(), r->s.B, r->s.dtype, true);
+        }
+    });
+}
+int qbg_download(const qbg_reg* r, double* host, int64_t n) {
+    return guarded([&] {
+        check_reg(r);
+        if (static_cast<uint64_t>(n) != r->s.count()) raise(QBG_ERR_SHAPE, "download: element count mismatch");
+        const void* src = r->s.ptr;
+        if (r->s.B != 1) {
+            void* tmp = scratch(r->s.bytes(), 6);
+            launch_transpose(r->s.ptr, tmp, r->s.rows(), r->s.B, r->s.dtype, false);
+            src = tmp;
+        }
+        if (r->s.dtype == QBG_C64) {
+            std::vector<float> f(2 * n);
+            QBG_CUDA(cudaMemcpyAsync(f.data(), src, r->s.bytes(), cudaMemcpyDeviceToHost, g_stream));
+            stream_sync();
+            for (int64_t k = 0; k < 2 * n; ++k) host[k] = f[k];
+            return;
+        }
+        QBG_CUDA(cudaMemcpyAsync(host, src, r->s.bytes(), cudaMemcpyDeviceToHost, g_stream));
+        stream_sync();
+    });
+}
+int qbg_upload_raw(qbg_reg* r, const void* host, int64_t nbytes) {
+    return guarded([&] {
+        check_reg(r);
+        if (static_cast<size_t>(nbytes) != r->s.bytes()) raise(QBG_ERR_SHAPE, "upload_raw: byte count mismatch");
+        QBG_CUDA(cudaMemcpyAsync(r->s.ptr, host, nbytes, cudaMemcpyHostToDevice, g_stream));
+    });
+}
+int qbg_download_raw(const qbg_reg* r, void* host, int64_t nbytes) {
+    return guarded([&] {
+        check_reg(r);
+        if (static_cast<size_t>(nbytes) != r->s.bytes()) raise(QBG_ERR_SHAPE, "download_raw: byte count mismatch");
+        QBG_CUDA(cudaMemcpyAsync(host, r->s.ptr, nbytes, cudaMemcpyDeviceToHost, g_stream));
+        stream_sync();
+    });
+}
+
+// ---- instruct -------------------------------------------------------------------------------------
+int qbg_instruct(qbg_reg* r, const qbg_matrix* gate, const int32_t* locs, int32_t nloc, const int32_t* ctrl_locs,
+                 const int32_t* ctrl_cfg, int32_t nctrl) {
+    return guarded([&] {
+        check_reg(r);
+        qbg_op op{};
+        op.kind = gate->kind;
+        op.ntarget = nloc;
+        op.nctrl = nctrl;
+        op.dim = gate->dim;
+        if (nloc < 1) raise(QBG_ERR_VALIDATION, "instruct: need at least one target qubit");
+        if (nloc > QBG_MAX_TARGETS) raise(QBG_ERR_UNSUPPORTED, "instruct: more than 5 targets");
+        if (nctrl > QBG_MAX_CTRLS) raise(QBG_ERR_UNSUPPORTED, "instruct: too many controls");
+        for (int k = 0; k < nloc; ++k) op.targets[k] = locs[k];
+        for (int k = 0; k < nctrl; ++k) {
+            op.ctrls[k] = ctrl_locs[k];
+            op.ctrl_cfg[k] = ctrl_cfg[k];
+        }
+        validate_op(r->nactive, op);
+        std::vector<cdbl> m;
+        std::vector<int> perm;
+        int d = gate->dim;
+        const cdbl* v = reinterpret_cast<const cdbl*>(gate->vals);
+        if (gate->kind == QBG_MAT_IDENTITY) return;
+        if (gate->kind == QBG_MAT_DIAGONAL || gate->kind == QBG_MAT_PERMUTATION) m.assign(v, v + d);
+        else if (gate->kind == QBG_MAT_DENSE) m.assign(v, v + static_cast<size_t>(d) * d);
+        else raise(QBG_ERR_VALIDATION, "instruct: unknown matrix class");
+        if (gate->kind == QBG_MAT_PERMUTATION) {
+            std::vector<char> seen(d, 0);
+            for (int k = 0; k < d; ++k) {
+                if (gate->perm[k] < 0 || gate->perm[k] >= d || seen[gate->perm[k]])
+                    raise(QBG_ERR_VALIDATION, "Permutation: column indices must form a permutation");
+                seen[gate->perm[k]] = 1;
+                perm.push_back(static_cast<int>(gate->perm[k]));
+            }
+        }
+        launch_gate(r->s, place_gate(op, gate->kind, d, m, perm));
+    });
+}
+
+int qbg_instruct_tag(qbg_reg* r, const char* tag, const int32_t* locs, int32_t nloc, const int32_t* ctrl_locs,
+                     const int32_t* ctrl_cfg, int32_t nctrl, const double* params, int32_t nparams) {
+    return guarded([&] {
+        HostGate hg = gate_by_tag(tag, params, nparams);
+        std::vector<int64_t> perm(hg.perm.begin(), hg.perm.end());
+        qbg_matrix m{hg.kind, hg.dim, reinterpret_cast<const double*>(hg.v.data()), perm.data()};
+        int rc = qbg_instruct(r, &m, locs, nloc, ctrl_locs, ctrl_cfg, nctrl);
+        if (rc) raise(rc, g_err);
+    });
+}
+
+// ---- algebra -------------------------------------------------------------------------------------
+int qbg_norm(const qbg_reg* r, double* out) {
+    return guarded([&] {
+        check_reg(r);
+        double* d = static_cast<double*>(scratch(2 * r->s.B * sizeof(double), 2));
+        reduce_inner(r->s, nullptr, d);
+        std::vector<double> h(2 * r->s.B);
+        QBG_CUDA(cudaMemcpyAsync(h.data(), d, h.size() * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        stream_sync();
+        for (int64_t b = 0; b < r->s.B; ++b) out[b] = std::sqrt(h[2 * b]);
+    });
+}
+int qbg_inner(const qbg_reg* a, const qbg_reg* b, double* out) {
+    return guarded([&] {
+        same_shape(a, b, "Register::inner");
+        double* d = static_cast<double*>(scratch(2 * a->s.B * sizeof(double), 2));
+        reduce_inner(a->s, &b->s, d);
+        QBG_CUDA(cudaMemcpyAsync(out, d, 2 * a->s.B * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        stream_sync();
+    });
+}
+int qbg_scale(qbg_reg* r, double re, double im) {
+    return guarded([&] {
+        check_reg(r);
+        launch_scale(r->s, re, im);
+    });
+}
+int qbg_add_scaled(qbg_reg* r, const qbg_reg* o, double re, double im) {
+    return guarded([&] {
+        same_shape(r, o, "Register::add_scaled");
+        launch_axpy(r->s, o->s, re, im);
+    });
+}
+
+// ---- measurement (register.hpp:414-493) ----------------------------------------------------------
+namespace {
+std::vector<double> probs(const qbg_reg* r, int64_t b) {
+    uint64_t ra = uint64_t{1} << r->nactive;
+    double* d = static_cast<double*>(scratch(ra * sizeof(double), 8));
+    launch_probabilities(r->s, r->nactive, b, d);
+    std::vector<double> p(ra);
+    QBG_CUDA(cudaMemcpyAsync(p.data(), d, ra * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+    stream_sync();
+    return p;
+}
+// the reference's sequential prefix sum (register.hpp:444-449) and upper_bound (428-432)
+uint64_t sample(const std::vector<double>& cum, double u) {
+    auto it = std::upper_bound(cum.begin(), cum.end(), u * cum.back());
+    uint64_t idx = static_cast<uint64_t>(it - cum.begin());
+    return idx < cum.size() ? idx : cum.size() - 1;
+}
+}  // namespace
+
+int qbg_probabilities(const qbg_reg* r, int64_t b, double* out) {
+    return guarded([&] {
+        check_reg(r);
+        if (b < 0 || b >= r->s.B) raise(QBG_ERR_RANGE, "probabilities: batch out of range");
+        auto p = probs(r, b);
+        std::copy(p.begin(), p.end(), out);
+    });
+}
+int qbg_measure(const qbg_reg* r, int64_t nshots, qbg_rng* rng, uint64_t* out) {
+    return guarded([&] {
+        check_reg(r);
+        if (nshots < 1) raise(QBG_ERR_VALIDATION, "measure: nshots must be positive");
+        qbg_rng* g = rng ? rng : const_cast<qbg_rng*>(&r->rng);
+        for (int64_t b = 0; b < r->s.B; ++b) {
+            auto p = probs(r, b);
+            std::vector<double> cum(p.size());
+            double acc = 0.0;
+            for (size_t i = 0; i < p.size(); ++i) {
+                acc += p[i];
+                cum[i] = acc;
+            }
+            for (int64_t s = 0; s < nshots; ++s) out[b * nshots + s] = sample(cum, qbg_rng_uniform(g));
+        }
+    });
+}
+int qbg_measure_collapse(qbg_reg* r, qbg_rng* rng, uint64_t* out) {
+    return guarded([&] {
+        check_reg(r);
+        qbg_rng* g = rng ? rng : &r->rng;
+        for (int64_t b = 0; b < r->s.B; ++b) {
+            auto p = probs(r, b);
+            std::vector<double> cum(p.size());
+            double acc = 0.0;
+            for (size_t i = 0; i < p.size(); ++i) {
+                acc += p[i];
+                cum[i] = acc;
+            }
+            uint64_t hit = sample(cum, qbg_rng_uniform(g));
+            double prob = p[hit];
+            if (prob <= 1e-300)
+                raise(QBG_ERR_RENORMALIZATION, "measure!: outcome has numerically zero probability");
+            launch_collapse(r->s, r->nactive, b, hit, 1.0 / std::sqrt(prob));
+            out[b] = hit;
+        }
+        stream_sync();
+    });
+}
+
+// ---- focus / relax (register.hpp:156-177, 209-248) ----------------------------------------------------
+namespace {
+std::vector<int> focus_src(const qbg_reg* r, const int32_t* locs, int32_t nloc) {
+    if (nloc < 1) raise(QBG_ERR_VALIDATION, "focus: need at least one location");
+    std::vector<char> used(r->s.n, 0);
+    std::vector<int> src;
+    for (int k = 0; k < nloc; ++k) {
+        if (locs[k] < 1 || locs[k] > r->s.n) raise(QBG_ERR_RANGE, "focus: location out of range");
+        if (used[locs[k] - 1]) raise(QBG_ERR_VALIDATION, "focus: duplicate location");
+        used[locs[k] - 1] = 1;
+        src.push_back(locs[k] - 1);
+    }
+    for (int q = 0; q < r->s.n; ++q)
+        if (!used[q]) src.push_back(q);
+    return src;
+}
+// new bit k takes old bit src[k]; launch with new_of_old[src[k]] = k
+void permute(qbg_reg* r, const std::vector<int>& src) {
+    bool ident = true;
+    for (size_t k = 0; k < src.size(); ++k) ident &= src[k] == static_cast<int>(k);
+    if (ident) return;
+    std::vector<int> new_of_old(src.size());
+    for (size_t k = 0; k < src.size(); ++k) new_of_old[src[k]] = static_cast<int>(k);
+    DevState tmp = r->s;
+    tmp.ptr = scratch(r->s.bytes(), 6);
+    launch_permute_bits(r->s, tmp, new_of_old.data());
+    QBG_CUDA(cudaMemcpyAsync(r->s.ptr, tmp.ptr, r->s.bytes(), cudaMemcpyDeviceToDevice, g_stream));
+}
+}  // namespace
+
+int qbg_focus(qbg_reg* r, const int32_t* locs, int32_t nloc) {
+    return guarded([&] {
+        check_reg(r);
+        auto src = focus_src(r, locs, nloc);
+        permute(r, src);
+        r->focus_stack.emplace_back(locs, locs + nloc);
+        r->nactive = nloc;
+    });
+}
+int qbg_relax(qbg_reg* r, const int32_t* locs, int32_t nloc, int32_t to_nactive) {
+    return guarded([&] {
+        check_reg(r);
+        if (r->focus_stack.empty()) raise(QBG_ERR_VALIDATION, "relax: no focus to undo");
+        const auto& top = r->focus_stack.back();
+        if (!std::equal(top.begin(), top.end(), locs, locs + nloc))
+            raise(QBG_ERR_VALIDATION, "relax: locations do not match the previous focus");
+        if (to_nactive > r->s.n) raise(QBG_ERR_VALIDATION, "relax: to_nactive exceeds qubit count");
+        auto src = focus_src(r, locs, nloc);
+        std::vector<int> inv(src.size());
+        for (size_t k = 0; k < src.size(); ++k) inv[src[k]] = static_cast<int>(k);
+        permute(r, inv);
+        r->focus_stack.pop_back();
+        r->nactive = to_nactive;
+    });
+}
+
+// ---- programs -----------------------------------------------------------------------------------------
+int qbg_prog_create(int32_t n, const qbg_op* ops, int64_t nops, const double* vals, int64_t nvals,
+                    const int64_t* perms, int64_t nperms, qbg_prog** out) {
+    return guarded([&] {
+        if (n < 1 || n > 62) raise(QBG_ERR_VALIDATION, "program: qubit count out of range");
+        auto* p = new qbg_prog;
+        try {
+            p->p.n = n;
+            p->p.ops.assign(ops, ops + nops);
+            const cdbl* v = reinterpret_cast<const cdbl*>(vals);
+            p->p.vals.assign(v, v + nvals);
+            p->p.perms.assign(perms, perms + nperms);
+            int64_t np = 0;
+            for (auto& op : p->p.ops) {
+                validate_op(n, op);
+                if (op.gen != QBG_GEN_NONE) {
+                    if (op.param < 0) raise(QBG_ERR_VALIDATION, "program: parameterised op without a slot");
+                    np = std::max<int64_t>(np, op.param + 1);
+                    if (op.gen == QBG_GEN_SHIFT && op.dim != 2) raise(QBG_ERR_SHAPE, "shift acts on one qubit");
+                }
+                int64_t need = op.kind == QBG_MAT_DENSE ? int64_t{op.dim} * op.dim
+                               : (op.kind == QBG_MAT_IDENTITY || op.gen == QBG_GEN_SHIFT || op.gen == QBG_GEN_PHASE)
+                                   ? 0
+                                   : op.dim;
+                if (need && (op.data < 0 || op.data + need > nvals)) raise(QBG_ERR_SHAPE, "program: payload out of range");
+                if (op.kind == QBG_MAT_PERMUTATION && op.gen != QBG_GEN_SHIFT && op.gen != QBG_GEN_PHASE) {
+                    if (op.perm < 0 || op.perm + op.dim > nperms) raise(QBG_ERR_SHAPE, "program: permutation out of range");
+                    std::vector<char> seen(op.dim, 0);
+                    for (int k = 0; k < op.dim; ++k) {
+                        int64_t c = perms[op.perm + k];
+                        if (c < 0 || c >= op.dim || seen[c])
+                            raise(QBG_ERR_VALIDATION, "Permutation: column indices must form a permutation");
+                        seen[c] = 1;
+                    }
+                }
+            }
+            p->p.nparams = np;
+            p->p.theta.assign(np, 0.0);
+            realise(p->p);
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        *out = p;
+    });
+}
+int qbg_prog_destroy(qbg_prog* p) {
+    delete p;
+    return QBG_OK;
+}
+int64_t qbg_prog_nparams(const qbg_prog* p) { return p ? p->p.nparams : -1; }
+int qbg_prog_set_params(qbg_prog* p, const double* theta, int64_t n) {
+    return guarded([&] {
+        if (n != p->p.nparams) raise(QBG_ERR_VALIDATION, "dispatch: parameter count mismatch");
+        p->p.theta.assign(theta, theta + n);
+        realise(p->p);
+        p->p.version++;
+    });
+}
+int qbg_prog_stats(const qbg_prog* prog, int64_t* fwd, int64_t* bwd, int64_t* gates) {
+    return guarded([&] {
+        int64_t f = 0, b = 0;
+        fused_stats(prog->p, &f, &b);
+        if (fwd) *fwd = f;
+        if (bwd) *bwd = b;
+        if (gates) *gates = static_cast<int64_t>(prog->p.ops.size());
+    });
+}
+int qbg_apply(qbg_reg* r, const qbg_prog* prog) {
+    return guarded([&] {
+        check_reg(r);
+        if (prog->p.n != r->nactive) raise(QBG_ERR_SHAPE, "apply: block qubit count differs from active qubits");
+        run_program(r->s, const_cast<qbg_prog*>(prog)->p, false);
+    });
+}
+int qbg_apply_adjoint(qbg_reg* r, const qbg_prog* prog) {
+    return guarded([&] {
+        check_reg(r);
+        if (prog->p.n != r->nactive) raise(QBG_ERR_SHAPE, "apply: block qubit count differs from active qubits");
+        run_program(r->s, const_cast<qbg_prog*>(prog)->p, true);
+    });
+}
+
+// ---- observables / AD ---------------------------------------------------------------------------------
+int qbg_obs_create(int32_t n, const qbg_pauli_term* terms, int64_t nterms, qbg_obs** out) {
+    return guarded([&] {
+        auto* o = new qbg_obs;
+        o->o.n = n;
+        uint64_t full = n >= 64 ? ~uint64_t{0} : (uint64_t{1} << n) - 1;
+        for (int64_t t = 0; t < nterms; ++t) {
+            qbg_pauli_term q = terms[t];
+            if ((q.xmask | q.zmask) & ~full) {
+                delete o;
+                raise(QBG_ERR_RANGE, "observable: Pauli factor outside the register");
+            }
+            // fold i^{nY} (Y = i X Z) into the coefficient exactly
+            int ny = __builtin_popcountll(q.xmask & q.zmask) & 3;
+            double re = q.coef_re, im = q.coef_im;
+            for (int k = 0; k < ny; ++k) {
+                double t2 = re;
+                re = -im;
+                im = t2;
+            }
+            q.coef_re = re;
+            q.coef_im = im;
+            o->o.terms.push_back(q);
+        }
+        *out = o;
+    });
+}
+int qbg_obs_destroy(qbg_obs* o) {
+    delete o;
+    return QBG_OK;
+}
+int qbg_obs_apply(const qbg_reg* r, const qbg_obs* o, qbg_reg* out) {
+    return guarded([&] {
+        same_shape(r, out, "obs_apply");
+        if (o->o.n != r->nactive) raise(QBG_ERR_SHAPE, "observable qubit count differs from active qubits");
+        run_obs(r->s, out->s, const_cast<qbg_obs*>(o)->o, nullptr);
+    });
+}
+int qbg_expect(const qbg_reg* r, const qbg_obs* o, double* out) {
+    return guarded([&] {
+        check_reg(r);
+        if (o->o.n != r->nactive) raise(QBG_ERR_SHAPE, "observable qubit count differs from active qubits");
+        DevState phi = r->s;
+        phi.ptr = scratch(r->s.bytes(), 9);
+        double* e = static_cast<double*>(scratch(r->s.B * sizeof(double), 10));
+        run_obs(r->s, phi, const_cast<qbg_obs*>(o)->o, e);
+        QBG_CUDA(cudaMemcpyAsync(out, e, r->s.B * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        stream_sync();
+    });
+}
+int qbg_backward(qbg_reg* psi, qbg_reg* adj, const qbg_prog* prog, double* grads) {
+    return guarded([&] {
+        same_shape(psi, adj, "backward");
+        auto& p = const_cast<qbg_prog*>(prog)->p;
+        if (p.n != psi->nactive) raise(QBG_ERR_SHAPE, "backward: block qubit count differs from active qubits");
+        double* dg = static_cast<double*>(scratch(std::max<int64_t>(1, p.nparams) * sizeof(double), 11));
+        QBG_CUDA(cudaMemcpyAsync(dg, grads, p.nparams * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+        run_backward(psi->s, adj->s, p, dg);
+        QBG_CUDA(cudaMemcpyAsync(grads, dg, p.nparams * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        stream_sync();
+    });
+}
+int qbg_expect_grad(qbg_reg* r, const qbg_prog* prog, const qbg_obs* o, int32_t inplace, double* energies,
+                    double* grads, qbg_reg* state_grad) {
+    return guarded([&] {
+        check_reg(r);
+        auto& p = const_cast<qbg_prog*>(prog)->p;
+        auto& ob = const_cast<qbg_obs*>(o)->o;
+        if (p.n != r->nactive || ob.n != r->nactive)
+            raise(QBG_ERR_SHAPE, "expect': block qubit count differs from active qubits");
+        if (state_grad) same_shape(r, state_grad, "expect' state_grad");
+        // live full states: psi (the register itself when inplace) + adjoint (<= 4)
+        static thread_local DevState work{}, adjbuf{};
+        auto ensure = [&](DevState& d) {
+            if (d.ptr && d.bytes() >= r->s.bytes() && d.dtype == r->s.dtype) return;
+            if (d.ptr) {
+                stream_sync();
+                QBG_CUDA(cudaFree(d.ptr));
+            }
+            d = r->s;
+            d.ptr = dev_alloc(r->s.bytes(), true);
+        };
+        DevState psi = r->s;
+        if (!inplace) {
+            ensure(work);
+            psi.ptr = work.ptr;
+            QBG_CUDA(cudaMemcpyAsync(psi.ptr, r->s.ptr, r->s.bytes(), cudaMemcpyDeviceToDevice, g_stream));
+        }
+        DevState adj = r->s;
+        if (state_grad) {
+            adj.ptr = state_grad->s.ptr;
+        } else {
+            ensure(adjbuf);
+            adj.ptr = adjbuf.ptr;
+        }
+        run_program(psi, p, false);
+        double* e = static_cast<double*>(scratch(r->s.B * sizeof(double), 10));
+        run_obs(psi, adj, ob, e);
+        double* dg = static_cast<double*>(scratch(std::max<int64_t>(1, p.nparams) * sizeof(double), 11));
+        QBG_CUDA(cudaMemsetAsync(dg, 0, std::max<int64_t>(1, p.nparams) * sizeof(double), g_stream));
+        run_backward(psi, adj, p, dg);
+        QBG_CUDA(cudaMemcpyAsync(energies, e, r->s.B * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        QBG_CUDA(cudaMemcpyAsync(grads, dg, p.nparams * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        stream_sync();
+    });
+}
+
+}  // extern "C"

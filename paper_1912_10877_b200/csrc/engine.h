@@ -1,0 +1,67 @@
+// engine.h — host-side interfaces of the device engine (kernels live in *.cu).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace qbg {
+
+// A device state vector: 2^n rows of B batch-innermost complex amplitudes.
+struct DevState {
+    void* ptr = nullptr;
+    int n = 0;
+    int64_t B = 1;
+    int dtype = QBG_C128;
+    size_t elem() const { return dtype == QBG_C128 ? 16 : 8; }
+    uint64_t rows() const { return uint64_t{1} << n; }
+    uint64_t count() const { return rows() * static_cast<uint64_t>(B); }
+    size_t bytes() const { return static_cast<size_t>(count()) * elem(); }
+};
+
+// A realised gate placed on 0-based bit positions (register.hpp:292-339 KernelPlan).
+struct Gate {
+    int kind = QBG_MAT_IDENTITY;  // QBG_MAT_*
+    int t = 0;                    // number of targets
+    int dim = 0;                  // 2^t
+    uint8_t tbit[QBG_MAX_TARGETS] = {0};  // matrix qubit q acts on bit tbit[q]
+    uint64_t tmask = 0, cmask = 0, cval = 0;
+    std::vector<cdbl> m;     // DIAGONAL/PERMUTATION: dim; DENSE: dim*dim column-major
+    std::vector<int> perm;   // PERMUTATION: row k takes column perm[k]
+};
+
+Gate adjoint(const Gate& g);      // matrix.hpp:594-643
+bool is_diagonal(const Gate& g);  // IDENTITY or DIAGONAL
+
+// ---- generic per-gate kernels (register.hpp:352-385 on the device) --------------------
+void launch_gate(const DevState& s, const Gate& g);
+// Reverse step of one gate on (psi, adj): grad_slot (if >= 0) receives, per block, the
+// partial Im <adj| K |psi> (K restricted to the control subspace) BEFORE the uncompute;
+// then psi <- U^† psi, adj <- U^† adj with U^† = gdag.
+void launch_gate_back(const DevState& psi, const DevState& adj, const Gate& gdag, const Gate* K,
+                      double* partials, int64_t nblocks_cap, int* nblocks_used);
+
+// ---- reductions (register.hpp:120-150), deterministic two-level trees ------------------
+// out[2*b], out[2*b+1] = <a_b|c_b> (c == nullptr: a := c, i.e. squared norm in .re)
+void reduce_inner(const DevState& a, const DevState* c, double* d_out /* device, 2*B */);
+void sum_partials(const double* d_part, int64_t nrows, int64_t ncols, double* d_out);
+// part is [nslots][cap]; grads[slot_param[s]] += sum_b part[s][b], slots in order
+void accumulate_grads(const double* d_part, int64_t nslots, int64_t cap, const int* d_slot_param, double* d_grads);
+
+// ---- elementwise -------------------------------------------------------------------------
+void launch_scale(const DevState& s, double re, double im);
+void launch_axpy(const DevState& y, const DevState& x, double re, double im);
+void launch_set_basis(const DevState& s, const uint64_t* d_bits, int64_t nbits);
+void launch_transpose(const void* src, void* dst, uint64_t rows, int64_t B, int dtype, bool to_device_layout);
+void launch_pauli_axpy(const DevState& psi, const DevState& phi, uint64_t xmask, uint64_t zmask, double cre,
+                       double cim, bool overwrite);
+void launch_permute_bits(const DevState& src, const DevState& dst, const int* new_of_old);
+void launch_probabilities(const DevState& s, int nactive, int64_t batch, double* d_p);
+void launch_collapse(const DevState& s, int nactive, int64_t batch, uint64_t hit, double inv);
+
+// scratch device memory owned by the library (grows; stream-ordered reuse)
+void* scratch(size_t bytes, int slot);
+
+}  // namespace qbg

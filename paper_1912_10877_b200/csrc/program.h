@@ -1,0 +1,51 @@
+// program.h — compiled gate programs and observables (host side).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "engine.h"
+
+namespace qbg {
+
+struct FusedPlan;  // fused.cu
+
+// Realised instruction: U, U^† and the gradient generator K with θ̄ = Im <φ̄|K|ψ_{k+1}>
+// on the control subspace (rotation: K = G; shift: K = −2 P1; phase: K = −2 I).
+struct RealOp {
+    Gate u, udag, k;
+    int param = -1;
+};
+
+struct Program {
+    int n = 0;
+    std::vector<qbg_op> ops;
+    std::vector<cdbl> vals;
+    std::vector<int64_t> perms;
+    int64_t nparams = 0;
+    std::vector<double> theta;
+    std::vector<RealOp> real;  // realised at theta
+    bool realised = false;
+    // fused plans cached per (B, dtype); rebuilt on structural change only
+    std::vector<std::shared_ptr<FusedPlan>> plans;
+    uint64_t version = 0;  // bumps on set_params
+};
+
+struct Observable {
+    int n = 0;
+    std::vector<qbg_pauli_term> terms;  // coefficient already multiplied by i^{nY}
+    std::vector<std::shared_ptr<FusedPlan>> plans;
+};
+
+void validate_op(int nactive, const qbg_op& op);  // make_plan checks, register.hpp:299-339
+Gate place_gate(const qbg_op& op, int kind, int dim, const std::vector<cdbl>& m, const std::vector<int>& perm);
+void realise(Program& p);
+
+// fused engine (fused.cu); return false when the plan does not apply (caller falls back)
+bool fused_forward(const DevState& s, Program& p, bool adjoint);
+bool fused_backward(const DevState& psi, const DevState& adj, Program& p, double* d_grads /* nparams, += */);
+bool fused_obs_apply(const DevState& psi, const DevState& phi, Observable& o, double* d_energy /* B or null */);
+// passes of the most recently built forward / backward plans (0 when unfused)
+void fused_stats(const Program& p, int64_t* fwd, int64_t* bwd);
+
+}  // namespace qbg
