@@ -21,7 +21,11 @@
 #include <map>
 #include <memory>
 
+#include <sstream>
+
 #include "fused.h"
+#include "jit.h"
+#include "fused_kernels.h"
 #include "program.h"
 
 namespace qbg {
@@ -31,676 +35,6 @@ using namespace fz;
 // =====================================================================================
 // device side
 // =====================================================================================
-namespace {
-
-constexpr int kMaxOps = 256;    // ops per pass (smem resident)
-constexpr int kMaxMats = 512;   // complex matrix entries per pass (smem resident)
-constexpr int kMaxComps = 256;  // gradient components per pass
-
-template <typename V>
-__device__ __forceinline__ V ld_mat(const cdbl* m, int i) {
-    return from_cd<V>(m[i]);
-}
-
-template <typename V>
-__device__ __forceinline__ double im_conj_mul(V a, V b) {  // Im(conj(a) * b)
-    return static_cast<double>(a.x) * b.y - static_cast<double>(a.y) * b.x;
-}
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-// ---- register-slot gate kernels ---------------------------------------------------------
-// CHECK = false: no control on register slots (the common case: no per-pair predicate)
-template <typename V, int RB, int K, bool CHECK>
-__device__ __forceinline__ void dense1_k(V* x, V m00, V m10, V m01, V m11, int cm, int cv) {
-#pragma unroll
-    for (int j = 0; j < (1 << RB); ++j) {
-        if (j & (1 << K)) continue;
-        if (CHECK && (j & cm) != cv) continue;
-        V a = x[j], b = x[j | (1 << K)];
-        x[j] = cfma(cmul(m00, a), m01, b);
-        x[j | (1 << K)] = cfma(cmul(m10, a), m11, b);
-    }
-}
-
-template <typename V, int RB, int K, bool CHECK>
-__device__ __forceinline__ void swap1_k(V* x, int cm, int cv) {
-#pragma unroll
-    for (int j = 0; j < (1 << RB); ++j) {
-        if (j & (1 << K)) continue;
-        if (CHECK && (j & cm) != cv) continue;
-        V a = x[j];
-        x[j] = x[j | (1 << K)];
-        x[j | (1 << K)] = a;
-    }
-}
-
-// swap on slot K controlled by slot C == CV (all compile time: pure register moves)
-template <typename V, int RB, int K, int C, int CV>
-__device__ __forceinline__ void cswap1_k(V* x) {
-#pragma unroll
-    for (int j = 0; j < (1 << RB); ++j) {
-        if (j & (1 << K)) continue;
-        if (((j >> C) & 1) != CV) continue;
-        V a = x[j];
-        x[j] = x[j | (1 << K)];
-        x[j | (1 << K)] = a;
-    }
-}
-
-template <typename V, int RB, int K, bool CHECK>
-__device__ __forceinline__ void diag1_k(V* x, V d0, V d1, int cm, int cv) {
-#pragma unroll
-    for (int j = 0; j < (1 << RB); ++j) {
-        if (CHECK && (j & cm) != cv) continue;
-        x[j] = cmul(x[j], (j & (1 << K)) ? d1 : d0);
-    }
-}
-
-template <typename V, int RB, int K0, int K1>
-__device__ __forceinline__ void dense2_k(V* x, const cdbl* m, int cm, int cv) {
-#pragma unroll
-    for (int j = 0; j < (1 << RB); ++j) {
-        if (j & ((1 << K0) | (1 << K1))) continue;
-        if ((j & cm) != cv) continue;
-        const int i0 = j, i1 = j | (1 << K0), i2 = j | (1 << K1), i3 = j | (1 << K0) | (1 << K1);
-        V a0 = x[i0], a1 = x[i1], a2 = x[i2], a3 = x[i3];
-        V r[4];
-#pragma unroll
-        for (int rr = 0; rr < 4; ++rr) {
-            V acc = cmul(ld_mat<V>(m, rr), a0);
-            acc = cfma(acc, ld_mat<V>(m, 4 + rr), a1);
-            acc = cfma(acc, ld_mat<V>(m, 8 + rr), a2);
-            r[rr] = cfma(acc, ld_mat<V>(m, 12 + rr), a3);
-        }
-        x[i0] = r[0];
-        x[i1] = r[1];
-        x[i2] = r[2];
-        x[i3] = r[3];
-    }
-}
-
-// gradient terms: Σ Im(conj(adj) * (K psi)) over the thread's elements
-template <typename V, int RB, int K>
-__device__ __forceinline__ double gdense1_k(const V* p, const V* a, V k00, V k10, V k01, V k11, int cm, int cv) {
-    double g = 0.0;
-#pragma unroll
-    for (int j = 0; j < (1 << RB); ++j) {
-        if (j & (1 << K)) continue;
-        if ((j & cm) != cv) continue;
-        V p0 = p[j], p1 = p[j | (1 << K)];
-        g += im_conj_mul(a[j], cfma(cmul(k00, p0), k01, p1));
-        g += im_conj_mul(a[j | (1 << K)], cfma(cmul(k10, p0), k11, p1));
-    }
-    return g;
-}
-
-template <typename V, int RB, int K>
-__device__ __forceinline__ double gdiag1_k(const V* p, const V* a, V d0, V d1, int cm, int cv) {
-    double g = 0.0;
-#pragma unroll
-    for (int j = 0; j < (1 << RB); ++j) {
-        if ((j & cm) != cv) continue;
-        g += im_conj_mul(a[j], cmul((j & (1 << K)) ? d1 : d0, p[j]));
-    }
-    return g;
-}
-
-template <typename V, int RB, int K0, int K1>
-__device__ __forceinline__ double gdense2_k(const V* p, const V* a, const cdbl* m, int cm, int cv) {
-    double g = 0.0;
-#pragma unroll
-    for (int j = 0; j < (1 << RB); ++j) {
-        if (j & ((1 << K0) | (1 << K1))) continue;
-        if ((j & cm) != cv) continue;
-        const int idx[4] = {j, j | (1 << K0), j | (1 << K1), j | (1 << K0) | (1 << K1)};
-#pragma unroll
-        for (int rr = 0; rr < 4; ++rr) {
-            V acc = cmul(ld_mat<V>(m, rr), p[idx[0]]);
-            acc = cfma(acc, ld_mat<V>(m, 4 + rr), p[idx[1]]);
-            acc = cfma(acc, ld_mat<V>(m, 8 + rr), p[idx[2]]);
-            acc = cfma(acc, ld_mat<V>(m, 12 + rr), p[idx[3]]);
-            g += im_conj_mul(a[idx[rr]], acc);
-        }
-    }
-    return g;
-}
-
-// C_ab = Σ conj(adj_a) psi_b over pairs on slot K: c[2*(2a+b)] = Re, c[2*(2a+b)+1] = Im
-template <typename V, int RB, int K>
-__device__ __forceinline__ void gcross1_k(const V* p, const V* a, double* c) {
-#pragma unroll
-    for (int j = 0; j < (1 << RB); ++j) {
-        if (j & (1 << K)) continue;
-        const V av[2] = {a[j], a[j | (1 << K)]};
-        const V pv[2] = {p[j], p[j | (1 << K)]};
-#pragma unroll
-        for (int x = 0; x < 2; ++x)
-#pragma unroll
-            for (int y = 0; y < 2; ++y) {
-                c[2 * (2 * x + y)] += static_cast<double>(av[x].x) * pv[y].x + static_cast<double>(av[x].y) * pv[y].y;
-                c[2 * (2 * x + y) + 1] += static_cast<double>(av[x].x) * pv[y].y - static_cast<double>(av[x].y) * pv[y].x;
-            }
-    }
-}
-
-// Reduce 8 per-lane values over the warp by halving exchanges (9 double shuffles instead of
-// 40); returns the full sum of component (lane >> 2) in lanes with lane % 4 == 0.
-__device__ __forceinline__ double warp_sum8(double* v, int lane) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const bool hi = lane & 16;
-        double send = hi ? v[k] : v[k + 4];
-        double keep = hi ? v[k + 4] : v[k];
-        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const bool hi = lane & 8;
-        double send = hi ? v[k] : v[k + 2];
-        double keep = hi ? v[k + 2] : v[k];
-        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-    {
-        const bool hi = lane & 4;
-        double send = hi ? v[0] : v[1];
-        double keep = hi ? v[1] : v[0];
-        v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-    double s = v[0];
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    return s;
-}
-
-// runtime slot -> compile-time slot
-#define QBG_SLOT_SWITCH(slot, RB, CALL)                         \
-    switch (slot) {                                             \
-        case 0: CALL(0); break;                                 \
-        case 1: if constexpr (RB > 1) { CALL(1); } break;        \
-        case 2: if constexpr (RB > 2) { CALL(2); } break;        \
-        case 3: if constexpr (RB > 3) { CALL(3); } break;        \
-        case 4: if constexpr (RB > 4) { CALL(4); } break;        \
-        default: break;                                         \
-    }
-
-template <typename V, int RB>
-__device__ __forceinline__ void dense2_dispatch(V* x, int a, int b, const cdbl* m, int cm, int cv) {
-#define QBG_D2(A, B_)                                                                  \
-    if constexpr (A < RB && B_ < RB && A != B_) {                                      \
-        if (a == A && b == B_) { dense2_k<V, RB, A, B_>(x, m, cm, cv); return; }       \
-    }
-    QBG_D2(0, 1) QBG_D2(1, 0) QBG_D2(0, 2) QBG_D2(2, 0) QBG_D2(1, 2) QBG_D2(2, 1)
-    QBG_D2(0, 3) QBG_D2(3, 0) QBG_D2(1, 3) QBG_D2(3, 1) QBG_D2(2, 3) QBG_D2(3, 2)
-    QBG_D2(0, 4) QBG_D2(4, 0) QBG_D2(1, 4) QBG_D2(4, 1) QBG_D2(2, 4) QBG_D2(4, 2) QBG_D2(3, 4) QBG_D2(4, 3)
-#undef QBG_D2
-}
-
-template <typename V, int RB>
-__device__ __forceinline__ double gdense2_dispatch(const V* p, const V* q, int a, int b, const cdbl* m, int cm, int cv) {
-#define QBG_G2(A, B_)                                                              \
-    if constexpr (A < RB && B_ < RB && A != B_) {                                  \
-        if (a == A && b == B_) return gdense2_k<V, RB, A, B_>(p, q, m, cm, cv);    \
-    }
-    QBG_G2(0, 1) QBG_G2(1, 0) QBG_G2(0, 2) QBG_G2(2, 0) QBG_G2(1, 2) QBG_G2(2, 1)
-    QBG_G2(0, 3) QBG_G2(3, 0) QBG_G2(1, 3) QBG_G2(3, 1) QBG_G2(2, 3) QBG_G2(3, 2)
-    QBG_G2(0, 4) QBG_G2(4, 0) QBG_G2(1, 4) QBG_G2(4, 1) QBG_G2(2, 4) QBG_G2(4, 2) QBG_G2(3, 4) QBG_G2(4, 3)
-#undef QBG_G2
-    return 0.0;
-}
-
-// controlled swap with one control on a register slot (CNOT with both ends in registers)
-template <typename V, int RB>
-__device__ __forceinline__ bool cswap_dispatch(V* x, int k, int c, int cv) {
-#define QBG_CS(K, C)                                                                   \
-    if constexpr (K < RB && C < RB && K != C) {                                        \
-        if (k == K && c == C) {                                                        \
-            if (cv) cswap1_k<V, RB, K, C, 1>(x); else cswap1_k<V, RB, K, C, 0>(x);     \
-            return true;                                                               \
-        }                                                                              \
-    }
-    QBG_CS(0, 1) QBG_CS(1, 0) QBG_CS(0, 2) QBG_CS(2, 0) QBG_CS(1, 2) QBG_CS(2, 1)
-    QBG_CS(0, 3) QBG_CS(3, 0) QBG_CS(1, 3) QBG_CS(3, 1) QBG_CS(2, 3) QBG_CS(3, 2)
-    QBG_CS(0, 4) QBG_CS(4, 0) QBG_CS(1, 4) QBG_CS(4, 1) QBG_CS(2, 4) QBG_CS(4, 2) QBG_CS(3, 4) QBG_CS(4, 3)
-#undef QBG_CS
-    return false;
-}
-
-// index of the DIAGK entry for register element j
-__device__ __forceinline__ int diagk_index(const DOp& op, int j, int tid, uint64_t outer) {
-    int idx = 0;
-    for (int q = 0; q < op.t; ++q) {
-        uint32_t loc = static_cast<uint32_t>((op.aux >> (8 * q)) & 0xff);
-        uint32_t ty = loc >> 6, pos = loc & 63;
-        int bit = ty == LOC_REG ? ((j >> pos) & 1) : ty == LOC_THR ? ((tid >> pos) & 1) : static_cast<int>((outer >> pos) & 1);
-        idx |= bit << q;
-    }
-    return idx;
-}
-
-template <typename V, int RB, bool BACK>
-__device__ __forceinline__ void run_ops(V* x, V* y, const DOp* ops, int b0, int b1, const cdbl* mats, int tid,
-                                        uint64_t outer, double* sg, int nw) {
-    constexpr int R = 1 << RB;
-    const int warp = tid >> 5, lane = tid & 31;
-    for (int i = b0; i < b1; ++i) {
-        const DOp& op = ops[i];
-        const bool ok = ((outer & op.ctile_mask) == op.ctile_val) && ((static_cast<uint32_t>(tid) & op.cthr_mask) == op.cthr_val);
-        const int cm = op.creg_mask, cv = op.creg_val;
-        const cdbl* m = mats + op.mat;
-        switch (op.code) {
-            case OP_DENSE1: {
-                if (!ok) break;
-                V m00 = ld_mat<V>(m, 0), m10 = ld_mat<V>(m, 1), m01 = ld_mat<V>(m, 2), m11 = ld_mat<V>(m, 3);
-                if (cm == 0) {
-#define QBG_C(K)                                                  \
-    dense1_k<V, RB, K, false>(x, m00, m10, m01, m11, 0, 0);       \
-    if constexpr (BACK) dense1_k<V, RB, K, false>(y, m00, m10, m01, m11, 0, 0);
-                    QBG_SLOT_SWITCH(op.a, RB, QBG_C)
-#undef QBG_C
-                } else {
-#define QBG_C(K)                                                  \
-    dense1_k<V, RB, K, true>(x, m00, m10, m01, m11, cm, cv);      \
-    if constexpr (BACK) dense1_k<V, RB, K, true>(y, m00, m10, m01, m11, cm, cv);
-                    QBG_SLOT_SWITCH(op.a, RB, QBG_C)
-#undef QBG_C
-                }
-                break;
-            }
-            case OP_X1: {
-                if (!ok) break;
-                if (cm == 0) {
-#define QBG_C(K)                                  \
-    swap1_k<V, RB, K, false>(x, 0, 0);            \
-    if constexpr (BACK) swap1_k<V, RB, K, false>(y, 0, 0);
-                    QBG_SLOT_SWITCH(op.a, RB, QBG_C)
-#undef QBG_C
-                } else if (__popc(cm) == 1) {
-                    const int c = __ffs(cm) - 1;
-                    cswap_dispatch<V, RB>(x, op.a, c, cv != 0);
-                    if constexpr (BACK) cswap_dispatch<V, RB>(y, op.a, c, cv != 0);
-                } else {
-#define QBG_C(K)                                  \
-    swap1_k<V, RB, K, true>(x, cm, cv);           \
-    if constexpr (BACK) swap1_k<V, RB, K, true>(y, cm, cv);
-                    QBG_SLOT_SWITCH(op.a, RB, QBG_C)
-#undef QBG_C
-                }
-                break;
-            }
-            case OP_PERM1: {
-                if (!ok) break;
-                // y0 = v0 x[p0], y1 = v1 x[p1]: a swap (b = 1) followed by a diagonal
-                if (op.b) {
-#define QBG_C(K)                                  \
-    swap1_k<V, RB, K, true>(x, cm, cv);           \
-    if constexpr (BACK) swap1_k<V, RB, K, true>(y, cm, cv);
-                    QBG_SLOT_SWITCH(op.a, RB, QBG_C)
-#undef QBG_C
-                }
-                V d0 = ld_mat<V>(m, 0), d1 = ld_mat<V>(m, 1);
-#define QBG_C(K)                                          \
-    diag1_k<V, RB, K, true>(x, d0, d1, cm, cv);           \
-    if constexpr (BACK) diag1_k<V, RB, K, true>(y, d0, d1, cm, cv);
-                QBG_SLOT_SWITCH(op.a, RB, QBG_C)
-#undef QBG_C
-                break;
-            }
-            case OP_DIAG1R: {
-                if (!ok) break;
-                V d0 = ld_mat<V>(m, 0), d1 = ld_mat<V>(m, 1);
-                if (cm == 0) {
-#define QBG_C(K)                                          \
-    diag1_k<V, RB, K, false>(x, d0, d1, 0, 0);            \
-    if constexpr (BACK) diag1_k<V, RB, K, false>(y, d0, d1, 0, 0);
-                    QBG_SLOT_SWITCH(op.a, RB, QBG_C)
-#undef QBG_C
-                } else {
-#define QBG_C(K)                                          \
-    diag1_k<V, RB, K, true>(x, d0, d1, cm, cv);           \
-    if constexpr (BACK) diag1_k<V, RB, K, true>(y, d0, d1, cm, cv);
-                    QBG_SLOT_SWITCH(op.a, RB, QBG_C)
-#undef QBG_C
-                }
-                break;
-            }
-            case OP_DIAG1T:
-            case OP_DIAG1G: {
-                if (!ok) break;
-                int bit = op.code == OP_DIAG1T ? ((tid >> op.a) & 1) : static_cast<int>((outer >> op.a) & 1);
-                V d = ld_mat<V>(m, bit);
-#pragma unroll
-                for (int j = 0; j < R; ++j) {
-                    if ((j & cm) != cv) continue;
-                    x[j] = cmul(x[j], d);
-                    if constexpr (BACK) y[j] = cmul(y[j], d);
-                }
-                break;
-            }
-            case OP_DENSE2: {
-                if (!ok) break;
-                dense2_dispatch<V, RB>(x, op.a, op.b, m, cm, cv);
-                if constexpr (BACK) dense2_dispatch<V, RB>(y, op.a, op.b, m, cm, cv);
-                break;
-            }
-            case OP_DIAGK: {
-                if (!ok) break;
-#pragma unroll
-                for (int j = 0; j < R; ++j) {
-                    if ((j & cm) != cv) continue;
-                    V d = ld_mat<V>(m, diagk_index(op, j, tid, outer));
-                    x[j] = cmul(x[j], d);
-                    if constexpr (BACK) y[j] = cmul(y[j], d);
-                }
-                break;
-            }
-            case G_CROSS1: {
-                if constexpr (BACK) {
-                    double c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                    if (ok) {
-#define QBG_C(K) gcross1_k<V, RB, K>(x, y, c);
-                        QBG_SLOT_SWITCH(op.a, RB, QBG_C)
-#undef QBG_C
-                    }
-                    double s = warp_sum8(c, lane);
-                    if ((lane & 3) == 0) sg[(op.gslot + (lane >> 2)) * nw + warp] += s;
-                }
-                break;
-            }
-            default: {
-                if constexpr (BACK) {
-                    double g = 0.0;
-                    if (ok) {
-                        if (op.code == G_DENSE1) {
-                            V k00 = ld_mat<V>(m, 0), k10 = ld_mat<V>(m, 1), k01 = ld_mat<V>(m, 2), k11 = ld_mat<V>(m, 3);
-#define QBG_C(K) g = gdense1_k<V, RB, K>(x, y, k00, k10, k01, k11, cm, cv);
-                            QBG_SLOT_SWITCH(op.a, RB, QBG_C)
-#undef QBG_C
-                        } else if (op.code == G_DIAG1R) {
-                            V d0 = ld_mat<V>(m, 0), d1 = ld_mat<V>(m, 1);
-#define QBG_C(K) g = gdiag1_k<V, RB, K>(x, y, d0, d1, cm, cv);
-                            QBG_SLOT_SWITCH(op.a, RB, QBG_C)
-#undef QBG_C
-                        } else if (op.code == G_DIAG1U) {
-                            int bit = op.b == 0 ? ((tid >> op.a) & 1) : static_cast<int>((outer >> op.a) & 1);
-                            V d = ld_mat<V>(m, bit);
-                            double sr = 0.0, si = 0.0;  // Σ conj(adj) psi
-#pragma unroll
-                            for (int j = 0; j < R; ++j) {
-                                if ((j & cm) != cv) continue;
-                                sr += static_cast<double>(y[j].x) * x[j].x + static_cast<double>(y[j].y) * x[j].y;
-                                si += static_cast<double>(y[j].x) * x[j].y - static_cast<double>(y[j].y) * x[j].x;
-                            }
-                            g = static_cast<double>(d.x) * si + static_cast<double>(d.y) * sr;
-                        } else if (op.code == G_DENSE2) {
-                            g = gdense2_dispatch<V, RB>(x, y, op.a, op.b, m, cm, cv);
-                        } else if (op.code == G_DIAGK) {
-#pragma unroll
-                            for (int j = 0; j < R; ++j) {
-                                if ((j & cm) != cv) continue;
-                                V d = ld_mat<V>(m, diagk_index(op, j, tid, outer));
-                                g += im_conj_mul(y[j], cmul(d, x[j]));
-                            }
-                        }
-                    }
-                    g = warp_sum(g);
-                    if (lane == 0) sg[op.gslot * nw + warp] += g;
-                }
-                break;
-            }
-        }
-    }
-}
-
-template <int W>
-__device__ __forceinline__ uint32_t sm_thr(const DStage& S, int tid) {
-    uint32_t o = 0;
-#pragma unroll
-    for (int p = 0; p < W; ++p)
-        if ((tid >> p) & 1) o ^= S.sthr[p];
-    return o;
-}
-template <int RB>
-__device__ __forceinline__ uint32_t sm_reg(const DStage& S, int j) {
-    uint32_t o = 0;
-#pragma unroll
-    for (int k = 0; k < RB; ++k)
-        if ((j >> k) & 1) o ^= S.sreg[k];
-    return o;
-}
-template <int W>
-__device__ __forceinline__ int64_t g_thr(const DStage& S, int tid) {
-    int64_t o = 0;
-#pragma unroll
-    for (int p = 0; p < W; ++p)
-        if ((tid >> p) & 1) o += S.gthr[p];
-    return o;
-}
-template <int RB>
-__device__ __forceinline__ int64_t g_reg(const DStage& S, int j) {
-    int64_t o = 0;
-#pragma unroll
-    for (int k = 0; k < RB; ++k)
-        if ((j >> k) & 1) o += S.greg[k];
-    return o;
-}
-
-template <typename V, int M, bool BACK>
-constexpr size_t fused_smem_bytes(int ncomps_cells) {
-    return (BACK ? 2 : 1) * (sizeof(V) << M) + static_cast<size_t>(ncomps_cells) * 8 + kMaxOps * sizeof(DOp) +
-           kMaxMats * sizeof(cdbl);
-}
-
-// One pass over the whole state: grid-stride over tiles.
-template <typename V, int M, int RB, bool BACK>
-__global__ void __launch_bounds__(1 << (M - RB), 2)
-    k_fused(V* __restrict__ psi, V* __restrict__ adj, const __grid_constant__ DPass P, const DOp* __restrict__ gops,
-            const cdbl* __restrict__ gmats, double* __restrict__ gpart, int64_t gcols) {
-    constexpr int R = 1 << RB, W = M - RB, T = 1 << W, NW = T / 32;
-    extern __shared__ __align__(16) unsigned char smraw[];
-    V* sx = reinterpret_cast<V*>(smraw);
-    V* sy = sx + (1 << M);
-    unsigned char* p = smraw + (BACK ? 2 : 1) * (sizeof(V) << M);
-    DOp* sops = reinterpret_cast<DOp*>(p);
-    p += kMaxOps * sizeof(DOp);
-    cdbl* smats = reinterpret_cast<cdbl*>(p);
-    p += kMaxMats * sizeof(cdbl);
-    double* sg = reinterpret_cast<double*>(p);
-    const int tid = threadIdx.x;
-    {
-        const int4* src = reinterpret_cast<const int4*>(gops + P.op_base);
-        int4* dst = reinterpret_cast<int4*>(sops);
-        for (int i = tid; i < P.nops * 3; i += T) dst[i] = src[i];
-        for (int i = tid; i < P.nmats; i += T) smats[i] = gmats[P.mat_base + i];
-        if constexpr (BACK)
-            for (int i = tid; i < P.ngrad * NW; i += T) sg[i] = 0.0;
-        __syncthreads();
-    }
-    V x[R], y[BACK ? R : 1];
-    const int64_t bc = int64_t{1} << P.nb;
-    for (uint64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x) {
-        const uint64_t o = tile / static_cast<uint64_t>(P.nchunks);
-        const uint64_t c = tile - o * static_cast<uint64_t>(P.nchunks);
-        const uint64_t outer = deposit_zeros(o, P.qpos, P.mq);
-        const int64_t tbase = static_cast<int64_t>(outer) * P.B + static_cast<int64_t>(c) * bc;
-        {
-            const DStage& S = P.st[0];
-            const int64_t gt = tbase + g_thr<W>(S, tid);
-#pragma unroll
-            for (int j = 0; j < R; ++j) {
-                const int64_t e = gt + g_reg<RB>(S, j);
-                x[j] = psi[e];
-                if constexpr (BACK) y[j] = adj[e];
-            }
-        }
-        for (int s = 0; s < P.nstages; ++s) {
-            const DStage& S = P.st[s];
-            if (s > 0) {
-                const DStage& Sp = P.st[s - 1];
-                const uint32_t tp = sm_thr<W>(Sp, tid);
-#pragma unroll
-                for (int j = 0; j < R; ++j) {
-                    const uint32_t a = tp ^ sm_reg<RB>(Sp, j);
-                    sx[a] = x[j];
-                    if constexpr (BACK) sy[a] = y[j];
-                }
-                __syncthreads();
-                const uint32_t tc = sm_thr<W>(S, tid);
-#pragma unroll
-                for (int j = 0; j < R; ++j) {
-                    const uint32_t a = tc ^ sm_reg<RB>(S, j);
-                    x[j] = sx[a];
-                    if constexpr (BACK) y[j] = sy[a];
-                }
-                __syncthreads();
-            }
-            run_ops<V, RB, BACK>(x, BACK ? y : nullptr, sops, S.op_begin, S.op_end, smats, tid, outer, sg, NW);
-        }
-        {
-            const DStage& S = P.st[P.nstages - 1];
-            const int64_t gt = tbase + g_thr<W>(S, tid);
-#pragma unroll
-            for (int j = 0; j < R; ++j) {
-                const int64_t e = gt + g_reg<RB>(S, j);
-                psi[e] = x[j];
-                if constexpr (BACK) adj[e] = y[j];
-            }
-        }
-    }
-    if constexpr (BACK) {
-        __syncthreads();
-        for (int sl = tid; sl < P.ngrad; sl += T) {
-            double s = 0.0;
-            for (int w = 0; w < NW; ++w) s += sg[sl * NW + w];
-            gpart[static_cast<int64_t>(P.grad_base + sl) * gcols + blockIdx.x] = s;
-        }
-    }
-}
-
-// ---- gradient epilogue: partial rows -> parameter gradients (fixed order) ----------------------
-struct GradEntry {
-    int32_t type;  // 0 scalar component, 1 cross matrix (8 components)
-    int32_t comp;
-    int32_t param;
-    int32_t pad;
-    cdbl A[4];     // column-major 2x2, cross entries only
-};
-
-__global__ void k_grad_epilogue(const double* __restrict__ sums, const GradEntry* __restrict__ e, int64_t n,
-                                double* __restrict__ grads) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    for (int64_t k = 0; k < n; ++k) {
-        const GradEntry& g = e[k];
-        if (g.type == 0) {
-            grads[g.param] += sums[g.comp];
-        } else {
-            // θ̄ = Im Σ_ab A_ab C_ab, C_ab at comp + 2(2a+b)
-            double acc = 0.0;
-            for (int a = 0; a < 2; ++a)
-                for (int b = 0; b < 2; ++b) {
-                    const cdbl A = g.A[b * 2 + a];
-                    const double cr = sums[g.comp + 2 * (2 * a + b)], ci = sums[g.comp + 2 * (2 * a + b) + 1];
-                    acc += A.re * ci + A.im * cr;
-                }
-            grads[g.param] += acc;
-        }
-    }
-}
-
-__global__ void k_rows(const double* __restrict__ part, int64_t nrows, int64_t cols, double* __restrict__ out) {
-    int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (r >= nrows) return;
-    double s = 0.0;
-    for (int64_t b = 0; b < cols; ++b) s += part[r * cols + b];
-    out[r] = s;
-}
-
-// ---- observable seed: phi (+)= Σ_groups Σ_terms c (-1)^{|src & z|} psi[src], src = l ^ xloc ----
-struct SPass {
-    int32_t mq, nb;
-    uint8_t qpos[64];
-    int64_t B, nchunks;
-    uint64_t ntiles;
-    int32_t g0, g1;  // groups of this pass
-    int32_t first, last;
-};
-
-template <typename V, int M>
-__global__ void __launch_bounds__(256)
-    k_seed(const V* __restrict__ psi, V* __restrict__ phi, const __grid_constant__ SPass P,
-           const SGroup* __restrict__ groups, const STerm* __restrict__ terms, double* __restrict__ epart) {
-    extern __shared__ __align__(16) unsigned char smraw[];
-    V* sp = reinterpret_cast<V*>(smraw);
-    constexpr int L = 1 << M;
-    const int T = blockDim.x;
-    const int64_t bc = int64_t{1} << P.nb;
-    __shared__ double red[256];
-    for (uint64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x) {
-        const uint64_t o = tile / static_cast<uint64_t>(P.nchunks);
-        const uint64_t c = tile - o * static_cast<uint64_t>(P.nchunks);
-        const uint64_t outer = deposit_zeros(o, P.qpos, P.mq);
-        const int64_t tbase = static_cast<int64_t>(outer) * P.B + static_cast<int64_t>(c) * bc;
-        auto goff = [&](uint32_t l) -> int64_t {
-            int64_t e = l & (bc - 1);
-            uint32_t q = l >> P.nb;
-            for (int k = 0; q; ++k, q >>= 1)
-                if (q & 1) e += P.B << P.qpos[k];
-            return e;
-        };
-        __syncthreads();
-        for (uint32_t l = threadIdx.x; l < L; l += T) sp[l] = psi[tbase + goff(l)];
-        __syncthreads();
-        double eacc = 0.0;
-        for (uint32_t l = threadIdx.x; l < L; l += T) {
-            const int64_t e = tbase + goff(l);
-            V acc = P.first ? mk<V>(0, 0) : phi[e];
-            for (int gi = P.g0; gi < P.g1; ++gi) {
-                const SGroup g = groups[gi];
-                const uint32_t src = l ^ g.xloc;
-                const V v = sp[src];
-                double cr = 0.0, ci = 0.0;
-                for (int ti = g.term_begin; ti < g.term_end; ++ti) {
-                    const STerm t = terms[ti];
-                    const int par = (__popc(src & t.zloc) + __popcll(outer & t.zout)) & 1;
-                    cr += par ? -t.cre : t.cre;
-                    ci += par ? -t.cim : t.cim;
-                }
-                acc = cfma(acc, mk<V>(cr, ci), v);
-            }
-            phi[e] = acc;
-            if (P.last) {
-                const V pv = sp[l];
-                eacc += static_cast<double>(pv.x) * acc.x + static_cast<double>(pv.y) * acc.y;
-            }
-        }
-        if (P.last) {
-            red[threadIdx.x] = eacc;
-            __syncthreads();
-            if (threadIdx.x < bc) {
-                double s = 0.0;
-                for (int k = threadIdx.x; k < T; k += static_cast<int>(bc)) s += red[k];
-                epart[tile * bc + threadIdx.x] = s;
-            }
-        }
-    }
-}
-
-// E[b] = Σ_{tiles of chunk b/bc} epart[tile][b % bc]
-__global__ void k_energy(const double* __restrict__ epart, uint64_t nouter, int64_t nchunks, int64_t bc, int64_t B,
-                         double* __restrict__ e) {
-    int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (b >= B) return;
-    int64_t c = b / bc, beta = b - c * bc;
-    double s = 0.0;
-    for (uint64_t o = 0; o < nouter; ++o) s += epart[(o * nchunks + c) * bc + beta];
-    e[b] = s;
-}
-
-}  // namespace
 
 // =====================================================================================
 // host side: planner
@@ -830,6 +164,9 @@ struct Step {
     DPass pass;
     int single = -1;
     int single_comp = -1;
+    int jk = -1;                 // specialised kernel (index into the plan's kernel list)
+    std::vector<char> blob;      // its matrix parameter (PM<T, 2*nmats>)
+    size_t smem = 0;
 };
 
 }  // namespace
@@ -844,6 +181,7 @@ struct FusedPlan {
     std::vector<cdbl> mats;
     std::vector<GradEntry> epi;
     int64_t ncomps = 0;
+    std::vector<jit::Kernel> jk;
     DOp* d_ops = nullptr;
     cdbl* d_mats = nullptr;
     GradEntry* d_epi = nullptr;
@@ -1131,7 +469,7 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward) {
                         e.type = 1;
                         e.comp = static_cast<int>(P.grad_base) + ncomp;
                         e.param = rg.param;
-                        std::copy(rg.A, rg.A + 4, e.A);
+                        std::memcpy(e.A, rg.A, sizeof(e.A));
                         pl.epi.push_back(e);
                     }
                     ncomp += 8;
@@ -1228,25 +566,309 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward) {
     }
 }
 
+// ---- code generation: one straight-line kernel per distinct pass structure -----------------------
+std::string hex(uint64_t v) {
+    char b[32];
+    std::snprintf(b, sizeof(b), "0x%llxull", static_cast<unsigned long long>(v));
+    return b;
+}
+
+// Σ over tid bits p of ((tid >> p) & 1) * w[p]  (as a C expression)
+template <class W>
+std::string tid_sum(const W* w, int nbits, bool xr) {
+    std::ostringstream s;
+    bool any = false;
+    for (int p = 0; p < nbits; ++p) {
+        if (w[p] == 0) continue;
+        if (any) s << (xr ? " ^ " : " + ");
+        if (xr)
+            s << "(((tid >> " << p << ") & 1) ? " << static_cast<unsigned long long>(w[p]) << "u : 0u)";
+        else
+            s << "((i64)((tid >> " << p << ") & 1) * " << static_cast<long long>(w[p]) << "ll)";
+        any = true;
+    }
+    if (!any) return xr ? "0u" : "0ll";
+    return s.str();
+}
+
+std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, bool back, bool c128) {
+    const int R = 1 << RB, W = M - RB, TH = 1 << W, NW = TH / 32;
+    const size_t elem = c128 ? 16 : 8;
+    std::ostringstream s;
+    s << "extern \"C\" __global__ void __launch_bounds__(" << TH << ", 2) __NAME__(" << (c128 ? "c128" : "c64")
+      << "* __restrict__ psi, " << (c128 ? "c128" : "c64")
+      << "* __restrict__ adj, double* __restrict__ gpart, long long gcols, int gbase, const __grid_constant__ PM<"
+      << (c128 ? "double" : "float") << ", " << std::max(2, 2 * nmats) << "> pm) {\n";
+    s << "typedef " << (c128 ? "c128" : "c64") << " V;\nconstexpr int R = " << R << ";\nconst int tid = threadIdx.x;\n";
+    s << "#define MV(i) mk<V>(pm.m[2 * (i)], pm.m[2 * (i) + 1])\n";
+    s << "extern __shared__ __align__(16) unsigned char smraw[];\nV* sx = (V*)smraw;\nV* sy = sx + " << (1 << M) << ";\n";
+    if (back) {
+        s << "double* sg = (double*)(smraw + " << 2 * (elem << M) << ");\n";
+        s << "for (int i = tid; i < " << P.ngrad * NW << "; i += " << TH << ") sg[i] = 0.0;\n__syncthreads();\n";
+        s << "const int warp = tid >> 5, lane = tid & 31;\n";
+    }
+    // hoisted thread parts of every stage's offsets
+    const DStage& S0 = P.st[0];
+    const DStage& SL = P.st[P.nstages - 1];
+    s << "const i64 g0 = " << tid_sum(S0.gthr, W, false) << ";\n";
+    s << "const i64 gL = " << tid_sum(SL.gthr, W, false) << ";\n";
+    for (int k = 0; k < P.nstages; ++k) s << "const unsigned st" << k << " = " << tid_sum(P.st[k].sthr, W, true) << ";\n";
+    s << "V x[R];\n" << (back ? "V y[R];\n" : "");
+    s << "for (u64 tile = blockIdx.x; tile < " << P.ntiles << "ull; tile += gridDim.x) {\n";
+    if (P.nchunks == 1)
+        s << "const u64 o = tile; const u64 c = 0;\n";
+    else
+        s << "const u64 o = tile / " << P.nchunks << "ull; const u64 c = tile - o * " << P.nchunks << "ull;\n";
+    s << "u64 outer = o;\n";
+    for (int k = 0; k < P.mq; ++k) {
+        int p = P.qpos[k];
+        s << "outer = ((outer >> " << p << ") << " << p + 1 << ") | (outer & " << hex((uint64_t{1} << p) - 1) << ");\n";
+    }
+    s << "const i64 tb = (i64)outer * " << P.B << "ll + (i64)c * " << (int64_t{1} << P.nb) << "ll;\n";
+    auto goff = [&](const DStage& S, int j) {
+        int64_t o = 0;
+        for (int k = 0; k < RB; ++k)
+            if ((j >> k) & 1) o += S.greg[k];
+        return o;
+    };
+    auto soff = [&](const DStage& S, int j) {
+        uint32_t o = 0;
+        for (int k = 0; k < RB; ++k)
+            if ((j >> k) & 1) o ^= S.sreg[k];
+        return o;
+    };
+    for (int j = 0; j < R; ++j) {
+        s << "x[" << j << "] = psi[tb + g0 + " << goff(S0, j) << "ll];";
+        if (back) s << " y[" << j << "] = adj[tb + g0 + " << goff(S0, j) << "ll];";
+        s << "\n";
+    }
+    for (int st = 0; st < P.nstages; ++st) {
+        const DStage& S = P.st[st];
+        if (st > 0) {
+            const DStage& Sp = P.st[st - 1];
+            for (int j = 0; j < R; ++j) {
+                s << "sx[st" << st - 1 << " ^ " << soff(Sp, j) << "u] = x[" << j << "];";
+                if (back) s << " sy[st" << st - 1 << " ^ " << soff(Sp, j) << "u] = y[" << j << "];";
+                s << "\n";
+            }
+            s << "__syncthreads();\n";
+            for (int j = 0; j < R; ++j) {
+                s << "x[" << j << "] = sx[st" << st << " ^ " << soff(S, j) << "u];";
+                if (back) s << " y[" << j << "] = sy[st" << st << " ^ " << soff(S, j) << "u];";
+                s << "\n";
+            }
+            s << "__syncthreads();\n";
+        }
+        for (int i = S.op_begin; i < S.op_end; ++i) {
+            const DOp& op = ops[i];
+            const int o = op.mat;
+            std::ostringstream ctl;
+            bool has_ctl = false;
+            if (op.cthr_mask) {
+                ctl << "(((unsigned)tid & " << op.cthr_mask << "u) == " << op.cthr_val << "u)";
+                has_ctl = true;
+            }
+            if (op.ctile_mask) {
+                if (has_ctl) ctl << " && ";
+                ctl << "((outer & " << hex(op.ctile_mask) << ") == " << hex(op.ctile_val) << ")";
+                has_ctl = true;
+            }
+            const std::string cond = has_ctl ? ctl.str() : "true";
+            const std::string t5 = std::to_string(op.creg_mask) + ", " + std::to_string(op.creg_val);
+            auto both = [&](const std::string& call_x, const std::string& call_y) {
+                s << call_x;
+                if (back) s << " " << call_y;
+            };
+            auto mvs = [&](int base, int n) {
+                std::ostringstream t;
+                for (int k = 0; k < n; ++k) t << (k ? ", " : "") << "MV(" << base + k << ")";
+                return t.str();
+            };
+            switch (op.code) {
+                case OP_DENSE1: {
+                    s << "if (" << cond << ") { const V m00 = MV(" << o << "), m10 = MV(" << o + 1 << "), m01 = MV(" << o + 2
+                      << "), m11 = MV(" << o + 3 << "); ";
+                    std::string tp = "<V, R, " + std::to_string(op.a) + ", " + t5 + ">";
+                    both("dense1" + tp + "(x, m00, m10, m01, m11);", "dense1" + tp + "(y, m00, m10, m01, m11);");
+                    s << " }\n";
+                    break;
+                }
+                case OP_X1: {
+                    std::string tp = "<V, R, " + std::to_string(op.a) + ", " + t5 + ">";
+                    s << "if (" << cond << ") { ";
+                    both("swap1" + tp + "(x);", "swap1" + tp + "(y);");
+                    s << " }\n";
+                    break;
+                }
+                case OP_PERM1: {
+                    std::string tp = "<V, R, " + std::to_string(op.a) + ", " + t5 + ">";
+                    s << "if (" << cond << ") { ";
+                    if (op.b) both("swap1" + tp + "(x);", "swap1" + tp + "(y);");
+                    both("diag1" + tp + "(x, MV(" + std::to_string(o) + "), MV(" + std::to_string(o + 1) + "));",
+                         "diag1" + tp + "(y, MV(" + std::to_string(o) + "), MV(" + std::to_string(o + 1) + "));");
+                    s << " }\n";
+                    break;
+                }
+                case OP_DIAG1R: {
+                    std::string tp = "<V, R, " + std::to_string(op.a) + ", " + t5 + ">";
+                    s << "if (" << cond << ") { ";
+                    both("diag1" + tp + "(x, MV(" + std::to_string(o) + "), MV(" + std::to_string(o + 1) + "));",
+                         "diag1" + tp + "(y, MV(" + std::to_string(o) + "), MV(" + std::to_string(o + 1) + "));");
+                    s << " }\n";
+                    break;
+                }
+                case OP_DIAG1T:
+                case OP_DIAG1G: {
+                    std::string bit = op.code == OP_DIAG1T ? "((tid >> " + std::to_string(op.a) + ") & 1)"
+                                                           : "((outer >> " + std::to_string(op.a) + ") & 1ull)";
+                    s << "if (" << cond << ") { const V d = " << bit << " ? MV(" << o + 1 << ") : MV(" << o << "); ";
+                    both("scale<V, R, " + t5 + ">(x, d);", "scale<V, R, " + t5 + ">(y, d);");
+                    s << " }\n";
+                    break;
+                }
+                case OP_DENSE2: {
+                    std::string tp = "<V, R, " + std::to_string(op.a) + ", " + std::to_string(op.b) + ", " + t5 + ">";
+                    s << "if (" << cond << ") { const V m[16] = {" << mvs(o, 16) << "}; ";
+                    both("dense2" + tp + "(x, m);", "dense2" + tp + "(y, m);");
+                    s << " }\n";
+                    break;
+                }
+                case OP_DIAGK:
+                case G_DIAGK: {
+                    // per element: index from register bits (literal) | thread / tile bits (runtime)
+                    std::ostringstream rt;
+                    int regpart_mask[8] = {0};
+                    rt << "0";
+                    for (int q = 0; q < op.t; ++q) {
+                        uint32_t loc = static_cast<uint32_t>((op.aux >> (8 * q)) & 0xff);
+                        uint32_t ty = loc >> 6, pos = loc & 63;
+                        if (ty == LOC_THR) rt << " | (((tid >> " << pos << ") & 1) << " << q << ")";
+                        if (ty == LOC_TILE) rt << " | ((int)((outer >> " << pos << ") & 1ull) << " << q << ")";
+                        if (ty == LOC_REG) regpart_mask[q] = 1;
+                    }
+                    const bool grad = op.code == G_DIAGK;
+                    s << "{ " << (grad ? "double g = 0.0; " : "") << "if (" << cond << ") { const int ib = " << rt.str() << "; ";
+                    for (int j = 0; j < R; ++j) {
+                        if ((j & op.creg_mask) != op.creg_val) continue;
+                        int lit = 0;
+                        for (int q = 0; q < op.t; ++q) {
+                            uint32_t loc = static_cast<uint32_t>((op.aux >> (8 * q)) & 0xff);
+                            if (regpart_mask[q] && ((j >> (loc & 63)) & 1)) lit |= 1 << q;
+                        }
+                        s << "{ const int ix = " << o << " + (ib | " << lit << "); const V d = mk<V>(pm.m[2 * ix], pm.m[2 * ix + 1]); ";
+                        if (grad)
+                            s << "g += imcm(y[" << j << "], cmul(d, x[" << j << "])); }";
+                        else {
+                            s << "x[" << j << "] = cmul(x[" << j << "], d);";
+                            if (back) s << " y[" << j << "] = cmul(y[" << j << "], d);";
+                            s << " }";
+                        }
+                    }
+                    s << " }";
+                    if (grad) s << " g = warp_sum(g); if (lane == 0) sg[" << op.gslot * NW << " + warp] += g;";
+                    s << " }\n";
+                    break;
+                }
+                case G_CROSS1: {
+                    s << "{ double c[8] = {0, 0, 0, 0, 0, 0, 0, 0}; if (" << cond << ") gcross1<V, R, " << int(op.a)
+                      << ">(x, y, c); const double v = warp_sum8(c, lane); if ((lane & 3) == 0) sg[(" << op.gslot
+                      << " + (lane >> 2)) * " << NW << " + warp] += v; }\n";
+                    break;
+                }
+                case G_DENSE1:
+                case G_DIAG1R:
+                case G_DIAG1U:
+                case G_DENSE2: {
+                    s << "{ double g = 0.0; if (" << cond << ") { ";
+                    if (op.code == G_DENSE1)
+                        s << "g = gdense1<V, R, " << int(op.a) << ", " << t5 << ">(x, y, " << mvs(o, 4) << ");";
+                    else if (op.code == G_DIAG1R)
+                        s << "g = gdiag1<V, R, " << int(op.a) << ", " << t5 << ">(x, y, " << mvs(o, 2) << ");";
+                    else if (op.code == G_DIAG1U)
+                        s << "const V d = " << (op.b == 0 ? "((tid >> " + std::to_string(op.a) + ") & 1)"
+                                                          : "((outer >> " + std::to_string(op.a) + ") & 1ull)")
+                          << " ? MV(" << o + 1 << ") : MV(" << o << "); g = gscale<V, R, " << t5 << ">(x, y, d);";
+                    else
+                        s << "const V m[16] = {" << mvs(o, 16) << "}; g = gdense2<V, R, " << int(op.a) << ", " << int(op.b)
+                          << ", " << t5 << ">(x, y, m);";
+                    s << " } g = warp_sum(g); if (lane == 0) sg[" << op.gslot * NW << " + warp] += g; }\n";
+                    break;
+                }
+                default:
+                    raise(QBG_ERR_INTERNAL, "jit: unknown op");
+            }
+        }
+    }
+    for (int j = 0; j < R; ++j) {
+        s << "psi[tb + gL + " << goff(SL, j) << "ll] = x[" << j << "];";
+        if (back) s << " adj[tb + gL + " << goff(SL, j) << "ll] = y[" << j << "];";
+        s << "\n";
+    }
+    s << "}\n";  // tile loop
+    if (back) {
+        s << "__syncthreads();\nfor (int sl = tid; sl < " << P.ngrad << "; sl += " << TH
+          << ") { double a = 0.0; for (int w = 0; w < " << NW << "; ++w) a += sg[sl * " << NW
+          << " + w]; gpart[(i64)(gbase + sl) * gcols + blockIdx.x] = a; }\n";
+    }
+    s << "#undef MV\n}\n";
+    return s.str();
+}
+
+// Generates, compiles (cached) and attaches the specialised kernels of a plan.
+void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128) {
+    std::map<uint64_t, int> uniq;  // body hash -> kernel index
+    std::vector<std::string> names;
+    std::string src;
+    const int NW = (1 << (M - RB)) / 32;
+    const size_t elem = c128 ? 16 : 8;
+    for (auto& st : pl.steps) {
+        if (!st.tile) continue;
+        const DPass& P = st.pass;
+        std::string body = gen_pass(P, pl.ops.data() + P.op_base, P.nmats, M, RB, back, c128);
+        uint64_t h = jit::fnv(body);
+        auto it = uniq.find(h);
+        if (it == uniq.end()) {
+            char nm[40];
+            std::snprintf(nm, sizeof(nm), "qbg_%016llx", static_cast<unsigned long long>(h));
+            std::string b = body;
+            b.replace(b.find("__NAME__"), 8, nm);
+            src += b;
+            it = uniq.emplace(h, static_cast<int>(names.size())).first;
+            names.push_back(nm);
+        }
+        st.jk = it->second;
+        // matrix parameter blob
+        const int nm2 = std::max(2, 2 * P.nmats);
+        st.blob.assign(static_cast<size_t>(nm2) * (c128 ? 8 : 4), 0);
+        for (int k = 0; k < P.nmats; ++k) {
+            const cdbl& v = pl.mats[P.mat_base + k];
+            if (c128) {
+                double* d = reinterpret_cast<double*>(st.blob.data());
+                d[2 * k] = v.re;
+                d[2 * k + 1] = v.im;
+            } else {
+                float* f = reinterpret_cast<float*>(st.blob.data());
+                f[2 * k] = static_cast<float>(v.re);
+                f[2 * k + 1] = static_cast<float>(v.im);
+            }
+        }
+        st.smem = (P.nstages > 1 || back ? (back ? 2 : 1) * (elem << M) : 0) + (back ? static_cast<size_t>(P.ngrad) * NW * 8 : 0);
+    }
+    if (!names.empty()) pl.jk = jit::compile(src, names);
+}
+
 // ---- execution ---------------------------------------------------------------------------------
 template <typename V, int M, int RB, bool BACK>
-void launch_fused(V* psi, V* adj, const DPass& P, const FusedPlan& pl, double* gpart, int64_t gcols) {
-    constexpr int T = 1 << (M - RB), NW = T / 32;
-    constexpr size_t smem_max = fused_smem_bytes<V, M, BACK>(BACK ? kMaxComps * NW : 0);
-    static int per_sm = 0;
-    auto kern = k_fused<V, M, RB, BACK>;
-    if (per_sm == 0) {
-        QBG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_max)));
-        QBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem_max));
-        per_sm = std::max(1, per_sm);
-    }
-    size_t smem = fused_smem_bytes<V, M, BACK>(BACK ? P.ngrad * NW : 0);
-    int64_t grid = std::min<int64_t>(static_cast<int64_t>(P.ntiles), static_cast<int64_t>(num_sms()) * per_sm);
+void launch_jit(V* psi, V* adj, Step& st, FusedPlan& pl, double* gpart, int64_t gcols) {
+    constexpr int T = 1 << (M - RB);
+    const DPass& P = st.pass;
+    int64_t grid = std::min<int64_t>(static_cast<int64_t>(P.ntiles), static_cast<int64_t>(num_sms()) * 2);
     if (BACK) grid = std::min<int64_t>(grid, gcols);
     double bytes = static_cast<double>(P.ntiles) * (1 << M) * sizeof(V) * (BACK ? 4.0 : 2.0);
+    int gbase = P.grad_base;
+    void* args[] = {&psi, &adj, &gpart, &gcols, &gbase, st.blob.data()};
     LaunchScope ls(BACK ? "fused_bwd" : "fused_fwd", bytes);
-    kern<<<static_cast<unsigned>(grid), T, smem, stream()>>>(psi, adj, P, pl.d_ops, pl.d_mats, gpart, gcols);
-    QBG_CUDA(cudaGetLastError());
+    jit::launch(pl.jk[st.jk], static_cast<unsigned>(grid), T, st.smem, args);
 }
 
 int batch_bits(int64_t B) {
@@ -1301,6 +923,18 @@ std::shared_ptr<FusedPlan> get_plan(std::vector<std::shared_ptr<FusedPlan>>& cac
         } else if (!st.tile && !pl->gates[st.single].run.empty()) {
             raise(QBG_ERR_INTERNAL, "fused plan: untiled rotation run");
         }
+    if (jit::enabled()) {
+        try {
+            jit_prepare(*pl, M, RB, dir == 2, s.dtype == QBG_C128);
+        } catch (const Error& e) {
+            static bool warned = false;
+            const char* strict = std::getenv("QBG_JIT_STRICT");
+            if (strict && strict[0] == '1') throw;
+            if (!warned) std::fprintf(stderr, "qbg: JIT specialisation failed, using the interpreter kernels: %s\n", e.what());
+            warned = true;
+            for (auto& st : pl->steps) st.jk = -1;
+        }
+    }
     pl->d_ops = upload(pl->ops);
     pl->d_mats = upload(pl->mats);
     pl->d_epi = upload(pl->epi);
@@ -1318,7 +952,10 @@ void run_forward(const DevState& s, FusedPlan& pl) {
     V* psi = static_cast<V*>(s.ptr);
     for (auto& st : pl.steps) {
         if (st.tile)
-            launch_fused<V, kFwdM, kFwdRB, false>(psi, nullptr, st.pass, pl, nullptr, 0);
+            if (st.jk >= 0)
+                launch_jit<V, kFwdM, kFwdRB, false>(psi, nullptr, st, pl, nullptr, 0);
+            else
+                launch_interp(pl.dtype, false, psi, nullptr, st.pass, pl.d_ops, pl.d_mats, nullptr, 0);
         else
             launch_gate(s, pl.gates[st.single].gate());
     }
@@ -1332,8 +969,10 @@ void run_backward(const DevState& psi, const DevState& adj, FusedPlan& pl, doubl
     if (total) QBG_CUDA(cudaMemsetAsync(part, 0, total * cols * sizeof(double), stream()));
     for (auto& st : pl.steps) {
         if (st.tile) {
-            launch_fused<V, kBwdM, kBwdRB, true>(static_cast<V*>(psi.ptr), static_cast<V*>(adj.ptr), st.pass, pl, part,
-                                                  cols);
+            if (st.jk >= 0)
+                launch_jit<V, kBwdM, kBwdRB, true>(static_cast<V*>(psi.ptr), static_cast<V*>(adj.ptr), st, pl, part, cols);
+            else
+                launch_interp(pl.dtype, true, psi.ptr, adj.ptr, st.pass, pl.d_ops, pl.d_mats, part, cols);
         } else {
             const PG& g = pl.gates[st.single];
             int used = 0;
@@ -1342,14 +981,8 @@ void run_backward(const DevState& psi, const DevState& adj, FusedPlan& pl, doubl
     }
     if (total) {
         double* sums = static_cast<double*>(scratch(total * sizeof(double), 12));
-        {
-            LaunchScope ls("grad_rows", 8.0 * total * cols);
-            k_rows<<<static_cast<unsigned>((total + 127) / 128), 128, 0, stream()>>>(part, total, cols, sums);
-            QBG_CUDA(cudaGetLastError());
-        }
-        LaunchScope ls("grad_epilogue", 8.0 * total);
-        k_grad_epilogue<<<1, 32, 0, stream()>>>(sums, pl.d_epi, static_cast<int64_t>(pl.epi.size()), d_grads);
-        QBG_CUDA(cudaGetLastError());
+        launch_grad_rows(part, total, cols, sums);
+        launch_grad_epilogue(sums, pl.d_epi, static_cast<int64_t>(pl.epi.size()), d_grads);
     }
 }
 
@@ -1469,34 +1102,13 @@ std::shared_ptr<FusedPlan> get_seed_plan(Observable& o, const DevState& s) {
     return pl;
 }
 
-template <typename V>
 void run_seed(const DevState& psi, const DevState& phi, FusedPlan& pl, double* d_energy) {
-    constexpr int T = 256;
-    size_t smem = sizeof(V) << kSeedM;
-    auto kern = k_seed<V, kSeedM>;
-    static int per_sm = 0;
-    if (per_sm == 0) {
-        QBG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        QBG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T, smem));
-        per_sm = std::max(1, per_sm);
-    }
     const SPass& last = pl.spasses.back();
     const int64_t bc = int64_t{1} << last.nb;
     double* epart = static_cast<double*>(scratch(last.ntiles * bc * sizeof(double), 14));
-    for (auto& sp : pl.spasses) {
-        int64_t grid = std::min<int64_t>(static_cast<int64_t>(sp.ntiles), static_cast<int64_t>(num_sms()) * per_sm);
-        LaunchScope ls("seed", (sp.first ? 2.0 : 3.0) * psi.bytes());
-        kern<<<static_cast<unsigned>(grid), T, smem, stream()>>>(static_cast<const V*>(psi.ptr), static_cast<V*>(phi.ptr),
-                                                              sp, pl.d_groups, pl.d_terms, epart);
-        QBG_CUDA(cudaGetLastError());
-    }
-    if (d_energy) {
-        LaunchScope ls("energy", 8.0 * last.ntiles * bc);
-        uint64_t nouter = uint64_t{1} << (pl.n - last.mq);
-        k_energy<<<static_cast<unsigned>((psi.B + 127) / 128), 128, 0, stream()>>>(epart, nouter, last.nchunks, bc, psi.B,
-                                                                                 d_energy);
-        QBG_CUDA(cudaGetLastError());
-    }
+    for (auto& sp : pl.spasses)
+        launch_seed(psi.dtype, psi.ptr, phi.ptr, sp, pl.d_groups, pl.d_terms, epart, (sp.first ? 2.0 : 3.0) * psi.bytes());
+    if (d_energy) launch_energy(epart, uint64_t{1} << (pl.n - last.mq), last.nchunks, bc, psi.B, d_energy);
 }
 
 }  // namespace
@@ -1506,9 +1118,9 @@ bool fused_obs_apply(const DevState& psi, const DevState& phi, Observable& o, do
     if (psi.n < kSeedM - nb || o.terms.empty()) return false;
     auto pl = get_seed_plan(o, psi);
     if (psi.dtype == QBG_C128)
-        run_seed<double2>(psi, phi, *pl, d_energy);
+        run_seed(psi, phi, *pl, d_energy);
     else
-        run_seed<float2>(psi, phi, *pl, d_energy);
+        run_seed(psi, phi, *pl, d_energy);
     return true;
 }
 

@@ -89,5 +89,26 @@ struct STerm {
     uint64_t zout;          // Z support outside the tile (global bits)
 };
 
+constexpr int kMaxOps = 256;    // ops per pass (smem resident)
+constexpr int kMaxMats = 512;   // complex matrix entries per pass (smem resident)
+constexpr int kMaxComps = 256;  // gradient components per pass
+
+struct GradEntry {
+    int32_t type;  // 0 scalar component, 1 cross matrix (8 components)
+    int32_t comp;
+    int32_t param;
+    int32_t pad;
+    double A[8];  // cdbl A[4]     // column-major 2x2, cross entries only
+};
+
+struct SPass {
+    int32_t mq, nb;
+    uint8_t qpos[64];
+    int64_t B, nchunks;
+    uint64_t ntiles;
+    int32_t g0, g1;  // groups of this pass
+    int32_t first, last;
+};
+
 }  // namespace fz
 }  // namespace qbg

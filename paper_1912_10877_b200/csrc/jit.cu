@@ -1,0 +1,179 @@
+// jit.cu — NVRTC compile + cudaLibrary load + caches for the specialised tile kernels.
+#include "jit.h"
+
+#include <dlfcn.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <map>
+#include <mutex>
+#include <sstream>
+
+#include "common.cuh"
+#include "jit_prelude.h"
+
+namespace qbg {
+namespace jit {
+
+namespace {
+
+// minimal NVRTC ABI (nvrtc.h), resolved with dlopen so libqbg.so loads without NVRTC
+typedef int nvrtcResult;
+typedef struct _nvrtcProgram* nvrtcProgram;
+struct Nvrtc {
+    void* h = nullptr;
+    nvrtcResult (*create)(nvrtcProgram*, const char*, const char*, int, const char* const*, const char* const*);
+    nvrtcResult (*compile)(nvrtcProgram, int, const char* const*);
+    nvrtcResult (*logsize)(nvrtcProgram, size_t*);
+    nvrtcResult (*log)(nvrtcProgram, char*);
+    nvrtcResult (*cubinsize)(nvrtcProgram, size_t*);
+    nvrtcResult (*cubin)(nvrtcProgram, char*);
+    nvrtcResult (*destroy)(nvrtcProgram*);
+    bool ok = false;
+};
+
+Nvrtc& nvrtc() {
+    static Nvrtc n;
+    static bool tried = false;
+    if (tried) return n;
+    tried = true;
+    const char* names[] = {"libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so"};
+    for (const char* nm : names) {
+        n.h = dlopen(nm, RTLD_NOW | RTLD_LOCAL);
+        if (n.h) break;
+    }
+    if (!n.h) return n;
+    n.create = reinterpret_cast<decltype(n.create)>(dlsym(n.h, "nvrtcCreateProgram"));
+    n.compile = reinterpret_cast<decltype(n.compile)>(dlsym(n.h, "nvrtcCompileProgram"));
+    n.logsize = reinterpret_cast<decltype(n.logsize)>(dlsym(n.h, "nvrtcGetProgramLogSize"));
+    n.log = reinterpret_cast<decltype(n.log)>(dlsym(n.h, "nvrtcGetProgramLog"));
+    n.cubinsize = reinterpret_cast<decltype(n.cubinsize)>(dlsym(n.h, "nvrtcGetCUBINSize"));
+    n.cubin = reinterpret_cast<decltype(n.cubin)>(dlsym(n.h, "nvrtcGetCUBIN"));
+    n.destroy = reinterpret_cast<decltype(n.destroy)>(dlsym(n.h, "nvrtcDestroyProgram"));
+    n.ok = n.create && n.compile && n.logsize && n.log && n.cubinsize && n.cubin && n.destroy;
+    return n;
+}
+
+std::mutex g_mu;
+std::map<uint64_t, cudaLibrary_t> g_libs;  // source hash -> loaded library
+
+std::string cache_dir() {
+    const char* e = std::getenv("QBG_JIT_CACHE");
+    if (e && *e) return e;
+    const char* home = std::getenv("HOME");
+    return std::string(home ? home : "/tmp") + "/.cache/qbg_jit";
+}
+
+bool read_file(const std::string& p, std::string& out) {
+    std::ifstream f(p, std::ios::binary);
+    if (!f) return false;
+    std::ostringstream ss;
+    ss << f.rdbuf();
+    out = ss.str();
+    return !out.empty();
+}
+
+void write_file(const std::string& p, const std::string& data) {
+    std::string dir = cache_dir();
+    ::mkdir((dir.substr(0, dir.rfind('/'))).c_str(), 0755);
+    ::mkdir(dir.c_str(), 0755);
+    std::string tmp = p + ".tmp" + std::to_string(::getpid());
+    {
+        std::ofstream f(tmp, std::ios::binary);
+        if (!f) return;
+        f.write(data.data(), static_cast<std::streamsize>(data.size()));
+    }
+    std::rename(tmp.c_str(), p.c_str());
+}
+
+std::string build_cubin(const std::string& src, uint64_t key) {
+    Nvrtc& n = nvrtc();
+    if (!n.ok) raise(QBG_ERR_INTERNAL, "jit: NVRTC is not available");
+    std::string full = std::string(kPrelude) + src;
+    nvrtcProgram prog;
+    if (n.create(&prog, full.c_str(), "qbg_pass.cu", 0, nullptr, nullptr) != 0) raise(QBG_ERR_INTERNAL, "jit: nvrtcCreateProgram failed");
+    const char* opts[] = {"-arch=sm_100a", "-std=c++17", "-lineinfo", "-default-device", "--restrict"};
+    int rc = n.compile(prog, 5, opts);
+    if (rc != 0) {
+        size_t ls = 0;
+        n.logsize(prog, &ls);
+        std::string log(ls, '\0');
+        n.log(prog, log.data());
+        n.destroy(&prog);
+        raise(QBG_ERR_INTERNAL, "jit: NVRTC compilation failed (key " + std::to_string(key) + "):\n" + log.substr(0, 4000));
+    }
+    size_t cs = 0;
+    n.cubinsize(prog, &cs);
+    std::string cub(cs, '\0');
+    n.cubin(prog, cub.data());
+    n.destroy(&prog);
+    return cub;
+}
+
+}  // namespace
+
+uint64_t fnv(const std::string& s) {
+    uint64_t h = 1469598103934665603ULL;
+    for (unsigned char c : s) {
+        h ^= c;
+        h *= 1099511628211ULL;
+    }
+    return h;
+}
+
+bool enabled() {
+    const char* e = std::getenv("QBG_JIT");
+    if (e && e[0] == '0') return false;
+    return nvrtc().ok;
+}
+
+std::vector<Kernel> compile(const std::string& src, const std::vector<std::string>& names) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    const uint64_t key = fnv(std::string(kPrelude) + src);
+    cudaLibrary_t lib = nullptr;
+    auto it = g_libs.find(key);
+    if (it != g_libs.end()) {
+        lib = it->second;
+    } else {
+        char name[64];
+        std::snprintf(name, sizeof(name), "/%016llx.cubin", static_cast<unsigned long long>(key));
+        const std::string path = cache_dir() + name;
+        std::string cub;
+        if (!read_file(path, cub)) {
+            cub = build_cubin(src, key);
+            write_file(path, cub);
+        }
+        cudaError_t e = cudaLibraryLoadData(&lib, cub.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+        if (e != cudaSuccess) {
+            // a stale / foreign cache entry: rebuild once
+            cudaGetLastError();
+            cub = build_cubin(src, key);
+            write_file(path, cub);
+            QBG_CUDA(cudaLibraryLoadData(&lib, cub.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+        }
+        g_libs[key] = lib;
+    }
+    std::vector<Kernel> out;
+    for (const auto& nm : names) {
+        Kernel k;
+        QBG_CUDA(cudaLibraryGetKernel(&k.k, lib, nm.c_str()));
+        out.push_back(k);
+    }
+    return out;
+}
+
+void launch(Kernel& k, unsigned grid, unsigned block, size_t smem, void** args) {
+    if (static_cast<int>(smem) > k.max_dyn_smem) {
+        int dev = 0;
+        QBG_CUDA(cudaGetDevice(&dev));
+        QBG_CUDA(cudaKernelSetAttributeForDevice(k.k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem), dev));
+        k.max_dyn_smem = static_cast<int>(smem);
+    }
+    QBG_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(k.k), dim3(grid), dim3(block), args, smem, stream()));
+}
+
+}  // namespace jit
+}  // namespace qbg

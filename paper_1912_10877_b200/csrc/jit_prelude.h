@@ -1,0 +1,184 @@
+// jit_prelude.h — device templates the generated tile-pass kernels are written in.
+// Every slot index and register-control mask is a template argument: in the generated
+// straight-line code a controlled swap is a compile-time register rename (no instruction), a
+// register-controlled gate has no per-pair predicate, and matrix entries are constant-bank
+// operands of the FMAs (the pass's matrices are a __grid_constant__ kernel parameter).
+#pragma once
+
+namespace qbg {
+namespace jit {
+
+static const char kPrelude[] = R"QBGJIT(
+typedef unsigned long long u64;
+typedef long long i64;
+struct __align__(16) c128 { double x, y; };
+struct __align__(8) c64 { float x, y; };
+template <class V> struct RT;
+template <> struct RT<c128> { typedef double T; };
+template <> struct RT<c64> { typedef float T; };
+template <class T, int N> struct PM { T m[N]; };
+
+template <class V> __device__ __forceinline__ V mk(typename RT<V>::T a, typename RT<V>::T b) { V v; v.x = a; v.y = b; return v; }
+template <class V> __device__ __forceinline__ V cmul(V a, V b) { return mk<V>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+template <class V> __device__ __forceinline__ V cfma(V a, V b, V c) { return mk<V>(a.x + b.x * c.x - b.y * c.y, a.y + b.x * c.y + b.y * c.x); }
+template <class V> __device__ __forceinline__ double imcm(V a, V b) { return (double)a.x * b.y - (double)a.y * b.x; }
+
+template <class V, int R, int K, int CM, int CV>
+__device__ __forceinline__ void dense1(V* x, V m00, V m10, V m01, V m11) {
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    if (j & (1 << K)) continue;
+    if ((j & CM) != CV) continue;
+    V a = x[j], b = x[j | (1 << K)];
+    x[j] = cfma(cmul(m00, a), m01, b);
+    x[j | (1 << K)] = cfma(cmul(m10, a), m11, b);
+  }
+}
+template <class V, int R, int K, int CM, int CV>
+__device__ __forceinline__ void swap1(V* x) {
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    if (j & (1 << K)) continue;
+    if ((j & CM) != CV) continue;
+    V a = x[j]; x[j] = x[j | (1 << K)]; x[j | (1 << K)] = a;
+  }
+}
+template <class V, int R, int K, int CM, int CV>
+__device__ __forceinline__ void diag1(V* x, V d0, V d1) {
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    if ((j & CM) != CV) continue;
+    x[j] = cmul(x[j], (j & (1 << K)) ? d1 : d0);
+  }
+}
+template <class V, int R, int CM, int CV>
+__device__ __forceinline__ void scale(V* x, V d) {
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    if ((j & CM) != CV) continue;
+    x[j] = cmul(x[j], d);
+  }
+}
+template <class V, int R, int K0, int K1, int CM, int CV>
+__device__ __forceinline__ void dense2(V* x, const V* m) {
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    if (j & ((1 << K0) | (1 << K1))) continue;
+    if ((j & CM) != CV) continue;
+    const int i0 = j, i1 = j | (1 << K0), i2 = j | (1 << K1), i3 = j | (1 << K0) | (1 << K1);
+    V a0 = x[i0], a1 = x[i1], a2 = x[i2], a3 = x[i3];
+    V r[4];
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      V acc = cmul(m[rr], a0);
+      acc = cfma(acc, m[4 + rr], a1);
+      acc = cfma(acc, m[8 + rr], a2);
+      r[rr] = cfma(acc, m[12 + rr], a3);
+    }
+    x[i0] = r[0]; x[i1] = r[1]; x[i2] = r[2]; x[i3] = r[3];
+  }
+}
+// ---- gradient terms Σ Im(conj(adj) (K psi)) ----
+template <class V, int R, int K, int CM, int CV>
+__device__ __forceinline__ double gdense1(const V* p, const V* a, V k00, V k10, V k01, V k11) {
+  double g = 0.0;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    if (j & (1 << K)) continue;
+    if ((j & CM) != CV) continue;
+    V p0 = p[j], p1 = p[j | (1 << K)];
+    g += imcm(a[j], cfma(cmul(k00, p0), k01, p1));
+    g += imcm(a[j | (1 << K)], cfma(cmul(k10, p0), k11, p1));
+  }
+  return g;
+}
+template <class V, int R, int K, int CM, int CV>
+__device__ __forceinline__ double gdiag1(const V* p, const V* a, V d0, V d1) {
+  double g = 0.0;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    if ((j & CM) != CV) continue;
+    g += imcm(a[j], cmul((j & (1 << K)) ? d1 : d0, p[j]));
+  }
+  return g;
+}
+template <class V, int R, int CM, int CV>
+__device__ __forceinline__ double gscale(const V* p, const V* a, V d) {
+  double sr = 0.0, si = 0.0;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    if ((j & CM) != CV) continue;
+    sr += (double)a[j].x * p[j].x + (double)a[j].y * p[j].y;
+    si += (double)a[j].x * p[j].y - (double)a[j].y * p[j].x;
+  }
+  return (double)d.x * si + (double)d.y * sr;
+}
+template <class V, int R, int K0, int K1, int CM, int CV>
+__device__ __forceinline__ double gdense2(const V* p, const V* a, const V* m) {
+  double g = 0.0;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    if (j & ((1 << K0) | (1 << K1))) continue;
+    if ((j & CM) != CV) continue;
+    const int idx[4] = {j, j | (1 << K0), j | (1 << K1), j | (1 << K0) | (1 << K1)};
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      V acc = cmul(m[rr], p[idx[0]]);
+      acc = cfma(acc, m[4 + rr], p[idx[1]]);
+      acc = cfma(acc, m[8 + rr], p[idx[2]]);
+      acc = cfma(acc, m[12 + rr], p[idx[3]]);
+      g += imcm(a[idx[rr]], acc);
+    }
+  }
+  return g;
+}
+// C_ab = Σ conj(adj_a) psi_b over the pairs on slot K: c[2(2a+b)] = Re, c[2(2a+b)+1] = Im
+template <class V, int R, int K>
+__device__ __forceinline__ void gcross1(const V* p, const V* a, double* c) {
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    if (j & (1 << K)) continue;
+    const V av[2] = {a[j], a[j | (1 << K)]};
+    const V pv[2] = {p[j], p[j | (1 << K)]};
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        c[2 * (2 * u + v)] += (double)av[u].x * pv[v].x + (double)av[u].y * pv[v].y;
+        c[2 * (2 * u + v) + 1] += (double)av[u].x * pv[v].y - (double)av[u].y * pv[v].x;
+      }
+  }
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+// 8 values over the warp by halving exchanges; lane 4c ends with the sum of component c
+__device__ __forceinline__ double warp_sum8(double* v, int lane) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const bool hi = lane & 16;
+    double send = hi ? v[k] : v[k + 4], keep = hi ? v[k + 4] : v[k];
+    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const bool hi = lane & 8;
+    double send = hi ? v[k] : v[k + 2], keep = hi ? v[k + 2] : v[k];
+    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  {
+    const bool hi = lane & 4;
+    double send = hi ? v[0] : v[1], keep = hi ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  double s = v[0];
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  return s;
+}
+)QBGJIT";
+
+}  // namespace jit
+}  // namespace qbg
