@@ -200,6 +200,13 @@ int qbg_prog_set_params(qbg_prog* prog, const double* theta, int64_t nparams);
 /* Number of device passes the fusion planner emits for forward / backward. */
 int qbg_prog_stats(const qbg_prog* prog, int64_t* fwd_passes, int64_t* bwd_passes,
                    int64_t* fwd_gates);
+/* Text description of the fusion plans built so far (passes, tile qubits, stages, ops). */
+int qbg_prog_plan_info(const qbg_prog* prog, char* buf, int64_t cap);
+/* Runs the fusion planner on the host only (no device needed) for an nbatch register. */
+int qbg_prog_plan_preview(const qbg_prog* prog, int64_t nbatch, int32_t dtype, char* buf, int64_t cap);
+/* Generates and compiles (NVRTC -> sm_100a cubin, no device needed) every specialised kernel the
+   program (and observable, may be NULL) would use; *nkernels receives the number of passes. */
+int qbg_jit_check(const qbg_prog* prog, const qbg_obs* obs, int64_t nbatch, int32_t dtype, int64_t* nkernels);
 int qbg_apply(qbg_reg* reg, const qbg_prog* prog);
 /* Applies the adjoint program (Daggered chain). */
 int qbg_apply_adjoint(qbg_reg* reg, const qbg_prog* prog);

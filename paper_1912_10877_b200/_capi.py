@@ -97,6 +97,9 @@ def lib() -> ctypes.CDLL:
         "qbg_prog_destroy": (c_int32, [P]), "qbg_prog_nparams": (c_int64, [P]),
         "qbg_prog_set_params": (c_int32, [P, P, c_int64]),
         "qbg_prog_stats": (c_int32, [P, POINTER(c_int64), POINTER(c_int64), POINTER(c_int64)]),
+        "qbg_prog_plan_info": (c_int32, [P, c_char_p, c_int64]),
+        "qbg_prog_plan_preview": (c_int32, [P, c_int64, c_int32, c_char_p, c_int64]),
+        "qbg_jit_check": (c_int32, [P, P, c_int64, c_int32, POINTER(c_int64)]),
         "qbg_apply": (c_int32, [P, P]), "qbg_apply_adjoint": (c_int32, [P, P]),
         "qbg_obs_create": (c_int32, [c_int32, POINTER(QbgPauliTerm), c_int64, POINTER(P)]),
         "qbg_obs_destroy": (c_int32, [P]), "qbg_expect": (c_int32, [P, P, P]),

@@ -635,6 +635,18 @@ class Program:
         check(lib().qbg_prog_stats(self._h, ctypes.byref(f), ctypes.byref(b), ctypes.byref(g)))
         return {"fwd_passes": f.value, "bwd_passes": b.value, "gates": g.value}
 
+    def plan_info(self) -> str:
+        """Fusion plans built so far (passes, tile qubits, stages, ops per stage)."""
+        buf = ctypes.create_string_buffer(1 << 20)
+        check(lib().qbg_prog_plan_info(self._h, buf, len(buf)))
+        return buf.value.decode()
+
+    def plan_preview(self, nbatch: int = 1, dtype: str = "c128") -> str:
+        """Runs the fusion planner on the host only (no GPU needed)."""
+        buf = ctypes.create_string_buffer(1 << 20)
+        check(lib().qbg_prog_plan_preview(self._h, nbatch, 0 if dtype == "c128" else 1, buf, len(buf)))
+        return buf.value.decode()
+
     # raw op list (for the oracle / tests)
     def lowered(self):
         nodes = parameter_nodes(self.block)

@@ -985,6 +985,30 @@ int qbg_prog_stats(const qbg_prog* prog, int64_t* fwd, int64_t* bwd, int64_t* ga
         if (gates) *gates = static_cast<int64_t>(prog->p.ops.size());
     });
 }
+int qbg_prog_plan_info(const qbg_prog* prog, char* buf, int64_t cap) {
+    return guarded([&] {
+        std::string s = fused_plan_info(prog->p);
+        if (cap > 0) {
+            std::strncpy(buf, s.c_str(), static_cast<size_t>(cap - 1));
+            buf[cap - 1] = 0;
+        }
+    });
+}
+int qbg_prog_plan_preview(const qbg_prog* prog, int64_t nbatch, int32_t dtype, char* buf, int64_t cap) {
+    return guarded([&] {
+        std::string s = fused_plan_preview(prog->p, nbatch, dtype);
+        if (cap > 0) {
+            std::strncpy(buf, s.c_str(), static_cast<size_t>(cap - 1));
+            buf[cap - 1] = 0;
+        }
+    });
+}
+int qbg_jit_check(const qbg_prog* prog, const qbg_obs* obs, int64_t nbatch, int32_t dtype, int64_t* nkernels) {
+    return guarded([&] {
+        int64_t n = fused_jit_check(prog->p, obs ? &obs->o : nullptr, nbatch, dtype);
+        if (nkernels) *nkernels = n;
+    });
+}
 int qbg_apply(qbg_reg* r, const qbg_prog* prog) {
     return guarded([&] {
         check_reg(r);

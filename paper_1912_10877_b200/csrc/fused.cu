@@ -185,17 +185,24 @@ struct FusedPlan {
     DOp* d_ops = nullptr;
     cdbl* d_mats = nullptr;
     GradEntry* d_epi = nullptr;
+    std::vector<int> csr_ptr, csr_idx;  // gradient entries per parameter, in plan order
+    int* d_ptr = nullptr;
+    int* d_idx = nullptr;
     int64_t tile_passes = 0;
     // observable seed
     std::vector<SPass> spasses;
     std::vector<SGroup> groups;
     std::vector<STerm> terms;
+    std::vector<int> sjk;                  // specialised seed kernel per seed pass
+    std::vector<std::vector<char>> sblob;  // its coefficient parameter
     SGroup* d_groups = nullptr;
     STerm* d_terms = nullptr;
     ~FusedPlan() {
         cudaFree(d_ops);
         cudaFree(d_mats);
         cudaFree(d_epi);
+        cudaFree(d_ptr);
+        cudaFree(d_idx);
         cudaFree(d_groups);
         cudaFree(d_terms);
     }
@@ -323,26 +330,36 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward) {
             uint32_t S = 0;  // local register bits
             std::vector<int> gates;
         };
+        // Stages with lookahead: a stage takes every pending gate whose non-diagonal targets fit
+        // its register set and that commutes with the gates it passes over (same rule as the
+        // pass selection), so a CNOT ring and its rotation runs share stages.
         std::vector<StagePlan> stages;
-        StagePlan cur;
-        for (int gi : sel) {
-            const Gate& g = pl.gates[gi].gate();
-            uint32_t need = 0;
-            if (!is_diagonal(g))
-                for (int q = 0; q < g.t; ++q) need |= 1u << tg.local[g.tbit[q]];
-            if ((need & ~cur.S) == 0) {
-                cur.gates.push_back(gi);
-            } else if (__builtin_popcount(cur.S | need) <= R) {
-                cur.S |= need;
-                cur.gates.push_back(gi);
-            } else {
+        {
+            std::vector<int> pending = sel;
+            while (!pending.empty()) {
+                StagePlan cur;
+                std::vector<int> left;
+                uint64_t bnd = 0, ball = 0;
+                for (int gi : pending) {
+                    const PG& pg = pl.gates[gi];
+                    const Gate& g = pg.gate();
+                    uint32_t need = 0;
+                    if (!is_diagonal(g))
+                        for (int q = 0; q < g.t; ++q) need |= 1u << tg.local[g.tbit[q]];
+                    bool conflict = (pg.nd() & ball) | (pg.all() & bnd);
+                    if (!conflict && __builtin_popcount(cur.S | need) <= R) {
+                        cur.S |= need;
+                        cur.gates.push_back(gi);
+                    } else {
+                        bnd |= pg.nd();
+                        ball |= pg.all();
+                        left.push_back(gi);
+                    }
+                }
                 stages.push_back(cur);
-                cur = StagePlan{};
-                cur.S = need;
-                cur.gates.push_back(gi);
+                pending = left;
             }
         }
-        stages.push_back(cur);
         if (static_cast<int>(stages.size()) > kMaxStages - 2) {
             std::vector<int> back;
             for (size_t s = kMaxStages - 2; s < stages.size(); ++s)
@@ -593,6 +610,7 @@ std::string tid_sum(const W* w, int nbits, bool xr) {
 
 std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, bool back, bool c128) {
     const int R = 1 << RB, W = M - RB, TH = 1 << W, NW = TH / 32;
+    const int CS = NW + 1;  // gradient cell stride (odd: the 8 lanes of a warp_sum8 hit distinct banks)
     const size_t elem = c128 ? 16 : 8;
     std::ostringstream s;
     s << "extern \"C\" __global__ void __launch_bounds__(" << TH << ", 2) __NAME__(" << (c128 ? "c128" : "c64")
@@ -604,7 +622,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
     s << "extern __shared__ __align__(16) unsigned char smraw[];\nV* sx = (V*)smraw;\nV* sy = sx + " << (1 << M) << ";\n";
     if (back) {
         s << "double* sg = (double*)(smraw + " << 2 * (elem << M) << ");\n";
-        s << "for (int i = tid; i < " << P.ngrad * NW << "; i += " << TH << ") sg[i] = 0.0;\n__syncthreads();\n";
+        s << "for (int i = tid; i < " << P.ngrad * CS << "; i += " << TH << ") sg[i] = 0.0;\n__syncthreads();\n";
         s << "const int warp = tid >> 5, lane = tid & 31;\n";
     }
     // hoisted thread parts of every stage's offsets
@@ -765,14 +783,14 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                         }
                     }
                     s << " }";
-                    if (grad) s << " g = warp_sum(g); if (lane == 0) sg[" << op.gslot * NW << " + warp] += g;";
+                    if (grad) s << " g = warp_sum(g); if (lane == 0) sg[" << op.gslot * CS << " + warp] += g;";
                     s << " }\n";
                     break;
                 }
                 case G_CROSS1: {
                     s << "{ double c[8] = {0, 0, 0, 0, 0, 0, 0, 0}; if (" << cond << ") gcross1<V, R, " << int(op.a)
                       << ">(x, y, c); const double v = warp_sum8(c, lane); if ((lane & 3) == 0) sg[(" << op.gslot
-                      << " + (lane >> 2)) * " << NW << " + warp] += v; }\n";
+                      << " + (lane >> 2)) * " << CS << " + warp] += v; }\n";
                     break;
                 }
                 case G_DENSE1:
@@ -791,7 +809,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                     else
                         s << "const V m[16] = {" << mvs(o, 16) << "}; g = gdense2<V, R, " << int(op.a) << ", " << int(op.b)
                           << ", " << t5 << ">(x, y, m);";
-                    s << " } g = warp_sum(g); if (lane == 0) sg[" << op.gslot * NW << " + warp] += g; }\n";
+                    s << " } g = warp_sum(g); if (lane == 0) sg[" << op.gslot * CS << " + warp] += g; }\n";
                     break;
                 }
                 default:
@@ -807,7 +825,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
     s << "}\n";  // tile loop
     if (back) {
         s << "__syncthreads();\nfor (int sl = tid; sl < " << P.ngrad << "; sl += " << TH
-          << ") { double a = 0.0; for (int w = 0; w < " << NW << "; ++w) a += sg[sl * " << NW
+          << ") { double a = 0.0; for (int w = 0; w < " << NW << "; ++w) a += sg[sl * " << CS
           << " + w]; gpart[(i64)(gbase + sl) * gcols + blockIdx.x] = a; }\n";
     }
     s << "#undef MV\n}\n";
@@ -815,7 +833,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
 }
 
 // Generates, compiles (cached) and attaches the specialised kernels of a plan.
-void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128) {
+void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128, bool check_only = false) {
     std::map<uint64_t, int> uniq;  // body hash -> kernel index
     std::vector<std::string> names;
     std::string src;
@@ -852,9 +870,14 @@ void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128) {
                 f[2 * k + 1] = static_cast<float>(v.im);
             }
         }
-        st.smem = (P.nstages > 1 || back ? (back ? 2 : 1) * (elem << M) : 0) + (back ? static_cast<size_t>(P.ngrad) * NW * 8 : 0);
+        st.smem = (P.nstages > 1 || back ? (back ? 2 : 1) * (elem << M) : 0) +
+                  (back ? static_cast<size_t>(P.ngrad) * (NW + 1) * 8 : 0);
     }
-    if (!names.empty()) pl.jk = jit::compile(src, names);
+    if (names.empty()) return;
+    if (check_only)
+        jit::compile_only(src);
+    else
+        pl.jk = jit::compile(src, names);
 }
 
 // ---- execution ---------------------------------------------------------------------------------
@@ -877,6 +900,8 @@ int batch_bits(int64_t B) {
     return nb;
 }
 
+std::shared_ptr<FusedPlan> build_host_plan(const Program& p, const DevState& s, int dir);
+
 std::shared_ptr<FusedPlan> get_plan(std::vector<std::shared_ptr<FusedPlan>>& cache, const Program& p,
                                     const DevState& s, int dir) {
     for (auto& c : cache)
@@ -884,6 +909,41 @@ std::shared_ptr<FusedPlan> get_plan(std::vector<std::shared_ptr<FusedPlan>>& cac
     cache.erase(std::remove_if(cache.begin(), cache.end(),
                                [&](const std::shared_ptr<FusedPlan>& c) { return c->dir == dir && c->B == s.B; }),
                 cache.end());
+    auto pl = build_host_plan(p, s, dir);
+    const int M = dir == 2 ? kBwdM : kFwdM, RB = dir == 2 ? kBwdRB : kFwdRB;
+    if (jit::enabled()) {
+        try {
+            jit_prepare(*pl, M, RB, dir == 2, s.dtype == QBG_C128);
+        } catch (const Error& e) {
+            static bool warned = false;
+            const char* strict = std::getenv("QBG_JIT_STRICT");
+            if (strict && strict[0] == '1') throw;
+            if (!warned) std::fprintf(stderr, "qbg: JIT specialisation failed, using the interpreter kernels: %s\n", e.what());
+            warned = true;
+            for (auto& st : pl->steps) st.jk = -1;
+        }
+    }
+    pl->d_ops = upload(pl->ops);
+    pl->d_mats = upload(pl->mats);
+    pl->d_epi = upload(pl->epi);
+    {
+        int np = 0;
+        for (auto& e : pl->epi) np = std::max(np, e.param + 1);
+        pl->csr_ptr.assign(np + 1, 0);
+        for (auto& e : pl->epi) pl->csr_ptr[e.param + 1]++;
+        for (int k = 0; k < np; ++k) pl->csr_ptr[k + 1] += pl->csr_ptr[k];
+        pl->csr_idx.assign(pl->epi.size(), 0);
+        std::vector<int> cur(pl->csr_ptr.begin(), pl->csr_ptr.end() - 1);
+        for (size_t k = 0; k < pl->epi.size(); ++k) pl->csr_idx[cur[pl->epi[k].param]++] = static_cast<int>(k);
+        pl->d_ptr = upload(pl->csr_ptr);
+        pl->d_idx = upload(pl->csr_idx);
+    }
+    cache.push_back(pl);
+    return pl;
+}
+
+// The planner alone (no device, no JIT): used by get_plan and by the host-only preview.
+std::shared_ptr<FusedPlan> build_host_plan(const Program& p, const DevState& s, int dir) {
     auto pl = std::make_shared<FusedPlan>();
     pl->version = p.version;
     pl->B = s.B;
@@ -923,22 +983,6 @@ std::shared_ptr<FusedPlan> get_plan(std::vector<std::shared_ptr<FusedPlan>>& cac
         } else if (!st.tile && !pl->gates[st.single].run.empty()) {
             raise(QBG_ERR_INTERNAL, "fused plan: untiled rotation run");
         }
-    if (jit::enabled()) {
-        try {
-            jit_prepare(*pl, M, RB, dir == 2, s.dtype == QBG_C128);
-        } catch (const Error& e) {
-            static bool warned = false;
-            const char* strict = std::getenv("QBG_JIT_STRICT");
-            if (strict && strict[0] == '1') throw;
-            if (!warned) std::fprintf(stderr, "qbg: JIT specialisation failed, using the interpreter kernels: %s\n", e.what());
-            warned = true;
-            for (auto& st : pl->steps) st.jk = -1;
-        }
-    }
-    pl->d_ops = upload(pl->ops);
-    pl->d_mats = upload(pl->mats);
-    pl->d_epi = upload(pl->epi);
-    cache.push_back(pl);
     return pl;
 }
 
@@ -982,7 +1026,8 @@ void run_backward(const DevState& psi, const DevState& adj, FusedPlan& pl, doubl
     if (total) {
         double* sums = static_cast<double*>(scratch(total * sizeof(double), 12));
         launch_grad_rows(part, total, cols, sums);
-        launch_grad_epilogue(sums, pl.d_epi, static_cast<int64_t>(pl.epi.size()), d_grads);
+        launch_grad_epilogue(sums, pl.d_epi, static_cast<int64_t>(pl.epi.size()), pl.d_ptr, pl.d_idx,
+                             static_cast<int64_t>(pl.csr_ptr.size()) - 1, d_grads);
     }
 }
 
@@ -1018,12 +1063,61 @@ void fused_stats(const Program& p, int64_t* f, int64_t* b) {
     }
 }
 
+namespace {
+std::string plans_text(const std::vector<std::shared_ptr<FusedPlan>>& plans);
+}
+
+std::string fused_plan_info(const Program& p) { return plans_text(p.plans); }
+
+std::string fused_plan_preview(const Program& p, int64_t B, int dtype) {
+    DevState s;
+    s.n = p.n;
+    s.B = B;
+    s.dtype = dtype;
+    std::vector<std::shared_ptr<FusedPlan>> v;
+    if (fusable(s, kFwdM)) v.push_back(build_host_plan(p, s, 0));
+    if (fusable(s, kBwdM)) v.push_back(build_host_plan(p, s, 2));
+    return plans_text(v);
+}
+
+namespace {
+std::string plans_text(const std::vector<std::shared_ptr<FusedPlan>>& plans) {
+    std::ostringstream s;
+    for (auto& c : plans) {
+        s << "plan dir=" << c->dir << " B=" << c->B << " steps=" << c->steps.size() << " kernels=" << c->jk.size()
+          << " comps=" << c->ncomps << "\n";
+        for (auto& st : c->steps) {
+            if (!st.tile) {
+                s << "  single gate t=" << c->gates[st.single].gate().t << "\n";
+                continue;
+            }
+            const DPass& P = st.pass;
+            s << "  tile Q=";
+            for (int k = 0; k < P.mq; ++k) s << int(P.qpos[k]) << (k + 1 < P.mq ? "," : "");
+            s << " stages=" << P.nstages << " ops=" << P.nops << " [";
+            for (int k = 0; k < P.nstages; ++k) s << P.st[k].op_end - P.st[k].op_begin << (k + 1 < P.nstages ? " " : "");
+            s << "] comps=" << P.ngrad << " smem=" << st.smem << "\n";
+        }
+    }
+    return s.str();
+}
+}  // namespace
+
 // ---- observable seed ------------------------------------------------------------------------------
 namespace {
+
+std::shared_ptr<FusedPlan> make_seed_plan(const Observable& o, const DevState& s, bool check_only);
+void seed_jit_prepare(FusedPlan& pl, bool c128, bool check_only);
 
 std::shared_ptr<FusedPlan> get_seed_plan(Observable& o, const DevState& s) {
     for (auto& c : o.plans)
         if (c->B == s.B && c->dtype == s.dtype && c->n == s.n) return c;
+    auto pl = make_seed_plan(o, s, false);
+    o.plans.push_back(pl);
+    return pl;
+}
+
+std::shared_ptr<FusedPlan> make_seed_plan(const Observable& o, const DevState& s, bool check_only) {
     auto pl = std::make_shared<FusedPlan>();
     pl->B = s.B;
     pl->dtype = s.dtype;
@@ -1096,22 +1190,214 @@ std::shared_ptr<FusedPlan> get_seed_plan(Observable& o, const DevState& s) {
         left = rest;
     }
     if (!pl->spasses.empty()) pl->spasses.back().last = 1;
+    if (check_only) {
+        seed_jit_prepare(*pl, s.dtype == QBG_C128, true);
+        return pl;
+    }
+    if (jit::enabled()) {
+        try {
+            seed_jit_prepare(*pl, s.dtype == QBG_C128, false);
+        } catch (const Error& e) {
+            const char* strict = std::getenv("QBG_JIT_STRICT");
+            if (strict && strict[0] == '1') throw;
+            std::fprintf(stderr, "qbg: JIT seed specialisation failed, using the generic kernel: %s\n", e.what());
+            pl->sjk.clear();
+        }
+    }
     pl->d_groups = upload(pl->groups);
     pl->d_terms = upload(pl->terms);
-    o.plans.push_back(pl);
     return pl;
+}
+
+// Specialised seed pass: the ψ tile is staged in shared memory (linear layout), each thread
+// accumulates 2^M/256 elements l = tid + 256k of φ̄ in registers.  For a group with X support x
+// and term Z supports z_t:  φ̄_l += Σ_t c_t (-1)^{|src & z_t|} ψ_src,  src = l ^ x.  The parity
+// splits into a thread/tile part (per thread, once per tile) and a k part (compile time), and
+// terms with equal k-part Z mask are pre-summed per thread.
+std::string gen_seed(const SPass& sp, const std::vector<SGroup>& groups, const std::vector<STerm>& terms, bool c128) {
+    constexpr int M = kSeedM, TB = 8, T = 1 << TB, R = 1 << (M - TB);
+    const int64_t bc = int64_t{1} << sp.nb;
+    std::ostringstream s;
+    int nterm = 0;
+    for (int gi = sp.g0; gi < sp.g1; ++gi) nterm += groups[gi].term_end - groups[gi].term_begin;
+    s << "extern \"C\" __global__ void __launch_bounds__(" << T << ", 2) __NAME__(const " << (c128 ? "c128" : "c64")
+      << "* __restrict__ psi, " << (c128 ? "c128" : "c64")
+      << "* __restrict__ phi, double* __restrict__ epart, const __grid_constant__ PM<" << (c128 ? "double" : "float")
+      << ", " << std::max(2, 2 * nterm) << "> pm) {\n";
+    s << "typedef " << (c128 ? "c128" : "c64") << " V;\nconst int tid = threadIdx.x;\n";
+    s << "extern __shared__ __align__(16) unsigned char smraw[];\nV* sp = (V*)smraw;\n__shared__ double red[" << T << "];\n";
+    // element offset of local index l: batch bits, then tile qubits
+    auto goff = [&](uint32_t l) {
+        int64_t e = l & (bc - 1);
+        uint32_t q = l >> sp.nb;
+        for (int k = 0; q; ++k, q >>= 1)
+            if (q & 1) e += sp.B << sp.qpos[k];
+        return e;
+    };
+    int64_t wt[TB];
+    for (int p = 0; p < TB; ++p) wt[p] = goff(1u << p);
+    s << "const i64 gt = " << tid_sum(wt, TB, false) << ";\n";
+    s << "V acc[" << R << "];\n";
+    s << "for (u64 tile = blockIdx.x; tile < " << sp.ntiles << "ull; tile += gridDim.x) {\n";
+    if (sp.nchunks == 1)
+        s << "const u64 o = tile; const u64 c = 0;\n";
+    else
+        s << "const u64 o = tile / " << sp.nchunks << "ull; const u64 c = tile - o * " << sp.nchunks << "ull;\n";
+    s << "u64 outer = o;\n";
+    for (int k = 0; k < sp.mq; ++k) {
+        int p = sp.qpos[k];
+        s << "outer = ((outer >> " << p << ") << " << p + 1 << ") | (outer & " << hex((uint64_t{1} << p) - 1) << ");\n";
+    }
+    s << "const i64 tb = (i64)outer * " << sp.B << "ll + (i64)c * " << bc << "ll + gt;\n";
+    s << "__syncthreads();\n";
+    for (int k = 0; k < R; ++k) s << "sp[tid + " << k * T << "] = psi[tb + " << goff(static_cast<uint32_t>(k) << TB) << "ll];\n";
+    for (int k = 0; k < R; ++k) {
+        if (sp.first)
+            s << "acc[" << k << "] = mk<V>(0, 0);\n";
+        else
+            s << "acc[" << k << "] = phi[tb + " << goff(static_cast<uint32_t>(k) << TB) << "ll];\n";
+    }
+    s << "__syncthreads();\n";
+    int tix = 0;
+    for (int gi = sp.g0; gi < sp.g1; ++gi) {
+        const SGroup& g = groups[gi];
+        const uint32_t xlow = g.xloc & (T - 1), xhigh = g.xloc >> TB;
+        std::map<uint32_t, std::vector<int>> byh;
+        for (int t = g.term_begin; t < g.term_end; ++t) byh[terms[t].zloc >> TB].push_back(t);
+        s << "{\n";
+        int hi = 0;
+        std::vector<uint32_t> hs;
+        for (auto& [h, ts] : byh) {
+            s << "V W" << hi << " = mk<V>(0, 0);\n";
+            for (int t : ts) {
+                const STerm& st = terms[t];
+                const int pidx = tix + (t - g.term_begin);
+                s << "{ const int par = (__popc((tid ^ " << xlow << "u) & " << (st.zloc & (T - 1)) << "u) + __popcll(outer & "
+                  << hex(st.zout) << ")) & 1; const V c = mk<V>(pm.m[" << 2 * pidx << "], pm.m[" << 2 * pidx + 1
+                  << "]); W" << hi << " = par ? mk<V>(W" << hi << ".x - c.x, W" << hi << ".y - c.y) : mk<V>(W" << hi
+                  << ".x + c.x, W" << hi << ".y + c.y); }\n";
+            }
+            hs.push_back(h);
+            ++hi;
+        }
+        for (int k = 0; k < R; ++k) {
+            const uint32_t kk = static_cast<uint32_t>(k) ^ xhigh;
+            s << "{ const V v = sp[(tid ^ " << xlow << "u) + " << (kk << TB) << "u]; V cf = mk<V>(0, 0);";
+            for (size_t h = 0; h < hs.size(); ++h) {
+                const bool neg = __builtin_popcount(kk & hs[h]) & 1;
+                s << " cf = mk<V>(cf.x " << (neg ? "-" : "+") << " W" << h << ".x, cf.y " << (neg ? "-" : "+") << " W" << h
+                  << ".y);";
+            }
+            s << " acc[" << k << "] = cfma(acc[" << k << "], cf, v); }\n";
+        }
+        s << "}\n";
+        tix += g.term_end - g.term_begin;
+    }
+    for (int k = 0; k < R; ++k) s << "phi[tb + " << goff(static_cast<uint32_t>(k) << TB) << "ll] = acc[" << k << "];\n";
+    if (sp.last) {
+        s << "double e = 0.0;\n";
+        for (int k = 0; k < R; ++k)
+            s << "{ const V p = sp[tid + " << k * T << "]; e += (double)p.x * acc[" << k << "].x + (double)p.y * acc[" << k
+              << "].y; }\n";
+        s << "red[tid] = e;\n__syncthreads();\n";
+        s << "if (tid < " << bc << ") { double t = 0.0; for (int m = tid; m < " << T << "; m += " << bc
+          << ") t += red[m]; epart[tile * " << bc << "ull + tid] = t; }\n";
+    }
+    s << "}\n}\n";
+    return s.str();
+}
+
+void seed_jit_prepare(FusedPlan& pl, bool c128, bool check_only) {
+    std::map<uint64_t, int> uniq;
+    std::vector<std::string> names;
+    std::string src;
+    pl.sjk.clear();
+    pl.sblob.clear();
+    for (auto& sp : pl.spasses) {
+        std::string body = gen_seed(sp, pl.groups, pl.terms, c128);
+        uint64_t h = jit::fnv(body);
+        auto it = uniq.find(h);
+        if (it == uniq.end()) {
+            char nm[40];
+            std::snprintf(nm, sizeof(nm), "qbs_%016llx", static_cast<unsigned long long>(h));
+            std::string b = body;
+            b.replace(b.find("__NAME__"), 8, nm);
+            src += b;
+            it = uniq.emplace(h, static_cast<int>(names.size())).first;
+            names.push_back(nm);
+        }
+        pl.sjk.push_back(it->second);
+        std::vector<char> blob;
+        int nterm = 0;
+        for (int gi = sp.g0; gi < sp.g1; ++gi) nterm += pl.groups[gi].term_end - pl.groups[gi].term_begin;
+        blob.assign(static_cast<size_t>(std::max(2, 2 * nterm)) * (c128 ? 8 : 4), 0);
+        int tix = 0;
+        for (int gi = sp.g0; gi < sp.g1; ++gi)
+            for (int t = pl.groups[gi].term_begin; t < pl.groups[gi].term_end; ++t, ++tix) {
+                if (c128) {
+                    reinterpret_cast<double*>(blob.data())[2 * tix] = pl.terms[t].cre;
+                    reinterpret_cast<double*>(blob.data())[2 * tix + 1] = pl.terms[t].cim;
+                } else {
+                    reinterpret_cast<float*>(blob.data())[2 * tix] = static_cast<float>(pl.terms[t].cre);
+                    reinterpret_cast<float*>(blob.data())[2 * tix + 1] = static_cast<float>(pl.terms[t].cim);
+                }
+            }
+        pl.sblob.push_back(std::move(blob));
+    }
+    if (check_only)
+        jit::compile_only(src);
+    else
+        pl.jk = jit::compile(src, names);
 }
 
 void run_seed(const DevState& psi, const DevState& phi, FusedPlan& pl, double* d_energy) {
     const SPass& last = pl.spasses.back();
     const int64_t bc = int64_t{1} << last.nb;
     double* epart = static_cast<double*>(scratch(last.ntiles * bc * sizeof(double), 14));
-    for (auto& sp : pl.spasses)
-        launch_seed(psi.dtype, psi.ptr, phi.ptr, sp, pl.d_groups, pl.d_terms, epart, (sp.first ? 2.0 : 3.0) * psi.bytes());
+    if (!pl.sjk.empty()) {
+        for (size_t k = 0; k < pl.spasses.size(); ++k) {
+            const SPass& sp = pl.spasses[k];
+            const void* pp = psi.ptr;
+            void* qq = phi.ptr;
+            void* args[] = {&pp, &qq, &epart, pl.sblob[k].data()};
+            int64_t grid = std::min<int64_t>(static_cast<int64_t>(sp.ntiles), static_cast<int64_t>(num_sms()) * 2);
+            LaunchScope ls("seed", (sp.first ? 2.0 : 3.0) * psi.bytes());
+            jit::launch(pl.jk[pl.sjk[k]], static_cast<unsigned>(grid), 256, psi.elem() << kSeedM, args);
+        }
+    } else {
+        for (auto& sp : pl.spasses)
+            launch_seed(psi.dtype, psi.ptr, phi.ptr, sp, pl.d_groups, pl.d_terms, epart,
+                        (sp.first ? 2.0 : 3.0) * psi.bytes());
+    }
     if (d_energy) launch_energy(epart, uint64_t{1} << (pl.n - last.mq), last.nchunks, bc, psi.B, d_energy);
 }
 
 }  // namespace
+
+// Host-only: generate and NVRTC-compile (no device) every specialised kernel a program and an
+// observable need on a 2^n x B register.  Returns the number of kernels source-compiled.
+int64_t fused_jit_check(const Program& p, const Observable* o, int64_t B, int dtype) {
+    DevState s;
+    s.n = p.n;
+    s.B = B;
+    s.dtype = dtype;
+    int64_t count = 0;
+    if (fusable(s, kFwdM)) {
+        auto pl = build_host_plan(p, s, 0);
+        jit_prepare(*pl, kFwdM, kFwdRB, false, dtype == QBG_C128, true);
+        count += static_cast<int64_t>(pl->steps.size());
+    }
+    if (fusable(s, kBwdM)) {
+        auto pl = build_host_plan(p, s, 2);
+        jit_prepare(*pl, kBwdM, kBwdRB, true, dtype == QBG_C128, true);
+        count += static_cast<int64_t>(pl->steps.size());
+    }
+    if (o && !o->terms.empty() && s.n >= kSeedM - batch_bits(B)) {
+        auto pl = make_seed_plan(*o, s, true);
+        count += static_cast<int64_t>(pl->spasses.size());
+    }
+    return count;
+}
 
 bool fused_obs_apply(const DevState& psi, const DevState& phi, Observable& o, double* d_energy) {
     const int nb = batch_bits(psi.B);

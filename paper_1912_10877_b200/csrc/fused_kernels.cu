@@ -560,26 +560,35 @@ __global__ void __launch_bounds__(1 << (M - RB), 2)
 
 // ---- gradient epilogue: partial rows -> parameter gradients (fixed order) ----------------------
 
-__global__ void k_grad_epilogue(const double* __restrict__ sums, const GradEntry* __restrict__ e, int64_t n,
-                                double* __restrict__ grads) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    for (int64_t k = 0; k < n; ++k) {
-        const GradEntry& g = e[k];
-        const cdbl* GA = reinterpret_cast<const cdbl*>(g.A);
-        if (g.type == 0) {
-            grads[g.param] += sums[g.comp];
-        } else {
-            // θ̄ = Im Σ_ab A_ab C_ab, C_ab at comp + 2(2a+b)
-            double acc = 0.0;
-            for (int a = 0; a < 2; ++a)
-                for (int b = 0; b < 2; ++b) {
-                    const cdbl A = GA[b * 2 + a];
-                    const double cr = sums[g.comp + 2 * (2 * a + b)], ci = sums[g.comp + 2 * (2 * a + b) + 1];
-                    acc += A.re * ci + A.im * cr;
-                }
-            grads[g.param] += acc;
-        }
+// one thread per gradient entry: its contribution (scalar component or Im Σ_ab A_ab C_ab)
+__global__ void k_grad_values(const double* __restrict__ sums, const GradEntry* __restrict__ e, int64_t n,
+                              double* __restrict__ vals) {
+    int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const GradEntry& g = e[k];
+    if (g.type == 0) {
+        vals[k] = sums[g.comp];
+        return;
     }
+    const cdbl* GA = reinterpret_cast<const cdbl*>(g.A);
+    double acc = 0.0;  // C_ab at comp + 2(2a+b)
+    for (int a = 0; a < 2; ++a)
+        for (int b = 0; b < 2; ++b) {
+            const cdbl A = GA[b * 2 + a];
+            const double cr = sums[g.comp + 2 * (2 * a + b)], ci = sums[g.comp + 2 * (2 * a + b) + 1];
+            acc += A.re * ci + A.im * cr;
+        }
+    vals[k] = acc;
+}
+
+// one thread per parameter: its entries (CSR, in plan order) summed in a fixed order
+__global__ void k_grad_csr(const double* __restrict__ vals, const int* __restrict__ ptr, const int* __restrict__ idx,
+                           int64_t nparams, double* __restrict__ grads) {
+    int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= nparams) return;
+    double s = 0.0;
+    for (int k = ptr[p]; k < ptr[p + 1]; ++k) s += vals[idx[k]];
+    if (ptr[p + 1] > ptr[p]) grads[p] += s;
 }
 
 __global__ void k_rows(const double* __restrict__ part, int64_t nrows, int64_t cols, double* __restrict__ out) {
@@ -653,14 +662,21 @@ __global__ void __launch_bounds__(256)
 }
 
 // E[b] = Σ_{tiles of chunk b/bc} epart[tile][b % bc]
-__global__ void k_energy(const double* __restrict__ epart, uint64_t nouter, int64_t nchunks, int64_t bc, int64_t B,
-                         double* __restrict__ e) {
-    int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (b >= B) return;
-    int64_t c = b / bc, beta = b - c * bc;
+// one block per batch column, fixed strided split + fixed tree: deterministic
+__global__ void __launch_bounds__(256) k_energy(const double* __restrict__ epart, uint64_t nouter, int64_t nchunks,
+                                                int64_t bc, int64_t B, double* __restrict__ e) {
+    const int64_t b = blockIdx.x;
+    const int64_t c = b / bc, beta = b - c * bc;
     double s = 0.0;
-    for (uint64_t o = 0; o < nouter; ++o) s += epart[(o * nchunks + c) * bc + beta];
-    e[b] = s;
+    for (uint64_t o = threadIdx.x; o < nouter; o += blockDim.x) s += epart[(o * nchunks + c) * bc + beta];
+    __shared__ double red[256];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int h = 128; h > 0; h >>= 1) {
+        if (threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) e[b] = red[0];
 }
 
 }  // namespace
@@ -710,9 +726,16 @@ void launch_grad_rows(const double* part, int64_t nrows, int64_t cols, double* s
     QBG_CUDA(cudaGetLastError());
 }
 
-void launch_grad_epilogue(const double* sums, const GradEntry* d_epi, int64_t n, double* grads) {
-    LaunchScope ls("grad_epilogue", 8.0 * n);
-    k_grad_epilogue<<<1, 32, 0, stream()>>>(sums, d_epi, n, grads);
+void launch_grad_epilogue(const double* sums, const GradEntry* d_epi, int64_t n, const int* d_ptr, const int* d_idx,
+                          int64_t nparams, double* grads) {
+    double* vals = static_cast<double*>(scratch(std::max<int64_t>(1, n) * sizeof(double), 15));
+    {
+        LaunchScope ls("grad_values", 80.0 * n);
+        k_grad_values<<<static_cast<unsigned>((n + 127) / 128), 128, 0, stream()>>>(sums, d_epi, n, vals);
+        QBG_CUDA(cudaGetLastError());
+    }
+    LaunchScope ls("grad_csr", 16.0 * n);
+    k_grad_csr<<<static_cast<unsigned>((nparams + 127) / 128), 128, 0, stream()>>>(vals, d_ptr, d_idx, nparams, grads);
     QBG_CUDA(cudaGetLastError());
 }
 
@@ -746,7 +769,7 @@ void launch_seed(int dtype, const void* psi, void* phi, const SPass& sp, const S
 
 void launch_energy(const double* epart, uint64_t nouter, int64_t nchunks, int64_t bc, int64_t B, double* e) {
     LaunchScope ls("energy", 8.0 * nouter * nchunks * bc);
-    k_energy<<<static_cast<unsigned>((B + 127) / 128), 128, 0, stream()>>>(epart, nouter, nchunks, bc, B, e);
+    k_energy<<<static_cast<unsigned>(B), 256, 0, stream()>>>(epart, nouter, nchunks, bc, B, e);
     QBG_CUDA(cudaGetLastError());
 }
 

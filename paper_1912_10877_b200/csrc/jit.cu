@@ -124,6 +124,8 @@ uint64_t fnv(const std::string& s) {
     return h;
 }
 
+size_t compile_only(const std::string& src) { return build_cubin(src, fnv(src)).size(); }
+
 bool enabled() {
     const char* e = std::getenv("QBG_JIT");
     if (e && e[0] == '0') return false;

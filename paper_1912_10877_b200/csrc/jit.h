@@ -27,6 +27,9 @@ struct Kernel {
 // handles of `names` in order.  Throws qbg::Error(QBG_ERR_INTERNAL) with the NVRTC log on failure.
 std::vector<Kernel> compile(const std::string& src, const std::vector<std::string>& names);
 
+// NVRTC only (no device): compiles `src` to an sm_100a cubin and returns its size.
+size_t compile_only(const std::string& src);
+
 // Enabled unless QBG_JIT=0 or NVRTC cannot be loaded.
 bool enabled();
 

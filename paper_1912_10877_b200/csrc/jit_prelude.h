@@ -143,9 +143,9 @@ __device__ __forceinline__ void gcross1(const V* p, const V* a, double* c) {
 #pragma unroll
     for (int u = 0; u < 2; ++u)
 #pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        c[2 * (2 * u + v)] += (double)av[u].x * pv[v].x + (double)av[u].y * pv[v].y;
-        c[2 * (2 * u + v) + 1] += (double)av[u].x * pv[v].y - (double)av[u].y * pv[v].x;
+      for (int v = 0; v < 2; ++v) {  // explicit FMA chains: 4 DFMA per complex product-accumulate
+        c[2 * (2 * u + v)] = fma((double)av[u].y, (double)pv[v].y, fma((double)av[u].x, (double)pv[v].x, c[2 * (2 * u + v)]));
+        c[2 * (2 * u + v) + 1] = fma(-(double)av[u].y, (double)pv[v].x, fma((double)av[u].x, (double)pv[v].y, c[2 * (2 * u + v) + 1]));
       }
   }
 }

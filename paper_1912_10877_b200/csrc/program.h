@@ -47,5 +47,10 @@ bool fused_backward(const DevState& psi, const DevState& adj, Program& p, double
 bool fused_obs_apply(const DevState& psi, const DevState& phi, Observable& o, double* d_energy /* B or null */);
 // passes of the most recently built forward / backward plans (0 when unfused)
 void fused_stats(const Program& p, int64_t* fwd, int64_t* bwd);
+std::string fused_plan_info(const Program& p);  // human-readable pass/stage layout
+// Host-only planner run (no device): forward + reverse plans for a 2^n x B register.
+std::string fused_plan_preview(const Program& p, int64_t B, int dtype);
+// Host-only NVRTC compile of every specialised kernel (program + observable); no device.
+int64_t fused_jit_check(const Program& p, const Observable* o, int64_t B, int dtype);
 
 }  // namespace qbg

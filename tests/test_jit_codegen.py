@@ -1,0 +1,51 @@
+"""The runtime-specialised tile kernels: the host planner runs without a device, and every
+kernel it generates compiles with NVRTC for sm_100a (no GPU needed).  CPU only."""
+import ctypes
+import re
+
+import pytest
+
+import paper_1912_10877_b200 as qb
+from paper_1912_10877_b200._capi import check, lib
+
+
+def test_plan_preview_25q_metric_workload():
+    c = qb.variational_circuit(25, 10)
+    qb.dispatch(c, "random")
+    t = qb.compile_block(c).plan_preview()
+    fwd, bwd = t.split("plan dir=2")
+    nf = len(re.findall(r"tile Q=", fwd))
+    nb = len(re.findall(r"tile Q=", bwd))
+    # the fusion planner must cover 1025 gates in far fewer passes than gates
+    assert 0 < nf <= 40 and 0 < nb <= 45, (nf, nb)
+    assert "single gate" not in t  # every gate of the variational circuit tiles
+    # every tile holds the three low (coalescing) qubits
+    assert all(q.startswith("0,1,2,") for q in re.findall(r"tile Q=([\d,]+)", t))
+
+
+@pytest.mark.parametrize("n,depth,nb,dtype", [(13, 1, 1, 0), (12, 1, 8, 1)])
+def test_generated_kernels_compile_for_sm100a(n, depth, nb, dtype):
+    c = qb.variational_circuit(n, depth)
+    qb.dispatch(c, "random")
+    p = qb.compile_block(c)
+    o = qb.compile_observable(qb.heisenberg(n))
+    k = ctypes.c_int64()
+    check(lib().qbg_jit_check(p._h, o._h, nb, dtype, ctypes.byref(k)))
+    assert k.value > 0
+
+
+def test_generic_gates_plan():
+    """Controlled / 2-qubit / multi-qubit diagonal gates all lower to tile ops (no fallbacks)."""
+    n = 14
+    blocks = [qb.put(n, (3, 9), qb.rot(qb.kron(qb.X, qb.X), 0.3)),
+              qb.control(n, (2, -5), 13, qb.shift(0.2)),
+              qb.put(n, (1, 14), qb.rot(qb.kron(qb.Z, qb.Z), 0.7)),
+              qb.control(n, 7, 8, qb.Ry(0.1)),
+              qb.put(n, 4, qb.H)]
+    c = qb.chain(n, *blocks)
+    p = qb.compile_block(c)
+    t = p.plan_preview()
+    assert "single gate" not in t
+    k = ctypes.c_int64()
+    check(lib().qbg_jit_check(p._h, None, 1, 0, ctypes.byref(k)))
+    assert k.value > 0
