@@ -190,6 +190,12 @@ int qbg_measure_collapse(qbg_reg* reg, qbg_rng* rng, uint64_t* out /* nbatch */)
 int qbg_focus(qbg_reg* reg, const int32_t* locs, int32_t nloc);
 int qbg_relax(qbg_reg* reg, const int32_t* locs, int32_t nloc, int32_t to_nactive);
 
+/* ---- state files: Register::save / load, register.hpp:181-205 ------------------------------
+   "QBREG1\0\0", u64 nqubits, u64 nactive, u64 nbatch, then the amplitudes in the reference
+   layout (batch slowest) as little-endian complex doubles.  Files interchange with qblock. */
+int qbg_save(const qbg_reg* reg, const char* path);
+int qbg_load(const char* path, uint64_t seed, int32_t dtype, qbg_reg** out);
+
 /* ---- gate programs: apply(reg, block) lowered to instruct, SPEC.md:315-323 --------------- */
 int qbg_prog_create(int32_t nqubits, const qbg_op* ops, int64_t nops, const double* vals,
                     int64_t nvals, const int64_t* perms, int64_t nperms, qbg_prog** out);

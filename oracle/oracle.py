@@ -46,6 +46,8 @@ class Oracle:
             "orc_focus": (c_int, [P, c_int, c_int64, P, c_int]), "orc_relax": (c_int, [P, c_int, c_int64, P, c_int]),
             "orc_backward": (c_int, [P, P, c_int, c_int64, P, c_int64, P, P, P, P]),
             "orc_set_threads": (None, [c_int]), "orc_last_kernel_seconds": (c_double, []),
+            "orc_save": (c_int, [P, c_int, c_int, c_int64, c_char_p]),
+            "orc_load": (c_int, [c_char_p, P, c_int64, POINTER(c_int), POINTER(c_int), POINTER(c_int64)]),
         }
         for k, (r, a) in sig.items():
             f = getattr(L, k)
@@ -140,6 +142,17 @@ class Oracle:
         th = np.ascontiguousarray(theta if len(theta) else [0.0], dtype=np.float64)
         self._chk(self.L.orc_backward(psi.ctypes.data, phi.ctypes.data, n, psi.shape[0], ops, len(em.ops),
                                       vals.ctypes.data, perms.ctypes.data, th.ctypes.data, grads.ctypes.data))
+
+    def save(self, st, n, nactive, path):
+        st = np.ascontiguousarray(st, dtype=np.complex128)
+        self._chk(self.L.orc_save(st.ctypes.data, n, nactive, st.shape[0], str(path).encode()))
+
+    def load(self, path, cap=1 << 22):
+        buf = np.empty(cap, dtype=np.complex128)
+        n, na, B = c_int(), c_int(), c_int64()
+        self._chk(self.L.orc_load(str(path).encode(), buf.ctypes.data, cap, ctypes.byref(n), ctypes.byref(na),
+                                  ctypes.byref(B)))
+        return buf[: (1 << n.value) * B.value].reshape(B.value, 1 << n.value).copy(), n.value, na.value
 
     def last_kernel_seconds(self) -> float:
         """Compute time of the last apply_program / obs_apply / backward call, excluding the

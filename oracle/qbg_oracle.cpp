@@ -24,6 +24,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <random>
 #include <string>
@@ -536,6 +537,46 @@ int orc_measure_collapse(double* st, int n, int nactive, std::int64_t B, void* r
             for (std::size_t i = 0; i < rows; ++i) sl[e * rows + i] = i == hit ? sl[e * rows + i] * inv : cd(0.0);
         out[b] = hit;
     }
+    return QBG_OK;
+}
+
+// ---- state files (register.hpp:181-205): "QBREG1\0\0", 3 x u64, raw complex doubles ------------------
+int orc_save(const double* st, int n, int nactive, std::int64_t B, const char* path) {
+    FILE* f = std::fopen(path, "wb");
+    if (!f) return fail(QBG_ERR_SERIALIZATION, "state file: cannot open");
+    const char magic[8] = {'Q', 'B', 'R', 'E', 'G', '1', 0, 0};
+    std::uint64_t hdr[3] = {static_cast<std::uint64_t>(n), static_cast<std::uint64_t>(nactive),
+                            static_cast<std::uint64_t>(B)};
+    std::size_t cnt = (std::size_t{1} << n) * static_cast<std::size_t>(B) * 2;
+    bool ok = std::fwrite(magic, 1, 8, f) == 8 && std::fwrite(hdr, 8, 3, f) == 3 && std::fwrite(st, 8, cnt, f) == cnt;
+    ok = std::fclose(f) == 0 && ok;
+    return ok ? QBG_OK : fail(QBG_ERR_SERIALIZATION, "state file: write failed");
+}
+
+int orc_load(const char* path, double* st, std::int64_t cap, int* n, int* nactive, std::int64_t* B) {
+    FILE* f = std::fopen(path, "rb");
+    if (!f) return fail(QBG_ERR_SERIALIZATION, "state file: cannot open");
+    char magic[8];
+    std::uint64_t hdr[3];
+    if (std::fread(magic, 1, 8, f) != 8 || std::memcmp(magic, "QBREG1\0\0", 8) != 0) {
+        std::fclose(f);
+        return fail(QBG_ERR_SERIALIZATION, "state file: bad magic");
+    }
+    if (std::fread(hdr, 8, 3, f) != 3 || hdr[0] < 1 || hdr[1] > hdr[0]) {
+        std::fclose(f);
+        return fail(QBG_ERR_SERIALIZATION, "state file: bad header");
+    }
+    std::size_t cnt = (std::size_t{1} << hdr[0]) * hdr[2];
+    if (static_cast<std::int64_t>(cnt) > cap) {
+        std::fclose(f);
+        return fail(QBG_ERR_SHAPE, "orc_load: buffer too small");
+    }
+    bool ok = std::fread(st, 16, cnt, f) == cnt;
+    std::fclose(f);
+    if (!ok) return fail(QBG_ERR_SERIALIZATION, "state file: truncated amplitudes");
+    *n = static_cast<int>(hdr[0]);
+    *nactive = static_cast<int>(hdr[1]);
+    *B = static_cast<std::int64_t>(hdr[2]);
     return QBG_OK;
 }
 

@@ -14,6 +14,7 @@
 #include <chrono>
 #include <complex>
 #include <cstring>
+#include <fstream>
 #include <string>
 #include <vector>
 
@@ -363,6 +364,32 @@ int orc_measure_collapse(double* st, int n, int nactive, std::int64_t B, void* r
         auto res = qblock::measure_collapse(r, *static_cast<qblock::Rng*>(rng));
         for (std::size_t k = 0; k < res.samples.size(); ++k) out[k] = res.samples[k].value;
         from_reg(r, st);
+    });
+}
+
+// Register::save / load (register.hpp:181-205), for file interchange tests
+int orc_save(const double* st, int n, int nactive, std::int64_t B, const char* path) {
+    return guarded([&] {
+        qblock::set_qubit_cap(63);
+        qblock::Register r(static_cast<std::size_t>(n), static_cast<std::size_t>(B), 42);
+        to_reg(r, st);
+        pin_active(r, nactive);
+        std::ofstream f(path, std::ios::binary);
+        r.save(f);
+    });
+}
+
+int orc_load(const char* path, double* st, std::int64_t cap, int* n, int* nactive, std::int64_t* B) {
+    return guarded([&] {
+        qblock::set_qubit_cap(63);
+        std::ifstream f(path, std::ios::binary);
+        auto r = qblock::Register::load(f);
+        *n = static_cast<int>(r.nqubits());
+        *nactive = static_cast<int>(r.nactive());
+        *B = static_cast<std::int64_t>(r.nbatch());
+        auto a = r.amplitudes();
+        if (static_cast<std::int64_t>(a.size()) > cap) throw qblock::ShapeError("orc_load: buffer too small");
+        std::memcpy(st, a.data(), a.size() * sizeof(cplx));
     });
 }
 

@@ -93,6 +93,7 @@ def lib() -> ctypes.CDLL:
         "qbg_measure": (c_int32, [P, c_int64, P, P]), "qbg_measure_collapse": (c_int32, [P, P, P]),
         "qbg_focus": (c_int32, [P, POINTER(c_int32), c_int32]),
         "qbg_relax": (c_int32, [P, POINTER(c_int32), c_int32, c_int32]),
+        "qbg_save": (c_int32, [P, c_char_p]), "qbg_load": (c_int32, [c_char_p, c_uint64, c_int32, POINTER(P)]),
         "qbg_prog_create": (c_int32, [c_int32, POINTER(QbgOp), c_int64, P, c_int64, P, c_int64, POINTER(P)]),
         "qbg_prog_destroy": (c_int32, [P]), "qbg_prog_nparams": (c_int64, [P]),
         "qbg_prog_set_params": (c_int32, [P, P, c_int64]),

@@ -66,6 +66,34 @@ def expect_grad(obs: Block, pair, want_state_grad: bool = False, inplace: bool =
     return GradResult(energies, grads[: p.nparams], sg)
 
 
+def faithful_grad(obs: Block, pair) -> np.ndarray:
+    """Parameter-shift ("faithful") gradient, exact mode (PAPER eq. shiftrule):
+    θ̄_k = ½(⟨O⟩_{θ_k+π/2} − ⟨O⟩_{θ_k−π/2}), summed over the batch.  Every parameter must belong to
+    a Rotation with a reflexive generator; Shift / Phase parameters raise UnsupportedError.
+    2P device evaluations of the circuit (the forward-mode cost the paper contrasts with AD)."""
+    from .blocks import Rotation, dispatch, parameter_nodes, parameters
+    reg, circuit = pair
+    nodes = parameter_nodes(circuit)
+    for nd in nodes:
+        if not isinstance(nd, Rotation):
+            raise errors.UnsupportedError("faithful_grad: shift rule needs Rotation parameters only")
+    theta = parameters(circuit)
+    grads = np.empty(theta.size)
+    try:
+        for k in range(theta.size):
+            t = theta.copy()
+            t[k] = theta[k] + np.pi / 2
+            dispatch(circuit, t)
+            ep = float(np.sum(expect(obs, (reg, circuit))))
+            t[k] = theta[k] - np.pi / 2
+            dispatch(circuit, t)
+            em = float(np.sum(expect(obs, (reg, circuit))))
+            grads[k] = 0.5 * (ep - em)
+    finally:
+        dispatch(circuit, theta)
+    return grads
+
+
 def backward(psi: Register, adj: Register, circuit: Block, grads: np.ndarray | None = None) -> np.ndarray:
     """apply_back through a whole circuit: uncomputes psi, back-propagates
     adj, and adds the parameter gradient into ``grads``."""

@@ -917,6 +917,58 @@ int qbg_relax(qbg_reg* r, const int32_t* locs, int32_t nloc, int32_t to_nactive)
     });
 }
 
+// ---- state files (register.hpp:181-205) -------------------------------------------------------------
+int qbg_save(const qbg_reg* r, const char* path) {
+    return guarded([&] {
+        check_reg(r);
+        std::vector<double> host(2 * r->s.count());
+        int rc = qbg_download(r, host.data(), static_cast<int64_t>(r->s.count()));
+        if (rc) raise(rc, g_err);
+        FILE* f = std::fopen(path, "wb");
+        if (!f) raise(QBG_ERR_SERIALIZATION, std::string("state file: cannot open ") + path);
+        const char magic[8] = {'Q', 'B', 'R', 'E', 'G', '1', 0, 0};
+        uint64_t hdr[3] = {static_cast<uint64_t>(r->s.n), static_cast<uint64_t>(r->nactive),
+                           static_cast<uint64_t>(r->s.B)};
+        bool ok = std::fwrite(magic, 1, 8, f) == 8 && std::fwrite(hdr, 8, 3, f) == 3 &&
+                  std::fwrite(host.data(), sizeof(double), host.size(), f) == host.size();
+        ok = (std::fclose(f) == 0) && ok;
+        if (!ok) raise(QBG_ERR_SERIALIZATION, "state file: write failed");
+    });
+}
+
+int qbg_load(const char* path, uint64_t seed, int32_t dtype, qbg_reg** out) {
+    return guarded([&] {
+        FILE* f = std::fopen(path, "rb");
+        if (!f) raise(QBG_ERR_SERIALIZATION, std::string("state file: cannot open ") + path);
+        char magic[8];
+        uint64_t hdr[3];
+        bool ok = std::fread(magic, 1, 8, f) == 8 && std::memcmp(magic, "QBREG1\0\0", 8) == 0;
+        if (!ok) {
+            std::fclose(f);
+            raise(QBG_ERR_SERIALIZATION, "state file: bad magic");
+        }
+        if (std::fread(hdr, 8, 3, f) != 3 || hdr[0] < 1 || hdr[1] > hdr[0] || hdr[0] > 62 || hdr[2] < 1) {
+            std::fclose(f);
+            raise(QBG_ERR_SERIALIZATION, "state file: bad header");
+        }
+        std::vector<double> host(2 * (uint64_t{1} << hdr[0]) * hdr[2]);
+        bool full = std::fread(host.data(), sizeof(double), host.size(), f) == host.size();
+        std::fclose(f);
+        if (!full) raise(QBG_ERR_SERIALIZATION, "state file: truncated amplitudes");
+        qbg_reg* r = nullptr;
+        int rc = qbg_reg_create(static_cast<int32_t>(hdr[0]), static_cast<int64_t>(hdr[2]), dtype, seed, &r);
+        if (rc) raise(rc, g_err);
+        rc = qbg_upload(r, host.data(), static_cast<int64_t>(host.size() / 2));
+        if (rc) {
+            qbg_reg_destroy(r);
+            raise(rc, g_err);
+        }
+        r->nactive = static_cast<int>(hdr[1]);
+        stream_sync();
+        *out = r;
+    });
+}
+
 // ---- programs -----------------------------------------------------------------------------------------
 int qbg_prog_create(int32_t n, const qbg_op* ops, int64_t nops, const double* vals, int64_t nvals,
                     const int64_t* perms, int64_t nperms, qbg_prog** out) {

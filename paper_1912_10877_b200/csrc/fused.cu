@@ -45,6 +45,47 @@ constexpr int kFwdM = 12, kFwdRB = 4;  // 4096-element tiles, 256 threads x 16 r
 constexpr int kBwdM = 11, kBwdRB = 3;  // two states: 2048-element tiles, 256 threads x 2x8
 constexpr int kSeedM = 12;
 
+// Tile geometry of a direction: M local bits, RB register bits, `coal` low qubit bits every
+// tile must hold so that loads/stores are contiguous (3 = 128-B runs at complex128).  The
+// interpreter kernels exist for the defaults only; other geometries need the JIT path.
+// Overridable for tuning: QBG_FWD_M / QBG_FWD_RB / QBG_BWD_M / QBG_BWD_RB / QBG_COALESCE.
+struct Geo {
+    int M, RB, coal;
+};
+int env_int(const char* k, int d) {
+    const char* e = std::getenv(k);
+    return (e && *e) ? std::atoi(e) : d;
+}
+Geo geo_for(int dir);
+bool prefetch_enabled() {
+    static const bool on = env_int("QBG_PREFETCH", 0) != 0;
+    return on;
+}
+// Specialised-kernel defaults (measured on B200, 25q apply+grad, tools/sweep.py logs in
+// profiles/): forward 2^11-element tiles of 128 threads x 16 registers, 3 CTAs/SM; reverse
+// 2^11 x 2 states of 128 threads x 2x16, 2 CTAs/SM.  The interpreter keeps (12,4) / (11,3).
+constexpr int kJitFwdM = 11, kJitFwdRB = 4, kJitFwdMinB = 3;
+constexpr int kJitBwdM = 11, kJitBwdRB = 4, kJitBwdMinB = 2;
+int ctas_per_sm(bool back, int threads) {
+    static const int f = env_int("QBG_FWD_MINB", 0), b = env_int("QBG_BWD_MINB", 0);
+    const int o = back ? b : f;
+    if (o > 0) return o;
+    if (jit::enabled()) {
+        const Geo g = geo_for(back ? 2 : 0);
+        if (!back && g.M == kJitFwdM && g.RB == kJitFwdRB) return kJitFwdMinB;
+        if (back && g.M == kJitBwdM && g.RB == kJitBwdRB) return kJitBwdMinB;
+    }
+    return threads >= 512 ? 1 : 2;
+}
+Geo geo_for(int dir) {
+    const bool j = jit::enabled();
+    static const Geo f{env_int("QBG_FWD_M", j ? kJitFwdM : kFwdM), env_int("QBG_FWD_RB", j ? kJitFwdRB : kFwdRB),
+                       env_int("QBG_COALESCE", 3)};
+    static const Geo b{env_int("QBG_BWD_M", j ? kJitBwdM : kBwdM), env_int("QBG_BWD_RB", j ? kJitBwdRB : kBwdRB),
+                       env_int("QBG_COALESCE", 3)};
+    return dir == 2 ? b : f;
+}
+
 inline uint32_t swz(uint32_t l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9) ^ (l >> 12) ^ (l >> 15)) & 7u); }
 
 struct RunGrad {  // one gradient of a fused rotation run: θ̄ = Im Σ A_ab C_ab
@@ -189,6 +230,7 @@ struct FusedPlan {
     int* d_ptr = nullptr;
     int* d_idx = nullptr;
     int64_t tile_passes = 0;
+    int M = 0, RB = 0;  // tile geometry of this plan
     // observable seed
     std::vector<SPass> spasses;
     std::vector<SGroup> groups;
@@ -257,12 +299,12 @@ void gate_cost(const PG& g, int& ops, int& mats, int& comps) {
 
 // Greedy pass construction (see fused.h): a gate joins the pass when it does not conflict with
 // any gate already passed over and its non-diagonal targets fit in the tile qubit set.
-void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward) {
+void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal = 3) {
     const int n = pl.n;
     const int mq = M - nb;
     const uint64_t full = n >= 64 ? ~uint64_t{0} : (uint64_t{1} << n) - 1;
     uint64_t Qc = 0;  // coalescing: local bits 0..2 must be contiguous in memory
-    for (int b = 0; b < 3 - nb; ++b) Qc |= uint64_t{1} << b;
+    for (int b = 0; b < coal - nb; ++b) Qc |= uint64_t{1} << b;
     std::vector<int> remaining(pl.gates.size());
     for (size_t i = 0; i < remaining.size(); ++i) remaining[i] = static_cast<int>(i);
     auto tileable = [&](const PG& g) { return g.gate().t <= 2 || is_diagonal(g.gate()); };
@@ -370,7 +412,8 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward) {
             std::merge(back.begin(), back.end(), remaining.begin(), remaining.end(), std::back_inserter(merged));
             remaining = merged;
         }
-        const uint32_t C = 7u;  // coalescing / bank lane bits
+        // coalescing lane bits of the load / store layouts: the batch bits and the low qubits
+        const uint32_t C = (1u << std::max(coal, nb)) - 1;
         const uint32_t qbits = ((1u << M) - 1) & ~((1u << nb) - 1);
         auto fill = [&](uint32_t S) {
             for (int b = M - 1; b >= 0 && __builtin_popcount(S) < R; --b)
@@ -416,16 +459,22 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward) {
                 for (int b = 0; b < M; ++b)
                     if (!((sp.S >> b) & 1)) avail.push_back(b);
                 std::vector<int> order;
-                if ((sp.S & C) == 0) {
-                    order = {0, 1, 2};
-                } else {
-                    bool used[3] = {false, false, false};
-                    for (int b : avail)
-                        if (!used[b % 3] && order.size() < 3) {
-                            used[b % 3] = true;
+                // lanes 0..2 first: the coalescing bits when they are thread bits, completed to
+                // three bits of distinct (bit mod 3) so the swizzled 16-B accesses of a quarter
+                // warp hit 8 distinct bank groups
+                bool used[3] = {false, false, false};
+                if ((sp.S & C) == 0)
+                    for (int b = 0; b < 32 && order.size() < 3; ++b)
+                        if ((C >> b) & 1) {
                             order.push_back(b);
+                            used[b % 3] = true;
                         }
-                }
+                for (int b : avail)
+                    if (!used[b % 3] && order.size() < 3 &&
+                        std::find(order.begin(), order.end(), b) == order.end()) {
+                        used[b % 3] = true;
+                        order.push_back(b);
+                    }
                 for (int b : avail)
                     if (std::find(order.begin(), order.end(), b) == order.end()) order.push_back(b);
                 for (int p = 0; p < Wn; ++p) thrb[p] = order[p];
@@ -613,15 +662,26 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
     const int CS = NW + 1;  // gradient cell stride (odd: the 8 lanes of a warp_sum8 hit distinct banks)
     const size_t elem = c128 ? 16 : 8;
     std::ostringstream s;
-    s << "extern \"C\" __global__ void __launch_bounds__(" << TH << ", 2) __NAME__(" << (c128 ? "c128" : "c64")
+    // two resident CTAs of 256 threads (128 registers each) or one of 512 (QBG_*_MINB overrides)
+    s << "extern \"C\" __global__ void __launch_bounds__(" << TH << ", " << ctas_per_sm(back, TH) << ") __NAME__("
+      << (c128 ? "c128" : "c64")
       << "* __restrict__ psi, " << (c128 ? "c128" : "c64")
       << "* __restrict__ adj, double* __restrict__ gpart, long long gcols, int gbase, const __grid_constant__ PM<"
       << (c128 ? "double" : "float") << ", " << std::max(2, 2 * nmats) << "> pm) {\n";
     s << "typedef " << (c128 ? "c128" : "c64") << " V;\nconstexpr int R = " << R << ";\nconst int tid = threadIdx.x;\n";
     s << "#define MV(i) mk<V>(pm.m[2 * (i)], pm.m[2 * (i) + 1])\n";
-    s << "extern __shared__ __align__(16) unsigned char smraw[];\nV* sx = (V*)smraw;\nV* sy = sx + " << (1 << M) << ";\n";
+    // prefetch mode: tile t+1 is copied global -> shared (cp.async, in the stage-0 layout) while
+    // tile t computes; two tile buffers alternate
+    const bool pf = prefetch_enabled();
+    const size_t tile_bytes = (back ? 2 : 1) * (elem << M);
+    const size_t nbuf = pf ? 2 : 1;
+    s << "extern __shared__ __align__(16) unsigned char smraw[];\n";
+    if (pf)
+        s << "V* sbase = (V*)smraw;\n";
+    else
+        s << "V* sx = (V*)smraw;\nV* sy = sx + " << (1 << M) << ";\n";
     if (back) {
-        s << "double* sg = (double*)(smraw + " << 2 * (elem << M) << ");\n";
+        s << "double* sg = (double*)(smraw + " << nbuf * tile_bytes << ");\n";
         s << "for (int i = tid; i < " << P.ngrad * CS << "; i += " << TH << ") sg[i] = 0.0;\n__syncthreads();\n";
         s << "const int warp = tid >> 5, lane = tid & 31;\n";
     }
@@ -632,17 +692,18 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
     s << "const i64 gL = " << tid_sum(SL.gthr, W, false) << ";\n";
     for (int k = 0; k < P.nstages; ++k) s << "const unsigned st" << k << " = " << tid_sum(P.st[k].sthr, W, true) << ";\n";
     s << "V x[R];\n" << (back ? "V y[R];\n" : "");
-    s << "for (u64 tile = blockIdx.x; tile < " << P.ntiles << "ull; tile += gridDim.x) {\n";
+    // tile id -> (outer index, element base)
+    s << "auto tile_geo = [&](u64 tile, u64& outer, i64& tb) {\n";
     if (P.nchunks == 1)
         s << "const u64 o = tile; const u64 c = 0;\n";
     else
         s << "const u64 o = tile / " << P.nchunks << "ull; const u64 c = tile - o * " << P.nchunks << "ull;\n";
-    s << "u64 outer = o;\n";
+    s << "outer = o;\n";
     for (int k = 0; k < P.mq; ++k) {
         int p = P.qpos[k];
         s << "outer = ((outer >> " << p << ") << " << p + 1 << ") | (outer & " << hex((uint64_t{1} << p) - 1) << ");\n";
     }
-    s << "const i64 tb = (i64)outer * " << P.B << "ll + (i64)c * " << (int64_t{1} << P.nb) << "ll;\n";
+    s << "tb = (i64)outer * " << P.B << "ll + (i64)c * " << (int64_t{1} << P.nb) << "ll;\n};\n";
     auto goff = [&](const DStage& S, int j) {
         int64_t o = 0;
         for (int k = 0; k < RB; ++k)
@@ -655,14 +716,59 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             if ((j >> k) & 1) o ^= S.sreg[k];
         return o;
     };
-    for (int j = 0; j < R; ++j) {
-        s << "x[" << j << "] = psi[tb + g0 + " << goff(S0, j) << "ll];";
-        if (back) s << " y[" << j << "] = adj[tb + g0 + " << goff(S0, j) << "ll];";
-        s << "\n";
+    const bool skip_first = pf && P.nstages > 1 && S0.op_end == S0.op_begin;  // data already in stage-0 layout
+    if (!pf) {
+        s << "for (u64 tile = blockIdx.x; tile < " << P.ntiles << "ull; tile += gridDim.x) {\n";
+        s << "u64 outer; i64 tb; tile_geo(tile, outer, tb);\n";
+        for (int j = 0; j < R; ++j) {
+            s << "x[" << j << "] = psi[tb + g0 + " << goff(S0, j) << "ll];";
+            if (back) s << " y[" << j << "] = adj[tb + g0 + " << goff(S0, j) << "ll];";
+            s << "\n";
+        }
+    } else {
+        const size_t stride = (back ? 2 : 1) << M;  // elements per buffer
+        auto prefetch = [&](const std::string& buf, const std::string& tbv) {
+            for (int j = 0; j < R; ++j) {
+                s << "cpa(" << buf << " + (st0 ^ " << soff(S0, j) << "u), psi + " << tbv << " + g0 + " << goff(S0, j) << "ll);";
+                if (back)
+                    s << " cpa(" << buf << " + " << (1 << M) << " + (st0 ^ " << soff(S0, j) << "u), adj + " << tbv
+                      << " + g0 + " << goff(S0, j) << "ll);";
+                s << "\n";
+            }
+            s << "cp_commit();\n";
+        };
+        s << "unsigned it = 0;\n";
+        s << "if (blockIdx.x < " << P.ntiles << "ull) { u64 on; i64 tbn; tile_geo(blockIdx.x, on, tbn);\n";
+        prefetch("sbase", "tbn");
+        s << "}\n";
+        s << "for (u64 tile = blockIdx.x; tile < " << P.ntiles << "ull; tile += gridDim.x, ++it) {\n";
+        s << "u64 outer; i64 tb; tile_geo(tile, outer, tb);\n";
+        s << "V* sx = sbase + (it & 1u) * " << stride << "u; V* sy = sx + " << (1 << M) << ";\n";
+        s << "const u64 tn = tile + gridDim.x;\n";
+        s << "if (tn < " << P.ntiles << "ull) { u64 on; i64 tbn; tile_geo(tn, on, tbn); V* nx = sbase + ((it + 1u) & 1u) * "
+          << stride << "u;\n";
+        prefetch("nx", "tbn");
+        s << "cp_wait<1>(); } else { cp_wait<0>(); }\n";
+        if (!skip_first) {
+            for (int j = 0; j < R; ++j) {
+                s << "x[" << j << "] = sx[st0 ^ " << soff(S0, j) << "u];";
+                if (back) s << " y[" << j << "] = sy[st0 ^ " << soff(S0, j) << "u];";
+                s << "\n";
+            }
+        }
     }
     for (int st = 0; st < P.nstages; ++st) {
         const DStage& S = P.st[st];
-        if (st > 0) {
+        if (st == 1 && skip_first) {
+            // the prefetched buffer already holds the tile in the stage-0 layout
+            s << "__syncthreads();\n";
+            for (int j = 0; j < R; ++j) {
+                s << "x[" << j << "] = sx[st" << st << " ^ " << soff(S, j) << "u];";
+                if (back) s << " y[" << j << "] = sy[st" << st << " ^ " << soff(S, j) << "u];";
+                s << "\n";
+            }
+            s << "__syncthreads();\n";
+        } else if (st > 0) {
             const DStage& Sp = P.st[st - 1];
             for (int j = 0; j < R; ++j) {
                 s << "sx[st" << st - 1 << " ^ " << soff(Sp, j) << "u] = x[" << j << "];";
@@ -870,7 +976,8 @@ void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128, bool check_
                 f[2 * k + 1] = static_cast<float>(v.im);
             }
         }
-        st.smem = (P.nstages > 1 || back ? (back ? 2 : 1) * (elem << M) : 0) +
+        const size_t tile_bytes = (back ? 2 : 1) * (elem << M);
+        st.smem = (prefetch_enabled() ? 2 * tile_bytes : (P.nstages > 1 || back ? tile_bytes : 0)) +
                   (back ? static_cast<size_t>(P.ngrad) * (NW + 1) * 8 : 0);
     }
     if (names.empty()) return;
@@ -881,13 +988,14 @@ void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128, bool check_
 }
 
 // ---- execution ---------------------------------------------------------------------------------
-template <typename V, int M, int RB, bool BACK>
+template <typename V, bool BACK>
 void launch_jit(V* psi, V* adj, Step& st, FusedPlan& pl, double* gpart, int64_t gcols) {
-    constexpr int T = 1 << (M - RB);
+    const int T = 1 << (pl.M - pl.RB);
     const DPass& P = st.pass;
-    int64_t grid = std::min<int64_t>(static_cast<int64_t>(P.ntiles), static_cast<int64_t>(num_sms()) * 2);
+    const int per_sm = ctas_per_sm(BACK, T);
+    int64_t grid = std::min<int64_t>(static_cast<int64_t>(P.ntiles), static_cast<int64_t>(num_sms()) * per_sm);
     if (BACK) grid = std::min<int64_t>(grid, gcols);
-    double bytes = static_cast<double>(P.ntiles) * (1 << M) * sizeof(V) * (BACK ? 4.0 : 2.0);
+    double bytes = static_cast<double>(P.ntiles) * (int64_t{1} << pl.M) * sizeof(V) * (BACK ? 4.0 : 2.0);
     int gbase = P.grad_base;
     void* args[] = {&psi, &adj, &gpart, &gcols, &gbase, st.blob.data()};
     LaunchScope ls(BACK ? "fused_bwd" : "fused_fwd", bytes);
@@ -910,7 +1018,9 @@ std::shared_ptr<FusedPlan> get_plan(std::vector<std::shared_ptr<FusedPlan>>& cac
                                [&](const std::shared_ptr<FusedPlan>& c) { return c->dir == dir && c->B == s.B; }),
                 cache.end());
     auto pl = build_host_plan(p, s, dir);
-    const int M = dir == 2 ? kBwdM : kFwdM, RB = dir == 2 ? kBwdRB : kFwdRB;
+    const int M = pl->M, RB = pl->RB;
+    const bool default_geo = M == (dir == 2 ? kBwdM : kFwdM) && RB == (dir == 2 ? kBwdRB : kFwdRB);
+    if (!jit::enabled() && !default_geo) raise(QBG_ERR_UNSUPPORTED, "fused: non-default tile geometry needs the JIT");
     if (jit::enabled()) {
         try {
             jit_prepare(*pl, M, RB, dir == 2, s.dtype == QBG_C128);
@@ -969,8 +1079,10 @@ std::shared_ptr<FusedPlan> build_host_plan(const Program& p, const DevState& s, 
     }
     pl->gates = fuse_runs(std::move(gs), dir == 2);
     const int nb = batch_bits(s.B);
-    const int M = dir == 2 ? kBwdM : kFwdM, RB = dir == 2 ? kBwdRB : kFwdRB;
-    plan_passes(*pl, M, RB, nb, dir == 2);
+    const Geo g = geo_for(dir);
+    pl->M = g.M;
+    pl->RB = g.RB;
+    plan_passes(*pl, g.M, g.RB, nb, dir == 2, g.coal);
     // per-gate fallback steps with a scalar gradient get their own component rows
     for (auto& st : pl->steps)
         if (!st.tile && pl->gates[st.single].k) {
@@ -997,7 +1109,7 @@ void run_forward(const DevState& s, FusedPlan& pl) {
     for (auto& st : pl.steps) {
         if (st.tile)
             if (st.jk >= 0)
-                launch_jit<V, kFwdM, kFwdRB, false>(psi, nullptr, st, pl, nullptr, 0);
+                launch_jit<V, false>(psi, nullptr, st, pl, nullptr, 0);
             else
                 launch_interp(pl.dtype, false, psi, nullptr, st.pass, pl.d_ops, pl.d_mats, nullptr, 0);
         else
@@ -1014,7 +1126,7 @@ void run_backward(const DevState& psi, const DevState& adj, FusedPlan& pl, doubl
     for (auto& st : pl.steps) {
         if (st.tile) {
             if (st.jk >= 0)
-                launch_jit<V, kBwdM, kBwdRB, true>(static_cast<V*>(psi.ptr), static_cast<V*>(adj.ptr), st, pl, part, cols);
+                launch_jit<V, true>(static_cast<V*>(psi.ptr), static_cast<V*>(adj.ptr), st, pl, part, cols);
             else
                 launch_interp(pl.dtype, true, psi.ptr, adj.ptr, st.pass, pl.d_ops, pl.d_mats, part, cols);
         } else {
@@ -1034,7 +1146,7 @@ void run_backward(const DevState& psi, const DevState& adj, FusedPlan& pl, doubl
 }  // namespace
 
 bool fused_forward(const DevState& s, Program& p, bool adjoint) {
-    if (!fusable(s, kFwdM)) return false;
+    if (!fusable(s, geo_for(0).M)) return false;
     auto pl = get_plan(p.plans, p, s, adjoint ? 1 : 0);
     if (s.dtype == QBG_C128)
         run_forward<double2>(s, *pl);
@@ -1044,7 +1156,7 @@ bool fused_forward(const DevState& s, Program& p, bool adjoint) {
 }
 
 bool fused_backward(const DevState& psi, const DevState& adj, Program& p, double* d_grads) {
-    if (!fusable(psi, kBwdM)) return false;
+    if (!fusable(psi, geo_for(2).M)) return false;
     auto pl = get_plan(p.plans, p, psi, 2);
     if (psi.dtype == QBG_C128)
         run_backward<double2>(psi, adj, *pl, d_grads);
@@ -1075,8 +1187,8 @@ std::string fused_plan_preview(const Program& p, int64_t B, int dtype) {
     s.B = B;
     s.dtype = dtype;
     std::vector<std::shared_ptr<FusedPlan>> v;
-    if (fusable(s, kFwdM)) v.push_back(build_host_plan(p, s, 0));
-    if (fusable(s, kBwdM)) v.push_back(build_host_plan(p, s, 2));
+    if (fusable(s, geo_for(0).M)) v.push_back(build_host_plan(p, s, 0));
+    if (fusable(s, geo_for(2).M)) v.push_back(build_host_plan(p, s, 2));
     return plans_text(v);
 }
 
@@ -1382,14 +1494,14 @@ int64_t fused_jit_check(const Program& p, const Observable* o, int64_t B, int dt
     s.B = B;
     s.dtype = dtype;
     int64_t count = 0;
-    if (fusable(s, kFwdM)) {
+    if (fusable(s, geo_for(0).M)) {
         auto pl = build_host_plan(p, s, 0);
-        jit_prepare(*pl, kFwdM, kFwdRB, false, dtype == QBG_C128, true);
+        jit_prepare(*pl, pl->M, pl->RB, false, dtype == QBG_C128, true);
         count += static_cast<int64_t>(pl->steps.size());
     }
-    if (fusable(s, kBwdM)) {
+    if (fusable(s, geo_for(2).M)) {
         auto pl = build_host_plan(p, s, 2);
-        jit_prepare(*pl, kBwdM, kBwdRB, true, dtype == QBG_C128, true);
+        jit_prepare(*pl, pl->M, pl->RB, true, dtype == QBG_C128, true);
         count += static_cast<int64_t>(pl->steps.size());
     }
     if (o && !o->terms.empty() && s.n >= kSeedM - batch_bits(B)) {

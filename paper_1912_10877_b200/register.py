@@ -170,6 +170,17 @@ class Register:
         check(lib().qbg_add_scaled(self._h, other._h, f.real, f.imag))
         return self
 
+    # ---- state files (register.hpp:181-205) -------------------------------------------------------------------
+    def save(self, path: str) -> None:
+        """QBREG1 file, interchangeable with qblock::Register::save."""
+        check(lib().qbg_save(self._h, str(path).encode()))
+
+    @staticmethod
+    def load(path: str, seed: int = 42, dtype: str = "c128") -> "Register":
+        h = ctypes.c_void_p()
+        check(lib().qbg_load(str(path).encode(), seed, DTYPES[dtype], ctypes.byref(h)))
+        return Register(0, _handle=h)
+
     # ---- focus / relax (register.hpp:156-177) ---------------------------------------------------------------
     def focus(self, *locs) -> "Register":
         arr, n = i32(_flat(locs))

@@ -114,6 +114,10 @@ def main():
     st = ref.rand_state(6, 2, 21)
     foc = ref.focus(st, 6, [3, 6, 1, 2])
     np.savez(os.path.join(OUT, "focus.npz"), state=st, locs=np.array([3, 6, 1, 2]), focused=foc)
+    # 6. QBREG1 state file written by the reference (register.hpp:181-188), nactive = 3 of 4
+    st = ref.rand_state(4, 2, 33)
+    ref.save(st, 4, 3, os.path.join(OUT, "state_qbreg1.bin"))
+    np.save(os.path.join(OUT, "state_qbreg1_amps.npy"), st)
     print("golden fixtures written to", OUT)
 
 

@@ -213,6 +213,44 @@ def test_focus_then_apply_matches_reference_semantics(orc):
     assert rel(reg.state(), orc.instruct(st, 6, M.h(), [3])) < TOL
 
 
+def test_qbreg1_interchange(tmp_path):
+    """Device register <-> QBREG1 file written by the compiled reference (register.hpp:181-205)."""
+    import os
+    from conftest import GOLDEN
+    path = os.path.join(GOLDEN, "state_qbreg1.bin")
+    amps = np.load(os.path.join(GOLDEN, "state_qbreg1_amps.npy"))
+    reg = qb.Register.load(path)
+    assert (reg.nqubits, reg.nactive, reg.nbatch) == (4, 3, 2)
+    assert np.array_equal(reg.state(), amps)
+    reg.save(tmp_path / "o.bin")
+    assert open(tmp_path / "o.bin", "rb").read() == open(path, "rb").read()
+    with pytest.raises(qb.errors.SerializationError):
+        qb.Register.load(os.path.join(GOLDEN, "rng.npz"))
+
+
+@pytest.mark.parametrize("n", [5, 12])
+def test_gradient_triangle(n):
+    """reverse mode = parameter shift = central FD (1e-6) — fused path at n = 12."""
+    circ = C.variational_circuit(n, 2)
+    B.dispatch(circ, "random")
+    h = C.heisenberg(n)
+    reg = qb.zero_state(n)
+    rev = qb.expect_grad(h, (reg, circ)).param_grads
+    shift = qb.faithful_grad(h, (reg, circ))
+    np.testing.assert_allclose(rev, shift, atol=1e-10, rtol=0)
+    th = B.parameters(circ)
+    for k in range(0, th.size, max(1, th.size // 6)):
+        tp, tm = th.copy(), th.copy()
+        tp[k] += 1e-4
+        tm[k] -= 1e-4
+        B.dispatch(circ, tp)
+        ep = qb.expect(h, (reg, circ))[0]
+        B.dispatch(circ, tm)
+        em = qb.expect(h, (reg, circ))[0]
+        assert abs((ep - em) / 2e-4 - rev[k]) < 1e-6
+    B.dispatch(circ, th)
+
+
 def test_register_algebra(orc):
     a = orc.rand_state(9, 3, 1)
     b = orc.rand_state(9, 3, 2)

@@ -103,6 +103,19 @@ def test_focus_relax_goldens(orc, golden):
     assert np.array_equal(orc.relax(f, 6, locs), g["state"])
 
 
+def test_qbreg1_interchange(orc, golden, tmp_path):
+    """register.hpp:181-205: the file the reference wrote loads bit-exactly; ours is byte-identical."""
+    import os
+    from conftest import GOLDEN
+    path = os.path.join(GOLDEN, "state_qbreg1.bin")
+    amps = np.load(os.path.join(GOLDEN, "state_qbreg1_amps.npy"))
+    st, n, na = orc.load(path)
+    assert (n, na) == (4, 3) and np.array_equal(st, amps)
+    out = tmp_path / "o.bin"
+    orc.save(amps, 4, 3, out)
+    assert open(out, "rb").read() == open(path, "rb").read()
+
+
 def test_validation_order(orc):
     st = O.Oracle.zero_state(3)
     with pytest.raises(O.OracleError) as e:
