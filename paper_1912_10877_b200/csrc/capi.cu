@@ -1118,10 +1118,15 @@ int qbg_expect(const qbg_reg* r, const qbg_obs* o, double* out) {
     return guarded([&] {
         check_reg(r);
         if (o->o.n != r->nactive) raise(QBG_ERR_SHAPE, "observable qubit count differs from active qubits");
-        DevState phi = r->s;
-        phi.ptr = scratch(r->s.bytes(), 9);
         double* e = static_cast<double*>(scratch(r->s.B * sizeof(double), 10));
-        run_obs(r->s, phi, const_cast<qbg_obs*>(o)->o, e);
+        // energy-only fused seed: no second full state (a 33-qubit register is 128 GiB)
+        DevState none = r->s;
+        none.ptr = nullptr;
+        if (!(g_fusion && fused_obs_apply(r->s, none, const_cast<qbg_obs*>(o)->o, e))) {
+            DevState phi = r->s;
+            phi.ptr = scratch(r->s.bytes(), 9);
+            run_obs(r->s, phi, const_cast<qbg_obs*>(o)->o, e);
+        }
         QBG_CUDA(cudaMemcpyAsync(out, e, r->s.B * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
         stream_sync();
     });

@@ -230,7 +230,8 @@ struct FusedPlan {
     int* d_ptr = nullptr;
     int* d_idx = nullptr;
     int64_t tile_passes = 0;
-    int M = 0, RB = 0;  // tile geometry of this plan
+    int M = 0, RB = 0;         // tile geometry of this plan
+    bool energy_only = false;  // seed plans: <O> without materialising φ = Oψ
     // observable seed
     std::vector<SPass> spasses;
     std::vector<SGroup> groups;
@@ -1218,23 +1219,24 @@ std::string plans_text(const std::vector<std::shared_ptr<FusedPlan>>& plans) {
 // ---- observable seed ------------------------------------------------------------------------------
 namespace {
 
-std::shared_ptr<FusedPlan> make_seed_plan(const Observable& o, const DevState& s, bool check_only);
+std::shared_ptr<FusedPlan> make_seed_plan(const Observable& o, const DevState& s, bool check_only, bool energy_only);
 void seed_jit_prepare(FusedPlan& pl, bool c128, bool check_only);
 
-std::shared_ptr<FusedPlan> get_seed_plan(Observable& o, const DevState& s) {
+std::shared_ptr<FusedPlan> get_seed_plan(Observable& o, const DevState& s, bool energy_only) {
     for (auto& c : o.plans)
-        if (c->B == s.B && c->dtype == s.dtype && c->n == s.n) return c;
-    auto pl = make_seed_plan(o, s, false);
+        if (c->B == s.B && c->dtype == s.dtype && c->n == s.n && c->energy_only == energy_only) return c;
+    auto pl = make_seed_plan(o, s, false, energy_only);
     o.plans.push_back(pl);
     return pl;
 }
 
-std::shared_ptr<FusedPlan> make_seed_plan(const Observable& o, const DevState& s, bool check_only) {
+std::shared_ptr<FusedPlan> make_seed_plan(const Observable& o, const DevState& s, bool check_only, bool energy_only) {
     auto pl = std::make_shared<FusedPlan>();
     pl->B = s.B;
     pl->dtype = s.dtype;
     pl->n = s.n;
     pl->dir = 3;
+    pl->energy_only = energy_only;
     const int nb = batch_bits(s.B);
     const int mq = kSeedM - nb;
     const int n = s.n;
@@ -1326,7 +1328,10 @@ std::shared_ptr<FusedPlan> make_seed_plan(const Observable& o, const DevState& s
 // and term Z supports z_t:  φ̄_l += Σ_t c_t (-1)^{|src & z_t|} ψ_src,  src = l ^ x.  The parity
 // splits into a thread/tile part (per thread, once per tile) and a k part (compile time), and
 // terms with equal k-part Z mask are pre-summed per thread.
-std::string gen_seed(const SPass& sp, const std::vector<SGroup>& groups, const std::vector<STerm>& terms, bool c128) {
+// energy_only: every pass starts from zero and contributes Re Σ conj(ψ_l) (O_pass ψ)_l to the energy
+// directly (the groups' contributions are independent), so φ is never written.
+std::string gen_seed(const SPass& sp, const std::vector<SGroup>& groups, const std::vector<STerm>& terms, bool c128,
+                     bool energy_only) {
     constexpr int M = kSeedM, TB = 8, T = 1 << TB, R = 1 << (M - TB);
     const int64_t bc = int64_t{1} << sp.nb;
     std::ostringstream s;
@@ -1364,7 +1369,7 @@ std::string gen_seed(const SPass& sp, const std::vector<SGroup>& groups, const s
     s << "__syncthreads();\n";
     for (int k = 0; k < R; ++k) s << "sp[tid + " << k * T << "] = psi[tb + " << goff(static_cast<uint32_t>(k) << TB) << "ll];\n";
     for (int k = 0; k < R; ++k) {
-        if (sp.first)
+        if (sp.first || energy_only)
             s << "acc[" << k << "] = mk<V>(0, 0);\n";
         else
             s << "acc[" << k << "] = phi[tb + " << goff(static_cast<uint32_t>(k) << TB) << "ll];\n";
@@ -1405,8 +1410,9 @@ std::string gen_seed(const SPass& sp, const std::vector<SGroup>& groups, const s
         s << "}\n";
         tix += g.term_end - g.term_begin;
     }
-    for (int k = 0; k < R; ++k) s << "phi[tb + " << goff(static_cast<uint32_t>(k) << TB) << "ll] = acc[" << k << "];\n";
-    if (sp.last) {
+    if (!energy_only)
+        for (int k = 0; k < R; ++k) s << "phi[tb + " << goff(static_cast<uint32_t>(k) << TB) << "ll] = acc[" << k << "];\n";
+    if (sp.last || energy_only) {
         s << "double e = 0.0;\n";
         for (int k = 0; k < R; ++k)
             s << "{ const V p = sp[tid + " << k * T << "]; e += (double)p.x * acc[" << k << "].x + (double)p.y * acc[" << k
@@ -1426,7 +1432,7 @@ void seed_jit_prepare(FusedPlan& pl, bool c128, bool check_only) {
     pl.sjk.clear();
     pl.sblob.clear();
     for (auto& sp : pl.spasses) {
-        std::string body = gen_seed(sp, pl.groups, pl.terms, c128);
+        std::string body = gen_seed(sp, pl.groups, pl.terms, c128, pl.energy_only);
         uint64_t h = jit::fnv(body);
         auto it = uniq.find(h);
         if (it == uniq.end()) {
@@ -1465,15 +1471,18 @@ void seed_jit_prepare(FusedPlan& pl, bool c128, bool check_only) {
 void run_seed(const DevState& psi, const DevState& phi, FusedPlan& pl, double* d_energy) {
     const SPass& last = pl.spasses.back();
     const int64_t bc = int64_t{1} << last.nb;
-    double* epart = static_cast<double*>(scratch(last.ntiles * bc * sizeof(double), 14));
+    const int64_t per_pass = static_cast<int64_t>(last.ntiles) * bc;
+    const int64_t npart = pl.energy_only ? static_cast<int64_t>(pl.spasses.size()) : 1;
+    double* epart = static_cast<double*>(scratch(npart * per_pass * sizeof(double), 14));
     if (!pl.sjk.empty()) {
         for (size_t k = 0; k < pl.spasses.size(); ++k) {
             const SPass& sp = pl.spasses[k];
             const void* pp = psi.ptr;
             void* qq = phi.ptr;
-            void* args[] = {&pp, &qq, &epart, pl.sblob[k].data()};
+            double* ep = epart + (pl.energy_only ? static_cast<int64_t>(k) * per_pass : 0);
+            void* args[] = {&pp, &qq, &ep, pl.sblob[k].data()};
             int64_t grid = std::min<int64_t>(static_cast<int64_t>(sp.ntiles), static_cast<int64_t>(num_sms()) * 2);
-            LaunchScope ls("seed", (sp.first ? 2.0 : 3.0) * psi.bytes());
+            LaunchScope ls("seed", (pl.energy_only ? 1.0 : sp.first ? 2.0 : 3.0) * psi.bytes());
             jit::launch(pl.jk[pl.sjk[k]], static_cast<unsigned>(grid), 256, psi.elem() << kSeedM, args);
         }
     } else {
@@ -1481,7 +1490,10 @@ void run_seed(const DevState& psi, const DevState& phi, FusedPlan& pl, double* d
             launch_seed(psi.dtype, psi.ptr, phi.ptr, sp, pl.d_groups, pl.d_terms, epart,
                         (sp.first ? 2.0 : 3.0) * psi.bytes());
     }
-    if (d_energy) launch_energy(epart, uint64_t{1} << (pl.n - last.mq), last.nchunks, bc, psi.B, d_energy);
+    // energy-only passes each left their own partials: sum them as extra "outer" tiles
+    if (d_energy)
+        launch_energy(epart, (uint64_t{1} << (pl.n - last.mq)) * static_cast<uint64_t>(npart), last.nchunks, bc, psi.B,
+                      d_energy);
 }
 
 }  // namespace
@@ -1505,7 +1517,7 @@ int64_t fused_jit_check(const Program& p, const Observable* o, int64_t B, int dt
         count += static_cast<int64_t>(pl->steps.size());
     }
     if (o && !o->terms.empty() && s.n >= kSeedM - batch_bits(B)) {
-        auto pl = make_seed_plan(*o, s, true);
+        auto pl = make_seed_plan(*o, s, true, false);
         count += static_cast<int64_t>(pl->spasses.size());
     }
     return count;
@@ -1514,11 +1526,10 @@ int64_t fused_jit_check(const Program& p, const Observable* o, int64_t B, int dt
 bool fused_obs_apply(const DevState& psi, const DevState& phi, Observable& o, double* d_energy) {
     const int nb = batch_bits(psi.B);
     if (psi.n < kSeedM - nb || o.terms.empty()) return false;
-    auto pl = get_seed_plan(o, psi);
-    if (psi.dtype == QBG_C128)
-        run_seed(psi, phi, *pl, d_energy);
-    else
-        run_seed(psi, phi, *pl, d_energy);
+    const bool energy_only = phi.ptr == nullptr;
+    auto pl = get_seed_plan(o, psi, energy_only);
+    if (energy_only && pl->sjk.empty()) return false;  // the generic seed kernel needs φ
+    run_seed(psi, phi, *pl, d_energy);
     return true;
 }
 
