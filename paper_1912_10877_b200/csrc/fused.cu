@@ -57,9 +57,26 @@ int env_int(const char* k, int d) {
     return (e && *e) ? std::atoi(e) : d;
 }
 Geo geo_for(int dir);
-bool prefetch_enabled() {
-    static const bool on = env_int("QBG_PREFETCH", 0) != 0;
+// Warp-specialised pipelined passes (QBG_PIPE=1): a producer warp streams tiles into a ring of
+// shared-memory slots with bulk async copies (the TMA engine) tracked by mbarriers.
+bool pipeline_enabled() {
+    static const bool on = env_int("QBG_PIPE", 0) != 0;
     return on;
+}
+// producer flavour: 1 = one warp of bulk async copies per contiguous run (TMA engine),
+// 2 = a producer warpgroup of 16-B cp.async completing the mbarrier with arrive.noinc
+int pipeline_mode() {
+    static const int m = env_int("QBG_PIPE", 0);
+    return m;
+}
+int producer_threads() { return pipeline_mode() == 2 ? 128 : 32; }
+// ring slots that fit next to the gradient cells and barriers (<= 220 KB, 2..4 slots)
+int pipe_slots(bool back, int M, bool c128, int ngrad, int nw) {
+    const size_t tile = (static_cast<size_t>(back ? 2 : 1) << M) * (c128 ? 16 : 8);
+    const size_t cells = back ? static_cast<size_t>(ngrad) * (nw + 1) * 8 : 0;
+    int n = 4;
+    while (n > 2 && n * tile + cells + 128 > 220 * 1024) --n;
+    return n;
 }
 // Specialised-kernel defaults (measured on B200, 25q apply+grad, tools/sweep.py logs in
 // profiles/): forward 2^11-element tiles of 128 threads x 16 registers, 3 CTAs/SM; reverse
@@ -78,11 +95,12 @@ int ctas_per_sm(bool back, int threads) {
     return threads >= 512 ? 1 : 2;
 }
 Geo geo_for(int dir) {
-    const bool j = jit::enabled();
-    static const Geo f{env_int("QBG_FWD_M", j ? kJitFwdM : kFwdM), env_int("QBG_FWD_RB", j ? kJitFwdRB : kFwdRB),
-                       env_int("QBG_COALESCE", 3)};
-    static const Geo b{env_int("QBG_BWD_M", j ? kJitBwdM : kBwdM), env_int("QBG_BWD_RB", j ? kJitBwdRB : kBwdRB),
-                       env_int("QBG_COALESCE", 3)};
+    const bool j = jit::enabled(), pp = j && pipeline_enabled();
+    // pipelined passes: one CTA per SM, 256 consumer threads (forward 2^12 x 16, reverse 2^11 x 2x8)
+    static const Geo f{env_int("QBG_FWD_M", pp ? 12 : j ? kJitFwdM : kFwdM),
+                       env_int("QBG_FWD_RB", pp ? 4 : j ? kJitFwdRB : kFwdRB), env_int("QBG_COALESCE", 3)};
+    static const Geo b{env_int("QBG_BWD_M", pp ? 11 : j ? kJitBwdM : kBwdM),
+                       env_int("QBG_BWD_RB", pp ? 3 : j ? kJitBwdRB : kBwdRB), env_int("QBG_COALESCE", 3)};
     return dir == 2 ? b : f;
 }
 
@@ -487,11 +505,13 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
                 slot_of[regb[k]] = k;
                 D.sreg[k] = swz(1u << regb[k]);
                 D.greg[k] = tg.gw[regb[k]];
+                D.lreg[k] = static_cast<uint8_t>(regb[k]);
             }
             for (int p = 0; p < Wn; ++p) {
                 pos_of[thrb[p]] = p;
                 D.sthr[p] = swz(1u << thrb[p]);
                 D.gthr[p] = tg.gw[thrb[p]];
+                D.lthr[p] = static_cast<uint8_t>(thrb[p]);
             }
             D.op_begin = static_cast<int>(pl.ops.size()) - P.op_base;
             for (int gi : sp.gates) {
@@ -662,37 +682,32 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
     const int R = 1 << RB, W = M - RB, TH = 1 << W, NW = TH / 32;
     const int CS = NW + 1;  // gradient cell stride (odd: the 8 lanes of a warp_sum8 hit distinct banks)
     const size_t elem = c128 ? 16 : 8;
+    // pipe mode (warp-specialised): one producer warp streams tiles global -> shared with bulk
+    // async copies into a ring of slots tracked by mbarriers; TH consumer threads compute
+    const bool pipe = pipeline_enabled();
+    const int nbuf = pipe ? pipe_slots(back, M, c128, P.ngrad, NW) : 1;
+    const size_t tile_elems = static_cast<size_t>(back ? 2 : 1) << M;
+    const size_t tile_bytes = tile_elems * elem;
+    const std::string SYNC = pipe ? "named_bar<" + std::to_string(TH) + ">();\n" : "__syncthreads();\n";
     std::ostringstream s;
-    // two resident CTAs of 256 threads (128 registers each) or one of 512 (QBG_*_MINB overrides)
-    s << "extern \"C\" __global__ void __launch_bounds__(" << TH << ", " << ctas_per_sm(back, TH) << ") __NAME__("
+    const int NP = pipe ? producer_threads() : 0;
+    s << "extern \"C\" __global__ void __launch_bounds__(" << TH + NP << ", "
+      << (pipe ? 1 : ctas_per_sm(back, TH)) << ") __NAME__(" << (c128 ? "c128" : "c64") << "* __restrict__ psi, "
       << (c128 ? "c128" : "c64")
-      << "* __restrict__ psi, " << (c128 ? "c128" : "c64")
       << "* __restrict__ adj, double* __restrict__ gpart, long long gcols, int gbase, const __grid_constant__ PM<"
       << (c128 ? "double" : "float") << ", " << std::max(2, 2 * nmats) << "> pm) {\n";
     s << "typedef " << (c128 ? "c128" : "c64") << " V;\nconstexpr int R = " << R << ";\nconst int tid = threadIdx.x;\n";
     s << "#define MV(i) mk<V>(pm.m[2 * (i)], pm.m[2 * (i) + 1])\n";
-    // prefetch mode: tile t+1 is copied global -> shared (cp.async, in the stage-0 layout) while
-    // tile t computes; two tile buffers alternate
-    const bool pf = prefetch_enabled();
-    const size_t tile_bytes = (back ? 2 : 1) * (elem << M);
-    const size_t nbuf = pf ? 2 : 1;
-    s << "extern __shared__ __align__(16) unsigned char smraw[];\n";
-    if (pf)
-        s << "V* sbase = (V*)smraw;\n";
-    else
+    s << "extern __shared__ __align__(128) unsigned char smraw[];\n";
+    const size_t cells_off = nbuf * tile_bytes;
+    const size_t bar_off = (cells_off + (back ? static_cast<size_t>(P.ngrad) * CS * 8 : 0) + 15) & ~size_t{15};
+    if (pipe) {
+        s << "V* ring = (V*)smraw;\n";
+        s << "unsigned long long* full = (unsigned long long*)(smraw + " << bar_off << ");\nunsigned long long* empty = full + "
+          << nbuf << ";\n";
+    } else {
         s << "V* sx = (V*)smraw;\nV* sy = sx + " << (1 << M) << ";\n";
-    if (back) {
-        s << "double* sg = (double*)(smraw + " << nbuf * tile_bytes << ");\n";
-        s << "for (int i = tid; i < " << P.ngrad * CS << "; i += " << TH << ") sg[i] = 0.0;\n__syncthreads();\n";
-        s << "const int warp = tid >> 5, lane = tid & 31;\n";
     }
-    // hoisted thread parts of every stage's offsets
-    const DStage& S0 = P.st[0];
-    const DStage& SL = P.st[P.nstages - 1];
-    s << "const i64 g0 = " << tid_sum(S0.gthr, W, false) << ";\n";
-    s << "const i64 gL = " << tid_sum(SL.gthr, W, false) << ";\n";
-    for (int k = 0; k < P.nstages; ++k) s << "const unsigned st" << k << " = " << tid_sum(P.st[k].sthr, W, true) << ";\n";
-    s << "V x[R];\n" << (back ? "V y[R];\n" : "");
     // tile id -> (outer index, element base)
     s << "auto tile_geo = [&](u64 tile, u64& outer, i64& tb) {\n";
     if (P.nchunks == 1)
@@ -705,6 +720,75 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         s << "outer = ((outer >> " << p << ") << " << p + 1 << ") | (outer & " << hex((uint64_t{1} << p) - 1) << ");\n";
     }
     s << "tb = (i64)outer * " << P.B << "ll + (i64)c * " << (int64_t{1} << P.nb) << "ll;\n};\n";
+    if (pipe) {
+        // contiguous run: the lowest local bits whose element weight is 1, 2, 4, ...
+        int64_t gw[32];
+        for (int b = 0; b < M; ++b) gw[b] = b < P.nb ? (int64_t{1} << b) : (P.B << P.qpos[b - P.nb]);
+        int cr = 0;
+        while (cr < M && gw[cr] == (int64_t{1} << cr)) ++cr;
+        const int nruns = 1 << (M - cr);
+        s << "if (tid == 0) { for (int i = 0; i < " << nbuf << "; ++i) { mbar_init(full + i, " << (NP == 32 ? 1 : NP)
+          << "); mbar_init(empty + i, 1); } }\n";
+        s << "__syncthreads();\n";
+        s << "if (tid >= " << TH << ") {  // producer\n";
+        s << "const int lane = tid - " << TH << ";  // producer thread index\n";
+        s << "const i64 RW[" << std::max(1, M - cr) << "] = {";
+        for (int k = cr; k < M; ++k) s << (k > cr ? ", " : "") << gw[k] << "ll";
+        if (M == cr) s << "0";
+        s << "};\n";
+        s << "u64 it = 0;\n";
+        s << "for (u64 tile = blockIdx.x; tile < " << P.ntiles << "ull; tile += gridDim.x, ++it) {\n";
+        s << "const unsigned slot = (unsigned)(it % " << nbuf << "), use = (unsigned)(it / " << nbuf << ");\n";
+        s << "if (use > 0) mbar_wait(empty + slot, (use - 1u) & 1u);\n";
+        s << "u64 outer; i64 tb; tile_geo(tile, outer, tb);\n";
+        s << "V* dst = ring + (size_t)slot * " << tile_elems << "u;\n";
+        if (NP == 32) {
+            s << "if (lane == 0) mbar_arrive_tx(full + slot, " << tile_bytes << "u);\n__syncwarp();\n";
+            s << "for (int r = lane; r < " << nruns << "; r += 32) { i64 go = 0;\n";
+            s << "for (int k = 0; k < " << (M - cr) << "; ++k) if ((r >> k) & 1) go += RW[k];\n";
+            s << "bulk_g2s(dst + ((size_t)r << " << cr << "), psi + tb + go, " << (elem << cr) << "u, full + slot);";
+            if (back)
+                s << " bulk_g2s(dst + " << (1 << M) << " + ((size_t)r << " << cr << "), adj + tb + go, " << (elem << cr)
+                  << "u, full + slot);";
+            s << " }\n";
+        } else {
+            // element l = lane + NP*k: thread part of the offset once, k part literal
+            int64_t lp[8] = {0};
+            int nlb = 0;
+            while ((1 << nlb) < NP) ++nlb;
+            for (int b = 0; b < nlb; ++b) lp[b] = gw[b];
+            std::string gp = tid_sum(lp, nlb, false);
+            for (size_t at = gp.find("tid"); at != std::string::npos; at = gp.find("tid", at)) gp.replace(at, 3, "lane");
+            s << "const i64 gp = " << gp << ";\n";
+            for (int k = 0; k < (1 << M) / NP; ++k) {
+                int64_t gk = 0;
+                for (int b = nlb; b < M; ++b)
+                    if (((static_cast<int64_t>(k) * NP) >> b) & 1) gk += gw[b];
+                s << "cpa(dst + lane + " << k * NP << ", psi + tb + gp + " << gk << "ll);";
+                if (back) s << " cpa(dst + " << (1 << M) << " + lane + " << k * NP << ", adj + tb + gp + " << gk << "ll);";
+                s << "\n";
+            }
+            s << "cp_arrive_noinc(full + slot);\n";
+        }
+        s << "}\nreturn;\n}\n";
+    }
+    if (back) {
+        s << "double* sg = (double*)(smraw + " << cells_off << ");\n";
+        s << "for (int i = tid; i < " << P.ngrad * CS << "; i += " << TH << ") sg[i] = 0.0;\n" << SYNC;
+        s << "const int warp = tid >> 5, lane = tid & 31;\n";
+    }
+    // hoisted thread parts of every stage's offsets
+    const DStage& S0 = P.st[0];
+    const DStage& SL = P.st[P.nstages - 1];
+    s << "const i64 g0 = " << tid_sum(S0.gthr, W, false) << ";\n";
+    s << "const i64 gL = " << tid_sum(SL.gthr, W, false) << ";\n";
+    for (int k = 0; k < P.nstages; ++k) s << "const unsigned st" << k << " = " << tid_sum(P.st[k].sthr, W, true) << ";\n";
+    if (pipe) {
+        uint32_t lw[kMaxW];
+        for (int p = 0; p < W; ++p) lw[p] = 1u << S0.lthr[p];
+        s << "const unsigned lin0 = " << tid_sum(lw, W, true) << ";\n";
+    }
+    s << "V x[R];\n" << (back ? "V y[R];\n" : "");
     auto goff = [&](const DStage& S, int j) {
         int64_t o = 0;
         for (int k = 0; k < RB; ++k)
@@ -717,8 +801,13 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             if ((j >> k) & 1) o ^= S.sreg[k];
         return o;
     };
-    const bool skip_first = pf && P.nstages > 1 && S0.op_end == S0.op_begin;  // data already in stage-0 layout
-    if (!pf) {
+    auto loff = [&](const DStage& S, int j) {
+        uint32_t o = 0;
+        for (int k = 0; k < RB; ++k)
+            if ((j >> k) & 1) o |= 1u << S.lreg[k];
+        return o;
+    };
+    if (!pipe) {
         s << "for (u64 tile = blockIdx.x; tile < " << P.ntiles << "ull; tile += gridDim.x) {\n";
         s << "u64 outer; i64 tb; tile_geo(tile, outer, tb);\n";
         for (int j = 0; j < R; ++j) {
@@ -727,62 +816,35 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             s << "\n";
         }
     } else {
-        const size_t stride = (back ? 2 : 1) << M;  // elements per buffer
-        auto prefetch = [&](const std::string& buf, const std::string& tbv) {
-            for (int j = 0; j < R; ++j) {
-                s << "cpa(" << buf << " + (st0 ^ " << soff(S0, j) << "u), psi + " << tbv << " + g0 + " << goff(S0, j) << "ll);";
-                if (back)
-                    s << " cpa(" << buf << " + " << (1 << M) << " + (st0 ^ " << soff(S0, j) << "u), adj + " << tbv
-                      << " + g0 + " << goff(S0, j) << "ll);";
-                s << "\n";
-            }
-            s << "cp_commit();\n";
-        };
-        s << "unsigned it = 0;\n";
-        s << "if (blockIdx.x < " << P.ntiles << "ull) { u64 on; i64 tbn; tile_geo(blockIdx.x, on, tbn);\n";
-        prefetch("sbase", "tbn");
-        s << "}\n";
+        s << "u64 it = 0;\n";
         s << "for (u64 tile = blockIdx.x; tile < " << P.ntiles << "ull; tile += gridDim.x, ++it) {\n";
+        s << "const unsigned slot = (unsigned)(it % " << nbuf << "), use = (unsigned)(it / " << nbuf << ");\n";
+        s << "mbar_wait(full + slot, use & 1u);\n";
+        s << "V* sx = ring + (size_t)slot * " << tile_elems << "u; V* sy = sx + " << (1 << M) << ";\n";
         s << "u64 outer; i64 tb; tile_geo(tile, outer, tb);\n";
-        s << "V* sx = sbase + (it & 1u) * " << stride << "u; V* sy = sx + " << (1 << M) << ";\n";
-        s << "const u64 tn = tile + gridDim.x;\n";
-        s << "if (tn < " << P.ntiles << "ull) { u64 on; i64 tbn; tile_geo(tn, on, tbn); V* nx = sbase + ((it + 1u) & 1u) * "
-          << stride << "u;\n";
-        prefetch("nx", "tbn");
-        s << "cp_wait<1>(); } else { cp_wait<0>(); }\n";
-        if (!skip_first) {
-            for (int j = 0; j < R; ++j) {
-                s << "x[" << j << "] = sx[st0 ^ " << soff(S0, j) << "u];";
-                if (back) s << " y[" << j << "] = sy[st0 ^ " << soff(S0, j) << "u];";
-                s << "\n";
-            }
+        for (int j = 0; j < R; ++j) {  // stage 0 from the linear (bulk-copied) layout
+            s << "x[" << j << "] = sx[lin0 | " << loff(S0, j) << "u];";
+            if (back) s << " y[" << j << "] = sy[lin0 | " << loff(S0, j) << "u];";
+            s << "\n";
         }
+        if (P.nstages > 1) s << SYNC;  // the transposes overwrite the slot
     }
     for (int st = 0; st < P.nstages; ++st) {
         const DStage& S = P.st[st];
-        if (st == 1 && skip_first) {
-            // the prefetched buffer already holds the tile in the stage-0 layout
-            s << "__syncthreads();\n";
-            for (int j = 0; j < R; ++j) {
-                s << "x[" << j << "] = sx[st" << st << " ^ " << soff(S, j) << "u];";
-                if (back) s << " y[" << j << "] = sy[st" << st << " ^ " << soff(S, j) << "u];";
-                s << "\n";
-            }
-            s << "__syncthreads();\n";
-        } else if (st > 0) {
+        if (st > 0) {
             const DStage& Sp = P.st[st - 1];
             for (int j = 0; j < R; ++j) {
                 s << "sx[st" << st - 1 << " ^ " << soff(Sp, j) << "u] = x[" << j << "];";
                 if (back) s << " sy[st" << st - 1 << " ^ " << soff(Sp, j) << "u] = y[" << j << "];";
                 s << "\n";
             }
-            s << "__syncthreads();\n";
+            s << SYNC;
             for (int j = 0; j < R; ++j) {
                 s << "x[" << j << "] = sx[st" << st << " ^ " << soff(S, j) << "u];";
                 if (back) s << " y[" << j << "] = sy[st" << st << " ^ " << soff(S, j) << "u];";
                 s << "\n";
             }
-            s << "__syncthreads();\n";
+            s << SYNC;
         }
         for (int i = S.op_begin; i < S.op_end; ++i) {
             const DOp& op = ops[i];
@@ -929,9 +991,10 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         if (back) s << " adj[tb + gL + " << goff(SL, j) << "ll] = y[" << j << "];";
         s << "\n";
     }
+    if (pipe) s << "fence_proxy_async();\n" << SYNC << "if (tid == 0) mbar_arrive(empty + slot);\n";
     s << "}\n";  // tile loop
     if (back) {
-        s << "__syncthreads();\nfor (int sl = tid; sl < " << P.ngrad << "; sl += " << TH
+        s << SYNC << "for (int sl = tid; sl < " << P.ngrad << "; sl += " << TH
           << ") { double a = 0.0; for (int w = 0; w < " << NW << "; ++w) a += sg[sl * " << CS
           << " + w]; gpart[(i64)(gbase + sl) * gcols + blockIdx.x] = a; }\n";
     }
@@ -978,8 +1041,13 @@ void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128, bool check_
             }
         }
         const size_t tile_bytes = (back ? 2 : 1) * (elem << M);
-        st.smem = (prefetch_enabled() ? 2 * tile_bytes : (P.nstages > 1 || back ? tile_bytes : 0)) +
-                  (back ? static_cast<size_t>(P.ngrad) * (NW + 1) * 8 : 0);
+        const size_t cells = back ? static_cast<size_t>(P.ngrad) * (NW + 1) * 8 : 0;
+        if (pipeline_enabled()) {
+            const int nbuf = pipe_slots(back, M, c128, P.ngrad, NW);
+            st.smem = ((nbuf * tile_bytes + cells + 15) & ~size_t{15}) + 2 * nbuf * 8;
+        } else {
+            st.smem = (P.nstages > 1 || back ? tile_bytes : 0) + cells;
+        }
     }
     if (names.empty()) return;
     if (check_only)
@@ -993,14 +1061,15 @@ template <typename V, bool BACK>
 void launch_jit(V* psi, V* adj, Step& st, FusedPlan& pl, double* gpart, int64_t gcols) {
     const int T = 1 << (pl.M - pl.RB);
     const DPass& P = st.pass;
-    const int per_sm = ctas_per_sm(BACK, T);
+    const bool pipe = pipeline_enabled();
+    const int per_sm = pipe ? 1 : ctas_per_sm(BACK, T);
     int64_t grid = std::min<int64_t>(static_cast<int64_t>(P.ntiles), static_cast<int64_t>(num_sms()) * per_sm);
     if (BACK) grid = std::min<int64_t>(grid, gcols);
     double bytes = static_cast<double>(P.ntiles) * (int64_t{1} << pl.M) * sizeof(V) * (BACK ? 4.0 : 2.0);
     int gbase = P.grad_base;
     void* args[] = {&psi, &adj, &gpart, &gcols, &gbase, st.blob.data()};
     LaunchScope ls(BACK ? "fused_bwd" : "fused_fwd", bytes);
-    jit::launch(pl.jk[st.jk], static_cast<unsigned>(grid), T, st.smem, args);
+    jit::launch(pl.jk[st.jk], static_cast<unsigned>(grid), pipe ? T + producer_threads() : T, st.smem, args);
 }
 
 int batch_bits(int64_t B) {

@@ -58,6 +58,8 @@ struct DStage {
     uint32_t sthr[kMaxW];  // swizzled smem offset of tid bit p's unit vector
     int64_t greg[kMaxR];   // global element-offset weight of register slot k
     int64_t gthr[kMaxW];   // global element-offset weight of tid bit p
+    uint8_t lreg[kMaxR];   // local bit of register slot k
+    uint8_t lthr[kMaxW];   // local bit of tid bit p
 };
 
 struct DPass {

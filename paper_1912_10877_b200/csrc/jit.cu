@@ -124,7 +124,18 @@ uint64_t fnv(const std::string& s) {
     return h;
 }
 
-size_t compile_only(const std::string& src) { return build_cubin(src, fnv(src)).size(); }
+size_t compile_only(const std::string& src) {
+    const uint64_t key = fnv(src);
+    std::string cub = build_cubin(src, key);
+    // QBG_JIT_DUMP=<dir>: keep the cubin for offline inspection (cuobjdump -sass / -res-usage)
+    if (const char* d = std::getenv("QBG_JIT_DUMP")) {
+        char name[64];
+        std::snprintf(name, sizeof(name), "/%016llx.cubin", static_cast<unsigned long long>(key));
+        std::ofstream f(std::string(d) + name, std::ios::binary);
+        f.write(cub.data(), static_cast<std::streamsize>(cub.size()));
+    }
+    return cub.size();
+}
 
 bool enabled() {
     const char* e = std::getenv("QBG_JIT");
