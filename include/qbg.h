@@ -105,6 +105,7 @@ typedef struct qbg_reg qbg_reg;   /* device register: replaces qblock::Register 
 typedef struct qbg_prog qbg_prog; /* compiled gate program (fusion plan + realised matrices) */
 typedef struct qbg_obs qbg_obs;   /* compiled observable (sum of Pauli terms) */
 typedef struct qbg_rng qbg_rng;   /* host RNG: replaces qblock::Rng (rng.hpp:25-66) */
+typedef struct qbg_mmd qbg_mmd;   /* MMD loss: target distribution + RBF-mixture kernel */
 
 /* ---- library ------------------------------------------------------------------------- */
 const char* qbg_last_error(void);
@@ -234,6 +235,28 @@ int qbg_backward(qbg_reg* psi, qbg_reg* adj, const qbg_prog* prog, double* grads
    state_grad (optional, may be NULL) receives the adjoint of the input state. */
 int qbg_expect_grad(qbg_reg* reg, const qbg_prog* prog, const qbg_obs* obs, int32_t inplace,
                     double* energies, double* grads, qbg_reg* state_grad);
+
+/* ---- MMD loss (SPEC.md:446-449 MMDLoss, 497-505 mmd_expect / mmd_grad; §3.2,
+   Listing 12 "expect'(mmd, zero_state(5)=>circuit)") -------------------------
+   L_b = sum_{x,y} K(x,y) (p_b - q)_x (p_b - q)_y with p_b = |psi_b|^2 over the 2^n basis states
+   and K(x,y) = sum_s exp(-(x-y)^2 / (2 sigma_s^2)) (the radial-basis mixture over the integer
+   distance, brbf_kernel(sigma)).  Errors: target_p must be >= 0 and sum to 1 within 1e-12,
+   sigmas > 0 (QBG_ERR_VALIDATION); the register must have nqubits == n and no focus
+   (QBG_ERR_SHAPE). */
+int qbg_mmd_create(int32_t nqubits, const double* target_p, const double* sigmas, int32_t nsigma, qbg_mmd** out);
+int qbg_mmd_destroy(qbg_mmd* m);
+/* taps kept by the banded convolution (every dropped tap is exactly 0.0 in double) */
+int qbg_mmd_band(const qbg_mmd* m, int32_t* band);
+/* loss[nbatch] */
+int qbg_mmd_loss(const qbg_reg* reg, const qbg_mmd* m, double* loss);
+/* loss[nbatch] and the reverse-mode seed adj = dL/dpsi* = 2 (K (p - q))_x psi_x */
+int qbg_mmd_seed(const qbg_reg* psi, const qbg_mmd* m, qbg_reg* adj, double* loss);
+/* out[b] = sum_{x,y} K(x,y) p^a_b(x) (p_b(y) - q(y)) with p^a = |a|^2, p = |reg|^2: the
+   shift-rule building block  dL/dtheta = sum_b cross(psi(theta+pi/2), psi) - cross(psi(theta-pi/2), psi) */
+int qbg_mmd_cross(const qbg_reg* a, const qbg_reg* reg, const qbg_mmd* m, double* out);
+/* expect'(mmd, reg => prog): forward, seed, reverse pass (as qbg_expect_grad). */
+int qbg_mmd_grad(qbg_reg* reg, const qbg_prog* prog, const qbg_mmd* m, int32_t inplace, double* loss,
+                 double* grads, qbg_reg* state_grad);
 
 #ifdef __cplusplus
 }

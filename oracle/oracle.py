@@ -250,3 +250,31 @@ def reference() -> Oracle | None:
     if "ref" not in _cache:
         _cache["ref"] = Oracle(REFERENCE) if os.path.exists(REFERENCE) else None
     return _cache["ref"]
+
+
+# ---- MMD loss (SPEC.md:446-449 MMDLoss; 497-505 mmd_expect / mmd_grad; §3.2) ---------
+def mmd_dense(st, q, sigmas):
+    """Dense restatement of the squared MMD: L_b = d_bᵀ K d_b with d_b = |ψ_b|² − q and
+    K(x,y) = Σ_σ exp(−(x−y)²/(2σ²)) ("radial-basis mixture over integer
+    distance", DESIGN DECISIONS of SPEC §AD).  Returns (L[B], seed φ̄ = ∂L/∂ψ* = 2(Kd)⊙ψ).
+    O(4^n): small n only."""
+    st = np.ascontiguousarray(st, dtype=np.complex128)
+    N = st.shape[1]
+    x = np.arange(N, dtype=np.float64)
+    d2 = (x[:, None] - x[None, :]) ** 2
+    K = sum(np.exp(-d2 / (2.0 * s * s)) for s in np.atleast_1d(sigmas))
+    d = np.abs(st) ** 2 - np.asarray(q)[None, :]
+    Kd = d @ K  # K symmetric
+    L = np.einsum("bx,bx->b", d, Kd)
+    return L, 2.0 * Kd * st
+
+
+def mmd_grad_dense(orc, st, n, em, theta, q, sigmas):
+    """Reverse-mode MMD gradient on the oracle: forward with the oracle's apply, dense seed,
+    then the oracle's backward (uncompute + θ̄ accumulation)."""
+    psi = orc.apply_program(st, n, em, theta)
+    L, phi = mmd_dense(psi, q, sigmas)
+    phi = np.ascontiguousarray(phi)
+    g = np.zeros(max(1, len(theta)))
+    orc.backward(psi, phi, n, em, theta, g)
+    return L, g[: len(theta)]

@@ -106,6 +106,10 @@ def lib() -> ctypes.CDLL:
         "qbg_obs_destroy": (c_int32, [P]), "qbg_expect": (c_int32, [P, P, P]),
         "qbg_obs_apply": (c_int32, [P, P, P]), "qbg_backward": (c_int32, [P, P, P, P]),
         "qbg_expect_grad": (c_int32, [P, P, P, c_int32, P, P, P]),
+        "qbg_mmd_create": (c_int32, [c_int32, P, P, c_int32, POINTER(P)]), "qbg_mmd_destroy": (c_int32, [P]),
+        "qbg_mmd_band": (c_int32, [P, POINTER(c_int32)]), "qbg_mmd_loss": (c_int32, [P, P, P]),
+        "qbg_mmd_seed": (c_int32, [P, P, P, P]), "qbg_mmd_cross": (c_int32, [P, P, P, P]),
+        "qbg_mmd_grad": (c_int32, [P, P, P, c_int32, P, P, P]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

@@ -30,7 +30,11 @@ def _pair(reg_or_pair):
 
 
 def expect(obs: Block, reg_or_pair) -> np.ndarray:
-    """expect(O, reg) or expect(O, (reg, circuit)) -> per-batch real <O>."""
+    """expect(O, reg) or expect(O, (reg, circuit)) -> per-batch real <O>.
+    An :class:`~paper_1912_10877_b200.mmd.MMD` loss in place of O gives the per-batch MMD."""
+    from .mmd import MMD, mmd_expect
+    if isinstance(obs, MMD):
+        return mmd_expect(obs, reg_or_pair)
     reg, circuit = _pair(reg_or_pair)
     if circuit is not None:
         reg = reg.copy()
@@ -52,7 +56,11 @@ def obs_apply(obs: Block, reg: Register, out: Register | None = None) -> Registe
 
 def expect_grad(obs: Block, pair, want_state_grad: bool = False, inplace: bool = False) -> GradResult:
     """expect'(O, reg => circuit).  ``inplace`` runs on ``reg`` itself (it
-    is uncomputed back to the input up to rounding) and saves one full-state copy."""
+    is uncomputed back to the input up to rounding) and saves one full-state copy.
+    ``obs`` may be an MMD loss (Listing 12: expect'(mmd, zero_state(n)=>circuit))."""
+    from .mmd import MMD, mmd_grad
+    if isinstance(obs, MMD):
+        return mmd_grad(obs, pair, "reverse", want_state_grad, inplace)
     reg, circuit = pair
     if circuit.nqubits != reg.nactive or obs.nqubits != reg.nactive:
         raise errors.ShapeError("expect': block qubit count differs from active qubits")
@@ -72,6 +80,9 @@ def faithful_grad(obs: Block, pair) -> np.ndarray:
     a Rotation with a reflexive generator; Shift / Phase parameters raise UnsupportedError.
     2P device evaluations of the circuit (the forward-mode cost the paper contrasts with AD)."""
     from .blocks import Rotation, dispatch, parameter_nodes, parameters
+    from .mmd import MMD, mmd_grad
+    if isinstance(obs, MMD):
+        return mmd_grad(obs, pair, "shift").param_grads
     reg, circuit = pair
     nodes = parameter_nodes(circuit)
     for nd in nodes:

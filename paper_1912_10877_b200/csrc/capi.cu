@@ -1143,6 +1143,61 @@ int qbg_backward(qbg_reg* psi, qbg_reg* adj, const qbg_prog* prog, double* grads
         stream_sync();
     });
 }
+}  // extern "C"
+
+namespace qbg {
+namespace {
+// forward → seed → reverse pass with at most two extra live full states;
+// seed(psi_out, adj, d_vals) writes the adjoint seed and the per-batch loss values.
+template <class Seed>
+void grad_driver(qbg_reg* r, Program& p, int32_t inplace, qbg_reg* state_grad, double* vals, double* grads,
+                 Seed&& seed) {
+    static thread_local DevState work{}, adjbuf{};
+    auto ensure = [&](DevState& d) {
+        if (d.ptr && d.bytes() >= r->s.bytes() && d.dtype == r->s.dtype) return;
+        if (d.ptr) {
+            stream_sync();
+            QBG_CUDA(cudaFree(d.ptr));
+        }
+        d = r->s;
+        d.ptr = dev_alloc(r->s.bytes(), true);
+    };
+    DevState psi = r->s;
+    if (!inplace) {
+        ensure(work);
+        psi.ptr = work.ptr;
+        QBG_CUDA(cudaMemcpyAsync(psi.ptr, r->s.ptr, r->s.bytes(), cudaMemcpyDeviceToDevice, g_stream));
+    }
+    DevState adj = r->s;
+    if (state_grad) {
+        adj.ptr = state_grad->s.ptr;
+    } else {
+        ensure(adjbuf);
+        adj.ptr = adjbuf.ptr;
+    }
+    run_program(psi, p, false);
+    double* e = static_cast<double*>(scratch(r->s.B * sizeof(double), 10));
+    seed(psi, adj, e);
+    double* dg = static_cast<double*>(scratch(std::max<int64_t>(1, p.nparams) * sizeof(double), 11));
+    QBG_CUDA(cudaMemsetAsync(dg, 0, std::max<int64_t>(1, p.nparams) * sizeof(double), g_stream));
+    run_backward(psi, adj, p, dg);
+    QBG_CUDA(cudaMemcpyAsync(vals, e, r->s.B * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+    QBG_CUDA(cudaMemcpyAsync(grads, dg, p.nparams * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+    stream_sync();
+}
+}  // namespace
+}  // namespace qbg
+
+struct qbg_mmd {
+    int n = 0;
+    int D = 0;
+    double* q = nullptr;  // device, 2^n
+    double* w = nullptr;  // device, D + 1 taps
+    std::vector<double> sigmas;
+};
+
+extern "C" {
+
 int qbg_expect_grad(qbg_reg* r, const qbg_prog* prog, const qbg_obs* o, int32_t inplace, double* energies,
                     double* grads, qbg_reg* state_grad) {
     return guarded([&] {
@@ -1152,39 +1207,138 @@ int qbg_expect_grad(qbg_reg* r, const qbg_prog* prog, const qbg_obs* o, int32_t 
         if (p.n != r->nactive || ob.n != r->nactive)
             raise(QBG_ERR_SHAPE, "expect': block qubit count differs from active qubits");
         if (state_grad) same_shape(r, state_grad, "expect' state_grad");
-        // live full states: psi (the register itself when inplace) + adjoint (<= 4)
-        static thread_local DevState work{}, adjbuf{};
-        auto ensure = [&](DevState& d) {
-            if (d.ptr && d.bytes() >= r->s.bytes() && d.dtype == r->s.dtype) return;
-            if (d.ptr) {
-                stream_sync();
-                QBG_CUDA(cudaFree(d.ptr));
-            }
-            d = r->s;
-            d.ptr = dev_alloc(r->s.bytes(), true);
-        };
-        DevState psi = r->s;
-        if (!inplace) {
-            ensure(work);
-            psi.ptr = work.ptr;
-            QBG_CUDA(cudaMemcpyAsync(psi.ptr, r->s.ptr, r->s.bytes(), cudaMemcpyDeviceToDevice, g_stream));
+        grad_driver(r, p, inplace, state_grad, energies, grads,
+                    [&](const DevState& psi, const DevState& adj, double* e) { run_obs(psi, adj, ob, e); });
+    });
+}
+
+int qbg_mmd_create(int32_t n, const double* target_p, const double* sigmas, int32_t nsigma, qbg_mmd** out) {
+    return guarded([&] {
+        ensure_device();
+        if (!out || !target_p || !sigmas) raise(QBG_ERR_VALIDATION, "mmd: null argument");
+        if (n < 1 || n > g_cap.load()) raise(QBG_ERR_RANGE, "mmd: qubit count out of range");
+        if (nsigma < 1) raise(QBG_ERR_VALIDATION, "mmd: the kernel needs at least one bandwidth");
+        const uint64_t rows = uint64_t{1} << n;
+        double sum = 0.0;
+        for (uint64_t x = 0; x < rows; ++x) {
+            if (!(target_p[x] >= 0.0) || !std::isfinite(target_p[x]))
+                raise(QBG_ERR_VALIDATION, "mmd: target_p must be finite and non-negative");
+            sum += target_p[x];
         }
-        DevState adj = r->s;
-        if (state_grad) {
-            adj.ptr = state_grad->s.ptr;
-        } else {
-            ensure(adjbuf);
-            adj.ptr = adjbuf.ptr;
+        if (std::fabs(sum - 1.0) > 1e-12) raise(QBG_ERR_VALIDATION, "mmd: target_p must sum to 1 within 1e-12");
+        double smax = 0.0;
+        for (int i = 0; i < nsigma; ++i) {
+            if (!(sigmas[i] > 0.0) || !std::isfinite(sigmas[i])) raise(QBG_ERR_VALIDATION, "mmd: sigma must be > 0");
+            smax = std::max(smax, sigmas[i]);
         }
-        run_program(psi, p, false);
-        double* e = static_cast<double*>(scratch(r->s.B * sizeof(double), 10));
-        run_obs(psi, adj, ob, e);
-        double* dg = static_cast<double*>(scratch(std::max<int64_t>(1, p.nparams) * sizeof(double), 11));
-        QBG_CUDA(cudaMemsetAsync(dg, 0, std::max<int64_t>(1, p.nparams) * sizeof(double), g_stream));
-        run_backward(psi, adj, p, dg);
-        QBG_CUDA(cudaMemcpyAsync(energies, e, r->s.B * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
-        QBG_CUDA(cudaMemcpyAsync(grads, dg, p.nparams * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        // taps: w[k] = sum_s exp(-k^2 / (2 s^2)); the band ends where every tap underflows to 0
+        std::vector<double> w;
+        for (uint64_t k = 0; k < rows; ++k) {
+            double t = 0.0;
+            for (int i = 0; i < nsigma; ++i) t += std::exp(-static_cast<double>(k) * static_cast<double>(k) /
+                                                           (2.0 * sigmas[i] * sigmas[i]));
+            if (t == 0.0) break;
+            w.push_back(t);
+        }
+        auto* m = new qbg_mmd;
+        m->n = n;
+        m->D = static_cast<int>(w.size()) - 1;
+        m->sigmas.assign(sigmas, sigmas + nsigma);
+        try {
+            int TX, BC;
+            size_t sm;
+            if (!mmd_geometry(rows, 1, m->D, &TX, &BC, &sm))
+                raise(QBG_ERR_UNSUPPORTED, "mmd: kernel bandwidth too wide for the banded convolution");
+            m->q = static_cast<double*>(dev_alloc(rows * sizeof(double), false));
+            m->w = static_cast<double*>(dev_alloc(w.size() * sizeof(double), false));
+            QBG_CUDA(cudaMemcpyAsync(m->q, target_p, rows * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+            QBG_CUDA(cudaMemcpyAsync(m->w, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+            stream_sync();
+        } catch (...) {
+            if (m->q) cudaFree(m->q);
+            if (m->w) cudaFree(m->w);
+            delete m;
+            throw;
+        }
+        *out = m;
+    });
+}
+
+int qbg_mmd_destroy(qbg_mmd* m) {
+    return guarded([&] {
+        if (!m) return;
         stream_sync();
+        if (m->q) QBG_CUDA(cudaFree(m->q));
+        if (m->w) QBG_CUDA(cudaFree(m->w));
+        delete m;
+    });
+}
+
+int qbg_mmd_band(const qbg_mmd* m, int32_t* band) {
+    return guarded([&] {
+        if (!m || !band) raise(QBG_ERR_VALIDATION, "mmd: null argument");
+        *band = m->D;
+    });
+}
+
+}  // extern "C"
+
+namespace qbg {
+namespace {
+void mmd_check(const qbg_reg* r, const qbg_mmd* m) {
+    check_reg(r);
+    if (!m) raise(QBG_ERR_VALIDATION, "mmd: null loss handle");
+    if (r->s.n != m->n || r->nactive != r->s.n)
+        raise(QBG_ERR_SHAPE, "mmd: circuit output dimension differs from target_p (register must be relaxed)");
+}
+void mmd_to_host(double* out, const double* d, int64_t B) {
+    QBG_CUDA(cudaMemcpyAsync(out, d, B * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+    stream_sync();
+}
+}  // namespace
+}  // namespace qbg
+
+extern "C" {
+
+int qbg_mmd_loss(const qbg_reg* r, const qbg_mmd* m, double* loss) {
+    return guarded([&] {
+        mmd_check(r, m);
+        double* e = static_cast<double*>(scratch(r->s.B * sizeof(double), 10));
+        launch_mmd(0, r->s, nullptr, nullptr, m->q, m->w, m->D, e);
+        mmd_to_host(loss, e, r->s.B);
+    });
+}
+
+int qbg_mmd_seed(const qbg_reg* r, const qbg_mmd* m, qbg_reg* adj, double* loss) {
+    return guarded([&] {
+        mmd_check(r, m);
+        same_shape(r, adj, "mmd seed");
+        double* e = static_cast<double*>(scratch(r->s.B * sizeof(double), 10));
+        launch_mmd(1, r->s, nullptr, &adj->s, m->q, m->w, m->D, e);
+        mmd_to_host(loss, e, r->s.B);
+    });
+}
+
+int qbg_mmd_cross(const qbg_reg* a, const qbg_reg* r, const qbg_mmd* m, double* out) {
+    return guarded([&] {
+        mmd_check(r, m);
+        same_shape(r, a, "mmd cross");
+        double* e = static_cast<double*>(scratch(r->s.B * sizeof(double), 10));
+        launch_mmd(2, r->s, &a->s, nullptr, m->q, m->w, m->D, e);
+        mmd_to_host(out, e, r->s.B);
+    });
+}
+
+int qbg_mmd_grad(qbg_reg* r, const qbg_prog* prog, const qbg_mmd* m, int32_t inplace, double* loss, double* grads,
+                 qbg_reg* state_grad) {
+    return guarded([&] {
+        mmd_check(r, m);
+        auto& p = const_cast<qbg_prog*>(prog)->p;
+        if (p.n != r->nactive) raise(QBG_ERR_SHAPE, "expect'(mmd): block qubit count differs from active qubits");
+        if (state_grad) same_shape(r, state_grad, "expect'(mmd) state_grad");
+        grad_driver(r, p, inplace, state_grad, loss, grads, [&](const DevState& psi, const DevState& adj, double* e) {
+            launch_mmd(1, psi, nullptr, &adj, m->q, m->w, m->D, e);
+        });
     });
 }
 

@@ -61,6 +61,12 @@ void launch_permute_bits(const DevState& src, const DevState& dst, const int* ne
 void launch_probabilities(const DevState& s, int nactive, int64_t batch, double* d_p);
 void launch_collapse(const DevState& s, int nactive, int64_t batch, uint64_t hit, double inv);
 
+// ---- MMD loss (mmd.cu): mode 0 loss, 1 loss + seed adj = 2 (K d) psi, 2 cross with `other` ----
+// d_loss[b] (device) receives the per-batch sum; taps d_w[0..D]; target d_q[2^n]
+void launch_mmd(int mode, const DevState& psi, const DevState* other, const DevState* adj, const double* d_q,
+                const double* d_w, int D, double* d_loss);
+bool mmd_geometry(uint64_t rows, int64_t B, int D, int* TX, int* BC, size_t* smem);
+
 // scratch device memory owned by the library (grows; stream-ordered reuse)
 void* scratch(size_t bytes, int slot);
 

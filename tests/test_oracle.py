@@ -169,3 +169,32 @@ def test_gradient_triangle_oracle(orc, seed):
         emn = orc.obs_apply(orc.apply_program(st, 4, em, tm), terms)[1][0]
         fd[k] = (ep - emn) / 2e-4
     np.testing.assert_allclose(g, fd, atol=1e-6, rtol=0)
+
+
+def test_mmd_oracle_zero_and_fd(orc):
+    """The dense MMD restatement (oracle.mmd_dense): L = 0 at p = q, L >= 0,
+    and its reverse-mode gradient (oracle backward) equals central finite differences."""
+    from paper_1912_10877_b200.mmd import brbf_kernel
+    n = 4
+    circ = C.variational_circuit(n, 2)
+    th = np.random.default_rng(3).uniform(0, 2 * np.pi, B.nparameters(circ))
+    B.dispatch(circ, th)
+    st = orc.zero_state(n)
+    q = np.random.default_rng(5).uniform(0, 1, 1 << n)
+    q /= q.sum()
+    psi = orc.apply_program(st, n, lowered(circ), th)
+    p = np.abs(psi[0]) ** 2
+    assert abs(O.mmd_dense(psi, p / p.sum(), [2.0])[0][0]) < 1e-15
+    L, g = O.mmd_grad_dense(orc, st, n, lowered(circ), th, q, [2.0, 0.7])
+    assert L[0] >= 0
+    for k in range(th.size):
+        tp, tm = th.copy(), th.copy()
+        tp[k] += 1e-5
+        tm[k] -= 1e-5
+        lp = O.mmd_dense(orc.apply_program(st, n, lowered(circ), tp), q, [2.0, 0.7])[0][0]
+        lm = O.mmd_dense(orc.apply_program(st, n, lowered(circ), tm), q, [2.0, 0.7])[0][0]
+        assert abs((lp - lm) / 2e-5 - g[k]) < 1e-7
+    kf = brbf_kernel(2.0, 0.7)
+    assert np.isclose(kf(3, 5), np.exp(-4 / 8) + np.exp(-4 / (2 * 0.49)))
+    with pytest.raises(Exception):
+        brbf_kernel(-1.0)
