@@ -547,19 +547,29 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
                 };
                 // gradient ops first (reverse pass: before the uncompute)
                 if (backward && !pg.run.empty()) {
+                    // Hermitian A (every rotation / shift / phase generator): 4 statistics suffice
+                    bool herm = jit::enabled();
+                    for (const RunGrad& rg : pg.run) {
+                        double sc = 0.0;
+                        for (int k = 0; k < 4; ++k) sc = std::max(sc, std::hypot(rg.A[k].re, rg.A[k].im));
+                        const double tol = 1e-12 * std::max(sc, 1e-300);
+                        if (std::fabs(rg.A[0].im) > tol || std::fabs(rg.A[3].im) > tol ||
+                            std::fabs(rg.A[2].re - rg.A[1].re) > tol || std::fabs(rg.A[2].im + rg.A[1].im) > tol)
+                            herm = false;
+                    }
                     DOp o = base;
-                    o.code = G_CROSS1;
+                    o.code = herm ? G_CROSSH : G_CROSS1;
                     o.a = static_cast<uint8_t>(slot_of[tg.local[g.tbit[0]]]);
                     o.gslot = ncomp;
                     for (const RunGrad& rg : pg.run) {
                         GradEntry e{};
-                        e.type = 1;
+                        e.type = herm ? 2 : 1;
                         e.comp = static_cast<int>(P.grad_base) + ncomp;
                         e.param = rg.param;
                         std::memcpy(e.A, rg.A, sizeof(e.A));
                         pl.epi.push_back(e);
                     }
-                    ncomp += 8;
+                    ncomp += herm ? 4 : 8;
                     pl.ops.push_back(o);
                 }
                 if (backward && pg.k) {
@@ -960,6 +970,12 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                     s << "{ double c[8] = {0, 0, 0, 0, 0, 0, 0, 0}; if (" << cond << ") gcross1<V, R, " << int(op.a)
                       << ">(x, y, c); const double v = warp_sum8(c, lane); if ((lane & 3) == 0) sg[(" << op.gslot
                       << " + (lane >> 2)) * " << CS << " + warp] += v; }\n";
+                    break;
+                }
+                case G_CROSSH: {
+                    s << "{ double c[4] = {0, 0, 0, 0}; if (" << cond << ") gcrossh<V, R, " << int(op.a)
+                      << ">(x, y, c); const double v = warp_sum4(c, lane); if ((lane & 7) == 0) sg[(" << op.gslot
+                      << " + (lane >> 3)) * " << CS << " + warp] += v; }\n";
                     break;
                 }
                 case G_DENSE1:

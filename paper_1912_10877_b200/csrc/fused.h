@@ -30,8 +30,10 @@ enum : uint8_t {
     G_DIAG1U,       // K diag on a thread bit (b = 0) or a tile bit (b = 1) at position a
     G_DENSE2,       // K 4x4 on slots a, b
     G_DIAGK,        // K diag over t targets at mixed locations
-    G_CROSS1        // 2x2 cross matrix C_ab = Σ conj(adj_a) psi_b on slot a (8 components):
+    G_CROSS1,       // 2x2 cross matrix C_ab = Σ conj(adj_a) psi_b on slot a (8 components):
                     // the gradients of a whole same-qubit rotation run follow from C on the host
+    G_CROSSH        // the same for a run whose gradient matrices are Hermitian: 4 components
+                    // Im C00, Im C11, Im(C01 + C10), Re(C01 − C10) (JIT kernels only)
 };
 
 // DIAGK target locations (aux, 8 bits per target: [7:6] type, [5:0] position)
@@ -96,7 +98,7 @@ constexpr int kMaxMats = 512;   // complex matrix entries per pass (smem residen
 constexpr int kMaxComps = 256;  // gradient components per pass
 
 struct GradEntry {
-    int32_t type;  // 0 scalar component, 1 cross matrix (8 components)
+    int32_t type;  // 0 scalar component, 1 cross matrix (8 components), 2 Hermitian cross (4)
     int32_t comp;
     int32_t param;
     int32_t pad;

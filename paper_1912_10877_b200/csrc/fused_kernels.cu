@@ -388,6 +388,20 @@ __device__ __forceinline__ void run_ops(V* x, V* y, const DOp* ops, int b0, int 
                 }
                 break;
             }
+            case G_CROSSH: {  // (planned for JIT kernels; folded from the 8 components here)
+                if constexpr (BACK) {
+                    double c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                    if (ok) {
+#define QBG_C(K) gcross1_k<V, RB, K>(x, y, c);
+                        QBG_SLOT_SWITCH(op.a, RB, QBG_C)
+#undef QBG_C
+                    }
+                    double h[8] = {c[1], c[7], c[3] + c[5], c[2] - c[4], 0, 0, 0, 0};
+                    double s = warp_sum8(h, lane);
+                    if ((lane & 3) == 0 && (lane >> 2) < 4) sg[(op.gslot + (lane >> 2)) * nw + warp] += s;
+                }
+                break;
+            }
             default: {
                 if constexpr (BACK) {
                     double g = 0.0;
@@ -571,6 +585,11 @@ __global__ void k_grad_values(const double* __restrict__ sums, const GradEntry* 
         return;
     }
     const cdbl* GA = reinterpret_cast<const cdbl*>(g.A);
+    if (g.type == 2) {  // Hermitian M = A: M00 Im C00 + M11 Im C11 + Re M01 Im(C01+C10) + Im M01 Re(C01−C10)
+        const double r = 0.5 * (GA[2].re + GA[1].re), s = 0.5 * (GA[2].im - GA[1].im);
+        vals[k] = GA[0].re * sums[g.comp] + GA[3].re * sums[g.comp + 1] + r * sums[g.comp + 2] + s * sums[g.comp + 3];
+        return;
+    }
     double acc = 0.0;  // C_ab at comp + 2(2a+b)
     for (int a = 0; a < 2; ++a)
         for (int b = 0; b < 2; ++b) {

@@ -149,6 +149,27 @@ __device__ __forceinline__ void gcross1(const V* p, const V* a, double* c) {
       }
   }
 }
+// Hermitian-run cross statistics (4 components instead of 8): for Hermitian M,
+//   Im Σ_ab M_ab C_ab = M00 Im C00 + M11 Im C11 + Re M01 Im(C01 + C10) + Im M01 Re(C01 − C10)
+// c[0] = Im C00, c[1] = Im C11, c[2] = Im(C01 + C10), c[3] = Re(C01 − C10): 12 DFMA per pair.
+template <class V, int R, int K>
+__device__ __forceinline__ void gcrossh(const V* p, const V* a, double* c) {
+  double i01 = 0.0, i10 = 0.0, r01 = 0.0, r10 = 0.0;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    if (j & (1 << K)) continue;
+    const double a0x = a[j].x, a0y = a[j].y, a1x = a[j | (1 << K)].x, a1y = a[j | (1 << K)].y;
+    const double p0x = p[j].x, p0y = p[j].y, p1x = p[j | (1 << K)].x, p1y = p[j | (1 << K)].y;
+    c[0] = fma(a0x, p0y, fma(-a0y, p0x, c[0]));
+    c[1] = fma(a1x, p1y, fma(-a1y, p1x, c[1]));
+    i01 = fma(a0x, p1y, fma(-a0y, p1x, i01));
+    i10 = fma(a1x, p0y, fma(-a1y, p0x, i10));
+    r01 = fma(a0x, p1x, fma(a0y, p1y, r01));
+    r10 = fma(a1x, p0x, fma(a1y, p0y, r10));
+  }
+  c[2] += i01 + i10;
+  c[3] += r01 - r10;
+}
 // global -> shared async copy of one element (LDGSTS); completion via cp_commit / cp_wait
 template <class V>
 __device__ __forceinline__ void cpa(V* sdst, const V* gsrc) {
@@ -200,6 +221,27 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 // 8 values over the warp by halving exchanges; lane 4c ends with the sum of component c
+// 4 values per lane -> lane l holds the warp total of component (l >> 3) & 3
+__device__ __forceinline__ double warp_sum4(double* v, int lane) {
+  {
+    const bool hi = lane & 16;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      double send = hi ? v[k] : v[k + 2], keep = hi ? v[k + 2] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+  }
+  {
+    const bool hi = lane & 8;
+    double send = hi ? v[0] : v[1], keep = hi ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  double s = v[0];
+  s += __shfl_xor_sync(0xffffffffu, s, 4);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  return s;
+}
 __device__ __forceinline__ double warp_sum8(double* v, int lane) {
 #pragma unroll
   for (int k = 0; k < 4; ++k) {

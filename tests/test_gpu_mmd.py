@@ -109,7 +109,8 @@ def test_mmd_errors():
     loss = qb.MMD(qb.brbf_kernel(2.0), np.full(8, 0.125))
     with pytest.raises(errors.ShapeError):
         qb.mmd_expect(loss, qb.zero_state(4))
-    assert loss.band == 77  # exp(-k^2/8) is 0.0 in double from k = 78 on
+    assert loss.band == 7  # clamped to the basis size
+    assert qb.MMD(qb.brbf_kernel(2.0), np.full(256, 1 / 256)).band == 77  # exp(-k^2/8) == 0.0 from k = 78
 
 
 def test_mmd_20q_band_matches_dense_sample(orc):
