@@ -57,24 +57,27 @@ int env_int(const char* k, int d) {
     return (e && *e) ? std::atoi(e) : d;
 }
 Geo geo_for(int dir);
-// Warp-specialised pipelined passes (QBG_PIPE=1): a producer warp streams tiles into a ring of
-// shared-memory slots with bulk async copies (the TMA engine) tracked by mbarriers.
+// Warp-specialised pipelined passes (QBG_PIPE=G, G = 1 or 2): a producer warpgroup streams
+// tiles global -> shared with 16-B cp.async into a ring of slots tracked by mbarriers
+// (cp.async.mbarrier.arrive.noinc); G consumer groups of TH threads take alternate tiles
+// (ping-pong), so one group's loads / transposes / stores overlap the other's FP64 work.
+// With G = 2 the producer gives registers back (setmaxnreg) to the consumers.
+// Default on (2 groups) for the specialised kernels; QBG_PIPE=0 selects the plain tile loop.
 bool pipeline_enabled() {
-    static const bool on = env_int("QBG_PIPE", 0) != 0;
+    static const bool on = jit::enabled() && env_int("QBG_PIPE", 2) > 0;
     return on;
 }
-// producer flavour: 1 = one warp of bulk async copies per contiguous run (TMA engine),
-// 2 = a producer warpgroup of 16-B cp.async completing the mbarrier with arrive.noinc
-int pipeline_mode() {
-    static const int m = env_int("QBG_PIPE", 0);
-    return m;
+int consumer_groups() {
+    static const int g = std::min(2, std::max(1, env_int("QBG_PIPE", 2)));
+    return g;
 }
-int producer_threads() { return pipeline_mode() == 2 ? 128 : 32; }
-// ring slots that fit next to the gradient cells and barriers (<= 220 KB, 2..4 slots)
-int pipe_slots(bool back, int M, bool c128, int ngrad, int nw) {
+constexpr int kProducerThreads = 128;
+constexpr int kProducerRegs = 40;
+// ring slots that fit next to the gradient cells and barriers (<= 220 KB, 2..6 slots)
+int pipe_slots(bool back, int M, bool c128, int ngrad, int nwt) {
     const size_t tile = (static_cast<size_t>(back ? 2 : 1) << M) * (c128 ? 16 : 8);
-    const size_t cells = back ? static_cast<size_t>(ngrad) * (nw + 1) * 8 : 0;
-    int n = 4;
+    const size_t cells = back ? static_cast<size_t>(ngrad) * (nwt + 1) * 8 : 0;
+    int n = 6;
     while (n > 2 && n * tile + cells + 128 > 220 * 1024) --n;
     return n;
 }
@@ -95,12 +98,11 @@ int ctas_per_sm(bool back, int threads) {
     return threads >= 512 ? 1 : 2;
 }
 Geo geo_for(int dir) {
-    const bool j = jit::enabled(), pp = j && pipeline_enabled();
-    // pipelined passes: one CTA per SM, 256 consumer threads (forward 2^12 x 16, reverse 2^11 x 2x8)
-    static const Geo f{env_int("QBG_FWD_M", pp ? 12 : j ? kJitFwdM : kFwdM),
-                       env_int("QBG_FWD_RB", pp ? 4 : j ? kJitFwdRB : kFwdRB), env_int("QBG_COALESCE", 3)};
-    static const Geo b{env_int("QBG_BWD_M", pp ? 11 : j ? kJitBwdM : kBwdM),
-                       env_int("QBG_BWD_RB", pp ? 3 : j ? kJitBwdRB : kBwdRB), env_int("QBG_COALESCE", 3)};
+    const bool j = jit::enabled();
+    static const Geo f{env_int("QBG_FWD_M", j ? kJitFwdM : kFwdM), env_int("QBG_FWD_RB", j ? kJitFwdRB : kFwdRB),
+                       env_int("QBG_COALESCE", 3)};
+    static const Geo b{env_int("QBG_BWD_M", j ? kJitBwdM : kBwdM), env_int("QBG_BWD_RB", j ? kJitBwdRB : kBwdRB),
+                       env_int("QBG_COALESCE", 3)};
     return dir == 2 ? b : f;
 }
 
@@ -690,34 +692,42 @@ std::string tid_sum(const W* w, int nbits, bool xr) {
 
 std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, bool back, bool c128) {
     const int R = 1 << RB, W = M - RB, TH = 1 << W, NW = TH / 32;
-    const int CS = NW + 1;  // gradient cell stride (odd: the 8 lanes of a warp_sum8 hit distinct banks)
     const size_t elem = c128 ? 16 : 8;
-    // pipe mode (warp-specialised): one producer warp streams tiles global -> shared with bulk
-    // async copies into a ring of slots tracked by mbarriers; TH consumer threads compute
+    // pipe mode (warp-specialised, see pipeline_enabled): NG consumer groups of TH threads take
+    // alternate tiles from a ring of nbuf shared-memory slots filled by a cp.async producer warpgroup
     const bool pipe = pipeline_enabled();
-    const int nbuf = pipe ? pipe_slots(back, M, c128, P.ngrad, NW) : 1;
+    const int NG = pipe ? consumer_groups() : 1;
+    const int NWT = NG * NW;  // consumer warps
+    const int CS = NWT + 1;   // gradient cell stride (odd: the lanes of a warp_sum hit distinct banks)
+    const int nbuf = pipe ? pipe_slots(back, M, c128, P.ngrad, NWT) : 1;
+    // who writes the results: with a deep ring the producer drains each computed slot to global
+    // memory (consumers only compute); with a shallow one (reverse pass: 3 slots of 2 states) the
+    // drain would delay the refill, so the consumers store from registers and release the slot
+    const bool pstore = pipe && nbuf >= 2 * NG + 2;
     const size_t tile_elems = static_cast<size_t>(back ? 2 : 1) << M;
     const size_t tile_bytes = tile_elems * elem;
-    const std::string SYNC = pipe ? "named_bar<" + std::to_string(TH) + ">();\n" : "__syncthreads();\n";
+    const std::string SYNC = pipe ? "group_bar<" + std::to_string(TH) + ">(1 + cg);\n" : "__syncthreads();\n";
     std::ostringstream s;
-    const int NP = pipe ? producer_threads() : 0;
-    s << "extern \"C\" __global__ void __launch_bounds__(" << TH + NP << ", "
+    const int NP = pipe ? kProducerThreads : 0;
+    s << "extern \"C\" __global__ void __launch_bounds__(" << NG * TH + NP << ", "
       << (pipe ? 1 : ctas_per_sm(back, TH)) << ") __NAME__(" << (c128 ? "c128" : "c64") << "* __restrict__ psi, "
       << (c128 ? "c128" : "c64")
       << "* __restrict__ adj, double* __restrict__ gpart, long long gcols, int gbase, const __grid_constant__ PM<"
       << (c128 ? "double" : "float") << ", " << std::max(2, 2 * nmats) << "> pm) {\n";
-    s << "typedef " << (c128 ? "c128" : "c64") << " V;\nconstexpr int R = " << R << ";\nconst int tid = threadIdx.x;\n";
+    s << "typedef " << (c128 ? "c128" : "c64") << " V;\nconstexpr int R = " << R << ";\n";
+    s << (pipe ? "const int tid_all = threadIdx.x;\n" : "const int tid = threadIdx.x;\n");
     s << "#define MV(i) mk<V>(pm.m[2 * (i)], pm.m[2 * (i) + 1])\n";
     s << "extern __shared__ __align__(128) unsigned char smraw[];\n";
     const size_t cells_off = nbuf * tile_bytes;
     const size_t bar_off = (cells_off + (back ? static_cast<size_t>(P.ngrad) * CS * 8 : 0) + 15) & ~size_t{15};
     if (pipe) {
         s << "V* ring = (V*)smraw;\n";
-        s << "unsigned long long* full = (unsigned long long*)(smraw + " << bar_off << ");\nunsigned long long* empty = full + "
+        s << "unsigned long long* full = (unsigned long long*)(smraw + " << bar_off << ");\nunsigned long long* done = full + "
           << nbuf << ";\n";
     } else {
         s << "V* sx = (V*)smraw;\nV* sy = sx + " << (1 << M) << ";\n";
     }
+    if (back) s << "double* sg = (double*)(smraw + " << cells_off << ");\n";
     // tile id -> (outer index, element base)
     s << "auto tile_geo = [&](u64 tile, u64& outer, i64& tb) {\n";
     if (P.nchunks == 1)
@@ -731,59 +741,64 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
     }
     s << "tb = (i64)outer * " << P.B << "ll + (i64)c * " << (int64_t{1} << P.nb) << "ll;\n};\n";
     if (pipe) {
-        // contiguous run: the lowest local bits whose element weight is 1, 2, 4, ...
         int64_t gw[32];
         for (int b = 0; b < M; ++b) gw[b] = b < P.nb ? (int64_t{1} << b) : (P.B << P.qpos[b - P.nb]);
-        int cr = 0;
-        while (cr < M && gw[cr] == (int64_t{1} << cr)) ++cr;
-        const int nruns = 1 << (M - cr);
-        s << "if (tid == 0) { for (int i = 0; i < " << nbuf << "; ++i) { mbar_init(full + i, " << (NP == 32 ? 1 : NP)
-          << "); mbar_init(empty + i, 1); } }\n";
+        s << "if (tid_all == 0) { for (int i = 0; i < " << nbuf << "; ++i) { mbar_init(full + i, " << NP
+          << "); mbar_init(done + i, 1); } }\n";
+        if (back) s << "for (int i = tid_all; i < " << P.ngrad * CS << "; i += " << NG * TH + NP << ") sg[i] = 0.0;\n";
         s << "__syncthreads();\n";
-        s << "if (tid >= " << TH << ") {  // producer\n";
-        s << "const int lane = tid - " << TH << ";  // producer thread index\n";
-        s << "const i64 RW[" << std::max(1, M - cr) << "] = {";
-        for (int k = cr; k < M; ++k) s << (k > cr ? ", " : "") << gw[k] << "ll";
-        if (M == cr) s << "0";
-        s << "};\n";
-        s << "u64 it = 0;\n";
-        s << "for (u64 tile = blockIdx.x; tile < " << P.ntiles << "ull; tile += gridDim.x, ++it) {\n";
+        s << "if (tid_all >= " << NG * TH << ") {  // producer warpgroup\n";
+        if (NG > 1 && 65536 / (NG * TH + NP) / 8 * 8 > kProducerRegs) s << "reg_dealloc<" << kProducerRegs << ">();\n";
+        s << "const int lane = tid_all - " << NG * TH << ";\n";
+        // iteration it: store the results of tile it - nbuf (slot computed), then load tile it
+        s << "const u64 nt = (" << P.ntiles << "ull - blockIdx.x + gridDim.x - 1) / gridDim.x;\n";
+        // element l = lane + NP*k (linear local index): thread part once, k part literal
+        int64_t lp[8] = {0};
+        int nlb = 0;
+        while ((1 << nlb) < NP) ++nlb;
+        for (int b = 0; b < nlb; ++b) lp[b] = gw[b];
+        std::string gp = tid_sum(lp, nlb, false);
+        for (size_t at = gp.find("tid"); at != std::string::npos; at = gp.find("tid", at)) gp.replace(at, 3, "lane");
+        s << "const i64 gp = " << gp << ";\nconst unsigned sl = swz(lane);\n";
+        s << "for (u64 it = 0; it < nt" << (pstore ? " + " + std::to_string(nbuf) : std::string()) << "; ++it) {\n";
         s << "const unsigned slot = (unsigned)(it % " << nbuf << "), use = (unsigned)(it / " << nbuf << ");\n";
-        s << "if (use > 0) mbar_wait(empty + slot, (use - 1u) & 1u);\n";
-        s << "u64 outer; i64 tb; tile_geo(tile, outer, tb);\n";
-        s << "V* dst = ring + (size_t)slot * " << tile_elems << "u;\n";
-        if (NP == 32) {
-            s << "if (lane == 0) mbar_arrive_tx(full + slot, " << tile_bytes << "u);\n__syncwarp();\n";
-            s << "for (int r = lane; r < " << nruns << "; r += 32) { i64 go = 0;\n";
-            s << "for (int k = 0; k < " << (M - cr) << "; ++k) if ((r >> k) & 1) go += RW[k];\n";
-            s << "bulk_g2s(dst + ((size_t)r << " << cr << "), psi + tb + go, " << (elem << cr) << "u, full + slot);";
-            if (back)
-                s << " bulk_g2s(dst + " << (1 << M) << " + ((size_t)r << " << cr << "), adj + tb + go, " << (elem << cr)
-                  << "u, full + slot);";
-            s << " }\n";
-        } else {
-            // element l = lane + NP*k: thread part of the offset once, k part literal
-            int64_t lp[8] = {0};
-            int nlb = 0;
-            while ((1 << nlb) < NP) ++nlb;
-            for (int b = 0; b < nlb; ++b) lp[b] = gw[b];
-            std::string gp = tid_sum(lp, nlb, false);
-            for (size_t at = gp.find("tid"); at != std::string::npos; at = gp.find("tid", at)) gp.replace(at, 3, "lane");
-            s << "const i64 gp = " << gp << ";\n";
+        s << "V* buf = ring + (size_t)slot * " << tile_elems << "u;\n";
+        s << "if (use > 0) {\nmbar_wait(done + slot, (use - 1u) & 1u);\n";
+        if (pstore) s << "u64 outer; i64 tb; tile_geo(blockIdx.x + (it - " << nbuf << ") * gridDim.x, outer, tb);\n";
+        auto kgo = [&](int k) {
+            int64_t gk = 0;
+            for (int b = nlb; b < M; ++b)
+                if (((static_cast<int64_t>(k) * NP) >> b) & 1) gk += gw[b];
+            return gk;
+        };
+        if (pstore) {
             for (int k = 0; k < (1 << M) / NP; ++k) {
-                int64_t gk = 0;
-                for (int b = nlb; b < M; ++b)
-                    if (((static_cast<int64_t>(k) * NP) >> b) & 1) gk += gw[b];
-                s << "cpa(dst + lane + " << k * NP << ", psi + tb + gp + " << gk << "ll);";
-                if (back) s << " cpa(dst + " << (1 << M) << " + lane + " << k * NP << ", adj + tb + gp + " << gk << "ll);";
+                const uint32_t sk = swz(static_cast<uint32_t>(k * NP));
+                s << "psi[tb + gp + " << kgo(k) << "ll] = buf[sl ^ " << sk << "u];";
+                if (back) s << " adj[tb + gp + " << kgo(k) << "ll] = buf[" << (1 << M) << " + (sl ^ " << sk << "u)];";
                 s << "\n";
             }
-            s << "cp_arrive_noinc(full + slot);\n";
+            s << "group_bar<" << NP << ">(" << 2 + NG << ");\n";  // slot read out before it is refilled
         }
+        s << "}\n";
+        s << "if (it < nt) {\nu64 outer; i64 tb; tile_geo(blockIdx.x + it * gridDim.x, outer, tb);\n";
+        for (int k = 0; k < (1 << M) / NP; ++k) {
+            s << "cpa(buf + lane + " << k * NP << ", psi + tb + gp + " << kgo(k) << "ll);";
+            if (back) s << " cpa(buf + " << (1 << M) << " + lane + " << k * NP << ", adj + tb + gp + " << kgo(k) << "ll);";
+            s << "\n";
+        }
+        s << "cp_arrive_noinc(full + slot);\n}\n";
         s << "}\nreturn;\n}\n";
-    }
-    if (back) {
-        s << "double* sg = (double*)(smraw + " << cells_off << ");\n";
+        if (NG > 1) {
+            // ptxas gives a setmaxnreg kernel the launch-bound register count L per thread; the
+            // consumers may grow only into what the producer frees (else TRY_ALLOC never succeeds)
+            const int L = 65536 / (NG * TH + NP) / 8 * 8;
+            const int inc = ((NG * TH + NP) * L - NP * kProducerRegs) / (NG * TH) / 8 * 8;
+            if (inc > L) s << "reg_alloc<" << std::min(inc, 248) << ">();\n";
+        }
+        s << "const int cg = tid_all / " << TH << ", tid = tid_all & " << TH - 1 << ";\n";
+        if (back) s << "const int warp = cg * " << NW << " + (tid >> 5), lane = tid & 31;\n";
+    } else if (back) {
         s << "for (int i = tid; i < " << P.ngrad * CS << "; i += " << TH << ") sg[i] = 0.0;\n" << SYNC;
         s << "const int warp = tid >> 5, lane = tid & 31;\n";
     }
@@ -817,17 +832,25 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             if ((j >> k) & 1) o |= 1u << S.lreg[k];
         return o;
     };
+    // diagnostics only (QBG_EXP): 1 = no global traffic (synthetic tile, stores never taken),
+    // 2 = no gate ops (pure load / transpose / store) — splits a pass into compute and memory time
+    const int exp_mode = env_int("QBG_EXP", 0);
     if (!pipe) {
         s << "for (u64 tile = blockIdx.x; tile < " << P.ntiles << "ull; tile += gridDim.x) {\n";
         s << "u64 outer; i64 tb; tile_geo(tile, outer, tb);\n";
         for (int j = 0; j < R; ++j) {
-            s << "x[" << j << "] = psi[tb + g0 + " << goff(S0, j) << "ll];";
-            if (back) s << " y[" << j << "] = adj[tb + g0 + " << goff(S0, j) << "ll];";
+            if (exp_mode == 1) {
+                s << "x[" << j << "] = mk<V>((double)(tid + " << j << ") * 1e-3, (double)tile * 1e-9);";
+                if (back) s << " y[" << j << "] = mk<V>((double)(tid - " << j << ") * 1e-3, 1e-9);";
+            } else {
+                s << "x[" << j << "] = psi[tb + g0 + " << goff(S0, j) << "ll];";
+                if (back) s << " y[" << j << "] = adj[tb + g0 + " << goff(S0, j) << "ll];";
+            }
             s << "\n";
         }
     } else {
-        s << "u64 it = 0;\n";
-        s << "for (u64 tile = blockIdx.x; tile < " << P.ntiles << "ull; tile += gridDim.x, ++it) {\n";
+        s << "for (u64 it = cg;; it += " << NG << ") {\n";
+        s << "const u64 tile = blockIdx.x + it * gridDim.x;\nif (tile >= " << P.ntiles << "ull) break;\n";
         s << "const unsigned slot = (unsigned)(it % " << nbuf << "), use = (unsigned)(it / " << nbuf << ");\n";
         s << "mbar_wait(full + slot, use & 1u);\n";
         s << "V* sx = ring + (size_t)slot * " << tile_elems << "u; V* sy = sx + " << (1 << M) << ";\n";
@@ -856,7 +879,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             }
             s << SYNC;
         }
-        for (int i = S.op_begin; i < S.op_end; ++i) {
+        for (int i = S.op_begin; i < (exp_mode == 2 ? S.op_begin : S.op_end); ++i) {
             const DOp& op = ops[i];
             const int o = op.mat;
             std::ostringstream ctl;
@@ -1002,16 +1025,35 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             }
         }
     }
-    for (int j = 0; j < R; ++j) {
-        s << "psi[tb + gL + " << goff(SL, j) << "ll] = x[" << j << "];";
-        if (back) s << " adj[tb + gL + " << goff(SL, j) << "ll] = y[" << j << "];";
-        s << "\n";
+    if (pstore) {
+        // results go back into the slot (swizzled: element l at swz(l)); the producer writes
+        // them to global memory while this group computes its next tile
+        const int ls = P.nstages - 1;
+        if (P.nstages == 1) s << SYNC;  // other threads may still read stage 0 from the slot
+        for (int j = 0; j < R; ++j) {
+            s << "sx[st" << ls << " ^ " << soff(SL, j) << "u] = x[" << j << "];";
+            if (back) s << " sy[st" << ls << " ^ " << soff(SL, j) << "u] = y[" << j << "];";
+            s << "\n";
+        }
+        s << SYNC << "if (tid == 0) mbar_arrive(done + slot);\n";
+    } else {
+        if (exp_mode == 1) s << "if (outer == ~0ull) {\n";
+        for (int j = 0; j < R; ++j) {
+            s << "psi[tb + gL + " << goff(SL, j) << "ll] = x[" << j << "];";
+            if (back) s << " adj[tb + gL + " << goff(SL, j) << "ll] = y[" << j << "];";
+            s << "\n";
+        }
+        if (exp_mode == 1) s << "}\n";
+        if (pipe) s << SYNC << "if (tid == 0) mbar_arrive(done + slot);\n";
     }
-    if (pipe) s << "fence_proxy_async();\n" << SYNC << "if (tid == 0) mbar_arrive(empty + slot);\n";
     s << "}\n";  // tile loop
     if (back) {
-        s << SYNC << "for (int sl = tid; sl < " << P.ngrad << "; sl += " << TH
-          << ") { double a = 0.0; for (int w = 0; w < " << NW << "; ++w) a += sg[sl * " << CS
+        if (pipe)
+            s << "group_bar<" << NG * TH << ">(" << 1 + NG << ");\nconst int tc = tid_all;\n";
+        else
+            s << SYNC << "const int tc = tid;\n";
+        s << "for (int sl = tc; sl < " << P.ngrad << "; sl += " << NG * TH
+          << ") { double a = 0.0; for (int w = 0; w < " << NWT << "; ++w) a += sg[sl * " << CS
           << " + w]; gpart[(i64)(gbase + sl) * gcols + blockIdx.x] = a; }\n";
     }
     s << "#undef MV\n}\n";
@@ -1057,9 +1099,10 @@ void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128, bool check_
             }
         }
         const size_t tile_bytes = (back ? 2 : 1) * (elem << M);
-        const size_t cells = back ? static_cast<size_t>(P.ngrad) * (NW + 1) * 8 : 0;
+        const int nwt = (pipeline_enabled() ? consumer_groups() : 1) * NW;
+        const size_t cells = back ? static_cast<size_t>(P.ngrad) * (nwt + 1) * 8 : 0;
         if (pipeline_enabled()) {
-            const int nbuf = pipe_slots(back, M, c128, P.ngrad, NW);
+            const int nbuf = pipe_slots(back, M, c128, P.ngrad, consumer_groups() * NW);
             st.smem = ((nbuf * tile_bytes + cells + 15) & ~size_t{15}) + 2 * nbuf * 8;
         } else {
             st.smem = (P.nstages > 1 || back ? tile_bytes : 0) + cells;
@@ -1085,7 +1128,8 @@ void launch_jit(V* psi, V* adj, Step& st, FusedPlan& pl, double* gpart, int64_t 
     int gbase = P.grad_base;
     void* args[] = {&psi, &adj, &gpart, &gcols, &gbase, st.blob.data()};
     LaunchScope ls(BACK ? "fused_bwd" : "fused_fwd", bytes);
-    jit::launch(pl.jk[st.jk], static_cast<unsigned>(grid), pipe ? T + producer_threads() : T, st.smem, args);
+    jit::launch(pl.jk[st.jk], static_cast<unsigned>(grid), pipe ? consumer_groups() * T + kProducerThreads : T, st.smem,
+                args);
 }
 
 int batch_bits(int64_t B) {

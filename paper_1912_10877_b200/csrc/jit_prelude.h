@@ -212,6 +212,16 @@ __device__ __forceinline__ void cp_arrive_noinc(unsigned long long* b) {
 }
 template <int NT>
 __device__ __forceinline__ void named_bar() { asm volatile("bar.sync 1, %0;\n" :: "n"(NT) : "memory"); }
+// shared-memory swizzle of a tile-local element index (same as the host planner's swz)
+__device__ __forceinline__ unsigned swz(unsigned l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9) ^ (l >> 12) ^ (l >> 15)) & 7u); }
+// barrier over NT threads with a runtime id (one id per consumer group)
+template <int NT>
+__device__ __forceinline__ void group_bar(int id) { asm volatile("bar.sync %0, %1;\n" :: "r"(id), "n"(NT) : "memory"); }
+// warpgroup register reallocation (producer gives registers to the consumers)
+template <int N>
+__device__ __forceinline__ void reg_alloc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" :: "n"(N)); }
+template <int N>
+__device__ __forceinline__ void reg_dealloc() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" :: "n"(N)); }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" :: "n"(N) : "memory"); }

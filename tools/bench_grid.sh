@@ -2,7 +2,7 @@
 # Sweep of env-selected kernel geometries through bench.py (one line per setting):
 #   tools/bench_grid.sh "QBG_PIPE=0" "QBG_PIPE=2 QBG_BWD_RB=3" ...
 for cfg in "$@"; do
-  out=$(env $cfg python bench.py --steps 5 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1)
+  out=$(env $cfg timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline 2>/dev/null | tail -1)
   python - "$cfg" "$out" <<'PY'
 import json, sys
 cfg, out = sys.argv[1], sys.argv[2]
