@@ -19,6 +19,8 @@
 #include <array>
 #include <cstring>
 #include <map>
+#include <mutex>
+#include <unordered_map>
 #include <memory>
 
 #include <sstream>
@@ -1061,29 +1063,47 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
 }
 
 // Generates, compiles (cached) and attaches the specialised kernels of a plan.
+// Structure key of a pass: everything gen_pass reads (not the matrix values), so a new
+// parameter vector finds its kernels without regenerating / hashing their source.
+uint64_t pass_key(const DPass& P, const DOp* ops, int M, int RB, bool back, bool c128) {
+    uint64_t h = 1469598103934665603ULL;
+    auto mix = [&](const void* p, size_t n) {
+        const unsigned char* c = static_cast<const unsigned char*>(p);
+        for (size_t i = 0; i < n; ++i) {
+            h ^= c[i];
+            h *= 1099511628211ULL;
+        }
+    };
+    auto mixv = [&](int64_t v) { mix(&v, sizeof(v)); };
+    const int W = M - RB;
+    for (int64_t v : {int64_t{M}, int64_t{RB}, int64_t{back}, int64_t{c128}, int64_t{P.nstages}, int64_t{P.ngrad},
+                      int64_t{P.mq}, int64_t{P.nb}, P.B, P.nchunks, static_cast<int64_t>(P.ntiles), int64_t{P.nops},
+                      int64_t{P.nmats}})
+        mixv(v);
+    mix(P.qpos, static_cast<size_t>(P.mq));
+    for (int k = 0; k < P.nstages; ++k) {
+        const DStage& S = P.st[k];
+        mixv(S.op_begin);
+        mixv(S.op_end);
+        mix(S.sreg, sizeof(uint32_t) * RB);
+        mix(S.sthr, sizeof(uint32_t) * W);
+        mix(S.greg, sizeof(int64_t) * RB);
+        mix(S.gthr, sizeof(int64_t) * W);
+        mix(S.lreg, static_cast<size_t>(RB));
+        mix(S.lthr, static_cast<size_t>(W));
+    }
+    mix(ops, sizeof(DOp) * static_cast<size_t>(P.nops));
+    return h;
+}
+
+std::mutex g_pass_mu;
+std::unordered_map<uint64_t, jit::Kernel> g_pass_kernels;  // pass_key -> loaded kernel
+
 void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128, bool check_only = false) {
-    std::map<uint64_t, int> uniq;  // body hash -> kernel index
-    std::vector<std::string> names;
-    std::string src;
     const int NW = (1 << (M - RB)) / 32;
     const size_t elem = c128 ? 16 : 8;
-    for (auto& st : pl.steps) {
-        if (!st.tile) continue;
+    auto fill = [&](Step& st) {  // matrix parameter blob + shared memory of one step
         const DPass& P = st.pass;
-        std::string body = gen_pass(P, pl.ops.data() + P.op_base, P.nmats, M, RB, back, c128);
-        uint64_t h = jit::fnv(body);
-        auto it = uniq.find(h);
-        if (it == uniq.end()) {
-            char nm[40];
-            std::snprintf(nm, sizeof(nm), "qbg_%016llx", static_cast<unsigned long long>(h));
-            std::string b = body;
-            b.replace(b.find("__NAME__"), 8, nm);
-            src += b;
-            it = uniq.emplace(h, static_cast<int>(names.size())).first;
-            names.push_back(nm);
-        }
-        st.jk = it->second;
-        // matrix parameter blob
         const int nm2 = std::max(2, 2 * P.nmats);
         st.blob.assign(static_cast<size_t>(nm2) * (c128 ? 8 : 4), 0);
         for (int k = 0; k < P.nmats; ++k) {
@@ -1102,17 +1122,66 @@ void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128, bool check_
         const int nwt = (pipeline_enabled() ? consumer_groups() : 1) * NW;
         const size_t cells = back ? static_cast<size_t>(P.ngrad) * (nwt + 1) * 8 : 0;
         if (pipeline_enabled()) {
-            const int nbuf = pipe_slots(back, M, c128, P.ngrad, consumer_groups() * NW);
+            const int nbuf = pipe_slots(back, M, c128, P.ngrad, nwt);
             st.smem = ((nbuf * tile_bytes + cells + 15) & ~size_t{15}) + 2 * nbuf * 8;
         } else {
             st.smem = (P.nstages > 1 || back ? tile_bytes : 0) + cells;
         }
+    };
+    std::vector<uint64_t> keys;
+    if (!check_only) {
+        bool all = true;
+        {
+            std::lock_guard<std::mutex> lk(g_pass_mu);
+            for (auto& st : pl.steps) {
+                if (!st.tile) continue;
+                keys.push_back(pass_key(st.pass, pl.ops.data() + st.pass.op_base, M, RB, back, c128));
+                if (!g_pass_kernels.count(keys.back())) all = false;
+            }
+            if (all) {  // re-parameterised circuit: every kernel is known
+                pl.jk.clear();
+                size_t i = 0;
+                for (auto& st : pl.steps) {
+                    if (!st.tile) continue;
+                    st.jk = static_cast<int>(pl.jk.size());
+                    pl.jk.push_back(g_pass_kernels[keys[i++]]);
+                    fill(st);
+                }
+                return;
+            }
+        }
+    }
+    std::map<uint64_t, int> uniq;  // body hash -> kernel index
+    std::vector<std::string> names;
+    std::string src;
+    for (auto& st : pl.steps) {
+        if (!st.tile) continue;
+        const DPass& P = st.pass;
+        std::string body = gen_pass(P, pl.ops.data() + P.op_base, P.nmats, M, RB, back, c128);
+        uint64_t h = jit::fnv(body);
+        auto it = uniq.find(h);
+        if (it == uniq.end()) {
+            char nm[40];
+            std::snprintf(nm, sizeof(nm), "qbg_%016llx", static_cast<unsigned long long>(h));
+            std::string b = body;
+            b.replace(b.find("__NAME__"), 8, nm);
+            src += b;
+            it = uniq.emplace(h, static_cast<int>(names.size())).first;
+            names.push_back(nm);
+        }
+        st.jk = it->second;
+        fill(st);
     }
     if (names.empty()) return;
-    if (check_only)
+    if (check_only) {
         jit::compile_only(src);
-    else
-        pl.jk = jit::compile(src, names);
+        return;
+    }
+    pl.jk = jit::compile(src, names);
+    std::lock_guard<std::mutex> lk(g_pass_mu);
+    size_t i = 0;
+    for (auto& st : pl.steps)
+        if (st.tile) g_pass_kernels[keys[i++]] = pl.jk[st.jk];
 }
 
 // ---- execution ---------------------------------------------------------------------------------
