@@ -822,16 +822,16 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             if ((j >> k) & 1) o += S.greg[k];
         return o;
     };
-    auto soff = [&](const DStage& S, int j) {
-        uint32_t o = 0;
-        for (int k = 0; k < RB; ++k)
-            if ((j >> k) & 1) o ^= S.sreg[k];
-        return o;
-    };
     auto loff = [&](const DStage& S, int j) {
         uint32_t o = 0;
         for (int k = 0; k < RB; ++k)
             if ((j >> k) & 1) o |= 1u << S.lreg[k];
+        return o;
+    };
+    auto soff = [&](const DStage& S, int j) {
+        uint32_t o = 0;
+        for (int k = 0; k < RB; ++k)
+            if ((j >> k) & 1) o ^= S.sreg[k];
         return o;
     };
     // diagnostics only (QBG_EXP): 1 = no global traffic (synthetic tile, stores never taken),
@@ -857,16 +857,21 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         s << "mbar_wait(full + slot, use & 1u);\n";
         s << "V* sx = ring + (size_t)slot * " << tile_elems << "u; V* sy = sx + " << (1 << M) << ";\n";
         s << "u64 outer; i64 tb; tile_geo(tile, outer, tb);\n";
-        for (int j = 0; j < R; ++j) {  // stage 0 from the linear (bulk-copied) layout
-            s << "x[" << j << "] = sx[lin0 | " << loff(S0, j) << "u];";
-            if (back) s << " y[" << j << "] = sy[lin0 | " << loff(S0, j) << "u];";
+        for (int j = 0; j < R; ++j) {  // stage 0 from the linear (copied) layout
+            if (exp_mode == 5) {  // (diagnostics: synthetic tile, no slot reads / global stores)
+                s << "x[" << j << "] = mk<V>((double)(tid + " << j << ") * 1e-3, (double)tile * 1e-9);";
+                if (back) s << " y[" << j << "] = mk<V>((double)(tid - " << j << ") * 1e-3, 1e-9);";
+            } else {
+                s << "x[" << j << "] = sx[lin0 | " << loff(S0, j) << "u];";
+                if (back) s << " y[" << j << "] = sy[lin0 | " << loff(S0, j) << "u];";
+            }
             s << "\n";
         }
         if (P.nstages > 1) s << SYNC;  // the transposes overwrite the slot
     }
     for (int st = 0; st < P.nstages; ++st) {
         const DStage& S = P.st[st];
-        if (st > 0) {
+        if (st > 0 && exp_mode != 4) {  // (QBG_EXP=4, diagnostics: no transposes)
             const DStage& Sp = P.st[st - 1];
             for (int j = 0; j < R; ++j) {
                 s << "sx[st" << st - 1 << " ^ " << soff(Sp, j) << "u] = x[" << j << "];";
@@ -998,6 +1003,11 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                     break;
                 }
                 case G_CROSSH: {
+                    if (exp_mode == 3) {  // (diagnostics: statistics without the warp reduction)
+                        s << "{ double c[4] = {0, 0, 0, 0}; if (" << cond << ") gcrossh<V, R, " << int(op.a)
+                          << ">(x, y, c); if (c[0] + c[1] + c[2] + c[3] == 1.2345) sg[" << op.gslot * CS << " + warp] += 1.0; }\n";
+                        break;
+                    }
                     s << "{ double c[4] = {0, 0, 0, 0}; if (" << cond << ") gcrossh<V, R, " << int(op.a)
                       << ">(x, y, c); const double v = warp_sum4(c, lane); if ((lane & 7) == 0) sg[(" << op.gslot
                       << " + (lane >> 3)) * " << CS << " + warp] += v; }\n";
@@ -1039,13 +1049,13 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         }
         s << SYNC << "if (tid == 0) mbar_arrive(done + slot);\n";
     } else {
-        if (exp_mode == 1) s << "if (outer == ~0ull) {\n";
+        if (exp_mode == 1 || exp_mode == 5) s << "if (outer == ~0ull) {\n";
         for (int j = 0; j < R; ++j) {
             s << "psi[tb + gL + " << goff(SL, j) << "ll] = x[" << j << "];";
             if (back) s << " adj[tb + gL + " << goff(SL, j) << "ll] = y[" << j << "];";
             s << "\n";
         }
-        if (exp_mode == 1) s << "}\n";
+        if (exp_mode == 1 || exp_mode == 5) s << "}\n";
         if (pipe) s << SYNC << "if (tid == 0) mbar_arrive(done + slot);\n";
     }
     s << "}\n";  // tile loop
