@@ -330,8 +330,16 @@ def _param_nodes(b: Block, seen: dict, out: list):
 
 
 def parameter_nodes(b: Block) -> list[Block]:
-    out: list[Block] = []
-    _param_nodes(b, {}, out)
+    """Depth-first distinct parameterised nodes.  Block structure is immutable (only θ values
+    change), so the list is cached on the block."""
+    out = getattr(b, "_qbg_param_nodes", None)
+    if out is None:
+        out = []
+        _param_nodes(b, {}, out)
+        try:
+            b._qbg_param_nodes = out
+        except AttributeError:
+            pass
     return out
 
 
