@@ -1162,8 +1162,7 @@ void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128, bool check_
         }
     }
     std::map<uint64_t, int> uniq;  // body hash -> kernel index
-    std::vector<std::string> names;
-    std::string src;
+    std::vector<std::string> names, bodies;
     for (auto& st : pl.steps) {
         if (!st.tile) continue;
         const DPass& P = st.pass;
@@ -1173,9 +1172,8 @@ void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128, bool check_
         if (it == uniq.end()) {
             char nm[40];
             std::snprintf(nm, sizeof(nm), "qbg_%016llx", static_cast<unsigned long long>(h));
-            std::string b = body;
-            b.replace(b.find("__NAME__"), 8, nm);
-            src += b;
+            body.replace(body.find("__NAME__"), 8, nm);
+            bodies.push_back(std::move(body));
             it = uniq.emplace(h, static_cast<int>(names.size())).first;
             names.push_back(nm);
         }
@@ -1184,10 +1182,12 @@ void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128, bool check_
     }
     if (names.empty()) return;
     if (check_only) {
+        std::string src;
+        for (auto& b : bodies) src += b;
         jit::compile_only(src);
         return;
     }
-    pl.jk = jit::compile(src, names);
+    pl.jk = jit::compile_parallel(bodies, names);
     std::lock_guard<std::mutex> lk(g_pass_mu);
     size_t i = 0;
     for (auto& st : pl.steps)
@@ -1637,6 +1637,7 @@ void seed_jit_prepare(FusedPlan& pl, bool c128, bool check_only) {
     std::map<uint64_t, int> uniq;
     std::vector<std::string> names;
     std::string src;
+    std::vector<std::string> sbodies;
     pl.sjk.clear();
     pl.sblob.clear();
     for (auto& sp : pl.spasses) {
@@ -1649,6 +1650,7 @@ void seed_jit_prepare(FusedPlan& pl, bool c128, bool check_only) {
             std::string b = body;
             b.replace(b.find("__NAME__"), 8, nm);
             src += b;
+            sbodies.push_back(std::move(b));
             it = uniq.emplace(h, static_cast<int>(names.size())).first;
             names.push_back(nm);
         }
@@ -1673,7 +1675,7 @@ void seed_jit_prepare(FusedPlan& pl, bool c128, bool check_only) {
     if (check_only)
         jit::compile_only(src);
     else
-        pl.jk = jit::compile(src, names);
+        pl.jk = jit::compile_parallel(sbodies, names);
 }
 
 void run_seed(const DevState& psi, const DevState& phi, FusedPlan& pl, double* d_energy) {

@@ -11,6 +11,8 @@
 #include <map>
 #include <mutex>
 #include <sstream>
+#include <thread>
+#include <algorithm>
 
 #include "common.cuh"
 #include "jit_prelude.h"
@@ -174,6 +176,69 @@ std::vector<Kernel> compile(const std::string& src, const std::vector<std::strin
         Kernel k;
         QBG_CUDA(cudaLibraryGetKernel(&k.k, lib, nm.c_str()));
         out.push_back(k);
+    }
+    return out;
+}
+
+std::vector<Kernel> compile_parallel(const std::vector<std::string>& bodies, const std::vector<std::string>& names) {
+    // chunks of whole kernels; each chunk is its own cached cubin / library, the missing ones are
+    // built by concurrent NVRTC invocations (first use of a large circuit: seconds, not tens)
+    const size_t nk = bodies.size();
+    unsigned hw = std::thread::hardware_concurrency();
+    const size_t nchunk = std::max<size_t>(1, std::min<size_t>({nk, hw ? hw : 4, 16}));
+    std::vector<std::string> srcs(nchunk);
+    std::vector<std::vector<size_t>> members(nchunk);
+    for (size_t i = 0; i < nk; ++i) {
+        srcs[i * nchunk / nk] += bodies[i];
+        members[i * nchunk / nk].push_back(i);
+    }
+    std::vector<uint64_t> keys(nchunk);
+    std::vector<std::string> cubs(nchunk);
+    std::vector<char> need(nchunk, 0);
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (size_t c = 0; c < nchunk; ++c) {
+        keys[c] = fnv(std::string(kPrelude) + srcs[c]);
+        if (g_libs.count(keys[c])) continue;
+        char name[64];
+        std::snprintf(name, sizeof(name), "/%016llx.cubin", static_cast<unsigned long long>(keys[c]));
+        if (!read_file(cache_dir() + name, cubs[c])) need[c] = 1;
+    }
+    std::vector<std::string> errs(nchunk);
+    {
+        std::vector<std::thread> th;
+        for (size_t c = 0; c < nchunk; ++c)
+            if (need[c])
+                th.emplace_back([&, c] {
+                    try {
+                        cubs[c] = build_cubin(srcs[c], keys[c]);
+                    } catch (const std::exception& e) {
+                        errs[c] = e.what();
+                    }
+                });
+        for (auto& t : th) t.join();
+    }
+    for (size_t c = 0; c < nchunk; ++c)
+        if (!errs[c].empty()) raise(QBG_ERR_INTERNAL, errs[c]);
+    std::vector<Kernel> out(nk);
+    for (size_t c = 0; c < nchunk; ++c) {
+        cudaLibrary_t lib = nullptr;
+        auto it = g_libs.find(keys[c]);
+        if (it != g_libs.end()) {
+            lib = it->second;
+        } else {
+            char name[64];
+            std::snprintf(name, sizeof(name), "/%016llx.cubin", static_cast<unsigned long long>(keys[c]));
+            if (need[c]) write_file(cache_dir() + name, cubs[c]);
+            cudaError_t e = cudaLibraryLoadData(&lib, cubs[c].data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+            if (e != cudaSuccess) {  // a stale / foreign cache entry: rebuild once
+                cudaGetLastError();
+                cubs[c] = build_cubin(srcs[c], keys[c]);
+                write_file(cache_dir() + name, cubs[c]);
+                QBG_CUDA(cudaLibraryLoadData(&lib, cubs[c].data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+            }
+            g_libs[keys[c]] = lib;
+        }
+        for (size_t i : members[c]) QBG_CUDA(cudaLibraryGetKernel(&out[i].k, lib, names[i].c_str()));
     }
     return out;
 }

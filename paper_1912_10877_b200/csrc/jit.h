@@ -27,6 +27,10 @@ struct Kernel {
 // handles of `names` in order.  Throws qbg::Error(QBG_ERR_INTERNAL) with the NVRTC log on failure.
 std::vector<Kernel> compile(const std::string& src, const std::vector<std::string>& names);
 
+// Same for one kernel body per entry of `bodies` (names[i] defined in bodies[i]): the bodies are
+// grouped into chunks compiled concurrently and cached per chunk.
+std::vector<Kernel> compile_parallel(const std::vector<std::string>& bodies, const std::vector<std::string>& names);
+
 // NVRTC only (no device): compiles `src` to an sm_100a cubin and returns its size.
 size_t compile_only(const std::string& src);
 
