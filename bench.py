@@ -147,6 +147,22 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def fp64_roofline(top, per_launch_ms):
+    """The tile passes are FP64-bound as much as HBM-bound: the same kernel's
+    algorithmic FP64 work (pass_flops in fused.cu) against the measured DFMA peak."""
+    if not top or not top.get("flops"):
+        return None
+    peak, src = 37.0, "nominal 64 DFMA/clk/SM x 148 SMs x 1.965 GHz"
+    try:
+        peak = json.load(open(os.path.join(ROOT, "profiles", "r01_fp64_pipes.json")))["dfma_tflops"]
+        src = "measured DFMA peak (profiles/r01_fp64_pipes.json, tools/fp64_pipes.cu)"
+    except Exception:
+        pass
+    ach = top["flops"] / top["launches"] / (per_launch_ms / 1e3) / 1e12
+    return {"achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+            "flops_per_launch": top["flops"] / top["launches"], "peak_source": src}
+
+
 def workload_config(args):
     n, d = args.qubits, args.depth
     G, P, T = n * (1 + 4 * d), n * (1 + 3 * d), 3 * (n - 1)
@@ -276,8 +292,9 @@ def main():
     L.qbg_profile_enable(0)
     kernels = []
     for line in buf.value.decode().strip().splitlines():
-        name, cnt, tot, byt = line.split("\t")
-        kernels.append({"name": name, "launches": int(cnt), "total_ms": float(tot), "bytes": float(byt)})
+        name, cnt, tot, byt, flo = line.split("\t")
+        kernels.append({"name": name, "launches": int(cnt), "total_ms": float(tot), "bytes": float(byt),
+                        "flops": float(flo)})
     kernels.sort(key=lambda x: -x["total_ms"])
     top = kernels[0] if kernels else None
     roofline = None
@@ -297,6 +314,7 @@ def main():
                     "traffic": traffic, "kernel": top["name"], "launches_per_step": top["launches"] / 2,
                     "bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms, "share_of_step": share,
                     "peak_source": peak_src,
+                    "fp64": fp64_roofline(top, per_launch_ms),
                     "kernels": [{k2: (round(v, 6) if isinstance(v, float) else v) for k2, v in kk.items()}
                                 for kk in kernels[:8]]}
 

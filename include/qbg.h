@@ -125,7 +125,8 @@ int qbg_set_fusion(int32_t enabled);
 /* Per-kernel CUDA-event timing of the library's own launches (measurement hook). */
 int qbg_profile_enable(int32_t enabled);
 int qbg_profile_reset(void);
-/* Writes up to `cap` records "name\tlaunches\ttotal_ms\tbytes" separated by '\n'. */
+/* Writes up to `cap` records "name\tlaunches\ttotal_ms\tbytes\tflops" separated by '\n'
+   (bytes / flops: the algorithmic traffic and floating-point work of those launches). */
 int qbg_profile_report(char* buf, int64_t cap);
 /* Number of kernels the library launched since the last reset. */
 uint64_t qbg_launch_count(void);

@@ -59,6 +59,7 @@ struct ProfRec {
     const char* name;
     cudaEvent_t a, b;
     double bytes;
+    double flops;
 };
 std::vector<ProfRec> g_prof;
 std::vector<cudaEvent_t> g_event_pool;
@@ -253,12 +254,12 @@ void* scratch(size_t bytes, int slot) {
     return s.p;
 }
 
-LaunchScope::LaunchScope(const char* n, double b) : name(n), bytes(b) {
+LaunchScope::LaunchScope(const char* n, double b, double flops) : name(n), bytes(b) {
     g_launches.fetch_add(1);
     if (g_profile) {
         cudaEvent_t a = get_event();
         QBG_CUDA(cudaEventRecord(a, g_stream));
-        g_prof.push_back(ProfRec{n, a, nullptr, b});
+        g_prof.push_back(ProfRec{n, a, nullptr, b, flops});
     }
 }
 LaunchScope::~LaunchScope() {
@@ -495,7 +496,7 @@ int qbg_profile_report(char* buf, int64_t cap) {
         stream_sync();
         struct Agg {
             int64_t n = 0;
-            double ms = 0, bytes = 0;
+            double ms = 0, bytes = 0, flops = 0;
         };
         std::map<std::string, Agg> agg;
         for (auto& r : g_prof) {
@@ -506,12 +507,13 @@ int qbg_profile_report(char* buf, int64_t cap) {
             a.n++;
             a.ms += ms;
             a.bytes += r.bytes;
+            a.flops += r.flops;
         }
         std::string out;
         char line[256];
         for (auto& [k, a] : agg) {
-            std::snprintf(line, sizeof(line), "%s\t%lld\t%.6f\t%.6e\n", k.c_str(), static_cast<long long>(a.n), a.ms,
-                          a.bytes);
+            std::snprintf(line, sizeof(line), "%s\t%lld\t%.6f\t%.6e\t%.6e\n", k.c_str(), static_cast<long long>(a.n),
+                          a.ms, a.bytes, a.flops);
             out += line;
         }
         if (cap > 0) {

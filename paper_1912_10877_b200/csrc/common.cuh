@@ -93,7 +93,7 @@ void note_launch(const char* name, double bytes);  // host; counts and (if enabl
 struct LaunchScope {
     const char* name;
     double bytes;
-    LaunchScope(const char* n, double b);
+    LaunchScope(const char* n, double b, double flops = 0.0);
     ~LaunchScope();
 };
 

@@ -16,6 +16,7 @@
 // order: deterministic for a given grid.
 // See fused.h for the tile/stage vocabulary and DESIGN.md for the roofline numbers.
 #include <algorithm>
+#include <cmath>
 #include <array>
 #include <cstring>
 #include <map>
@@ -230,6 +231,7 @@ struct Step {
     int jk = -1;                 // specialised kernel (index into the plan's kernel list)
     std::vector<char> blob;      // its matrix parameter (PM<T, 2*nmats>)
     size_t smem = 0;
+    double flops = 0;            // algorithmic FP64 flops of one launch (pass_flops)
 };
 
 }  // namespace
@@ -1073,6 +1075,38 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
 }
 
 // Generates, compiles (cached) and attaches the specialised kernels of a plan.
+// Algorithmic floating-point work of a pass (complex mul = 6, add = 2 flops; controls scale
+// by the fraction of elements they select): forward ops on one state, reverse ops on two
+// (uncompute of ψ and φ̄) plus the gradient statistics once.  Reported beside the bytes.
+double pass_flops(const DPass& P, const DOp* ops, int M, bool back) {
+    double per_elem = 0;
+    for (int i = 0; i < P.nops; ++i) {
+        const DOp& o = ops[i];
+        const double frac = std::ldexp(1.0, -(popc(o.creg_mask) + popc(o.cthr_mask) + popc(o.ctile_mask)));
+        double f = 0;
+        switch (o.code) {
+            case OP_DENSE1: f = 14; break;
+            case OP_PERM1: case OP_DIAG1R: case OP_DIAG1T: case OP_DIAG1G: case OP_DIAGK: f = 6; break;
+            case OP_DENSE2: f = 30; break;
+            case OP_X1: f = 0; break;
+            default: f = 0;
+        }
+        if (o.code < G_DENSE1) {
+            per_elem += frac * f * (back ? 2 : 1);
+            continue;
+        }
+        switch (o.code) {
+            case G_CROSSH: f = 12; break;
+            case G_CROSS1: f = 16; break;
+            case G_DENSE1: f = 17; break;
+            case G_DENSE2: f = 33; break;
+            default: f = 9;
+        }
+        per_elem += frac * f;
+    }
+    return per_elem * static_cast<double>(P.ntiles) * std::ldexp(1.0, M);
+}
+
 // Structure key of a pass: everything gen_pass reads (not the matrix values), so a new
 // parameter vector finds its kernels without regenerating / hashing their source.
 uint64_t pass_key(const DPass& P, const DOp* ops, int M, int RB, bool back, bool c128) {
@@ -1114,6 +1148,7 @@ void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128, bool check_
     const size_t elem = c128 ? 16 : 8;
     auto fill = [&](Step& st) {  // matrix parameter blob + shared memory of one step
         const DPass& P = st.pass;
+        st.flops = pass_flops(P, pl.ops.data() + P.op_base, M, back);
         const int nm2 = std::max(2, 2 * P.nmats);
         st.blob.assign(static_cast<size_t>(nm2) * (c128 ? 8 : 4), 0);
         for (int k = 0; k < P.nmats; ++k) {
@@ -1206,7 +1241,7 @@ void launch_jit(V* psi, V* adj, Step& st, FusedPlan& pl, double* gpart, int64_t 
     double bytes = static_cast<double>(P.ntiles) * (int64_t{1} << pl.M) * sizeof(V) * (BACK ? 4.0 : 2.0);
     int gbase = P.grad_base;
     void* args[] = {&psi, &adj, &gpart, &gcols, &gbase, st.blob.data()};
-    LaunchScope ls(BACK ? "fused_bwd" : "fused_fwd", bytes);
+    LaunchScope ls(BACK ? "fused_bwd" : "fused_fwd", bytes, st.flops);
     jit::launch(pl.jk[st.jk], static_cast<unsigned>(grid), pipe ? consumer_groups() * T + kProducerThreads : T, st.smem,
                 args);
 }
