@@ -19,6 +19,7 @@
 #include <cmath>
 #include <array>
 #include <cstring>
+#include <fstream>
 #include <map>
 #include <mutex>
 #include <unordered_map>
@@ -554,6 +555,10 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
                 // gradient ops first (reverse pass: before the uncompute)
                 if (backward && !pg.run.empty()) {
                     // Hermitian A (every rotation / shift / phase generator): 4 statistics suffice
+                    const uint8_t rl = loc_code(g.tbit[0]);
+                    const bool diag_run = is_diagonal(g);
+                    if ((rl >> 6) != LOC_REG && !diag_run)
+                        raise(QBG_ERR_INTERNAL, "fused plan: a non-diagonal run off the register slots");
                     bool herm = jit::enabled();
                     for (const RunGrad& rg : pg.run) {
                         double sc = 0.0;
@@ -563,9 +568,13 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
                             std::fabs(rg.A[2].re - rg.A[1].re) > tol || std::fabs(rg.A[2].im + rg.A[1].im) > tol)
                             herm = false;
                     }
+                    // a diagonal run only needs Im C00 / Im C11, wherever its qubit lives (its
+                    // A_k = K_k are diagonal); it may sit on a thread or tile bit
+                    if (diag_run) herm = true;
                     DOp o = base;
-                    o.code = herm ? G_CROSSH : G_CROSS1;
-                    o.a = static_cast<uint8_t>(slot_of[tg.local[g.tbit[0]]]);
+                    o.code = diag_run ? G_CROSSD : herm ? G_CROSSH : G_CROSS1;
+                    o.a = static_cast<uint8_t>(rl & 63);
+                    o.b = static_cast<uint8_t>(rl >> 6);
                     o.gslot = ncomp;
                     for (const RunGrad& rg : pg.run) {
                         GradEntry e{};
@@ -1004,6 +1013,19 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                       << " + (lane >> 2)) * " << CS << " + warp] += v; }\n";
                     break;
                 }
+                case G_CROSSD: {
+                    std::string call;
+                    if (op.b == LOC_REG)
+                        call = "gcrossd_r<V, R, " + std::to_string(op.a) + ">(x, y, c);";
+                    else if (op.b == LOC_THR)
+                        call = "gcrossd_u<V, R>(x, y, c, (tid >> " + std::to_string(op.a) + ") & 1);";
+                    else
+                        call = "gcrossd_u<V, R>(x, y, c, (int)((outer >> " + std::to_string(op.a) + ") & 1ull));";
+                    s << "{ double c[4] = {0, 0, 0, 0}; if (" << cond << ") " << call
+                      << " const double v = warp_sum4(c, lane); if ((lane & 7) == 0) sg[(" << op.gslot
+                      << " + (lane >> 3)) * " << CS << " + warp] += v; }\n";
+                    break;
+                }
                 case G_CROSSH: {
                     if (exp_mode == 3) {  // (diagnostics: statistics without the warp reduction)
                         s << "{ double c[4] = {0, 0, 0, 0}; if (" << cond << ") gcrossh<V, R, " << int(op.a)
@@ -1098,6 +1120,7 @@ double pass_flops(const DPass& P, const DOp* ops, int M, bool back) {
         switch (o.code) {
             case G_CROSSH: f = 12; break;
             case G_CROSS1: f = 16; break;
+            case G_CROSSD: f = 4; break;
             case G_DENSE1: f = 17; break;
             case G_DENSE2: f = 33; break;
             default: f = 9;
@@ -1216,6 +1239,10 @@ void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128, bool check_
         fill(st);
     }
     if (names.empty()) return;
+    if (const char* d = std::getenv("QBG_JIT_SRC")) {  // diagnostics: keep the generated source
+        std::ofstream f(std::string(d) + "/" + names[0] + ".cu");
+        for (auto& b : bodies) f << b << "\n";
+    }
     if (check_only) {
         std::string src;
         for (auto& b : bodies) src += b;

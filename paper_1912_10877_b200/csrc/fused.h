@@ -32,8 +32,11 @@ enum : uint8_t {
     G_DIAGK,        // K diag over t targets at mixed locations
     G_CROSS1,       // 2x2 cross matrix C_ab = Σ conj(adj_a) psi_b on slot a (8 components):
                     // the gradients of a whole same-qubit rotation run follow from C on the host
-    G_CROSSH        // the same for a run whose gradient matrices are Hermitian: 4 components
+    G_CROSSH,       // the same for a run whose gradient matrices are Hermitian: 4 components
                     // Im C00, Im C11, Im(C01 + C10), Re(C01 − C10) (JIT kernels only)
+    G_CROSSD        // a diagonal run (Rz / shift / phase only) on a register slot (b = 0), thread
+                    // bit (b = 1) or tile bit (b = 2) at position a: Im C00, Im C11 (+ 2 zero
+                    // components, the G_CROSSH layout; its A are diagonal)
 };
 
 // DIAGK target locations (aux, 8 bits per target: [7:6] type, [5:0] position)

@@ -388,6 +388,24 @@ __device__ __forceinline__ void run_ops(V* x, V* y, const DOp* ops, int b0, int 
                 }
                 break;
             }
+            case G_CROSSD: {  // diagonal run: Im C00, Im C11 by the run bit (register / thread / tile)
+                if constexpr (BACK) {
+                    double h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                    if (ok) {
+#pragma unroll
+                        for (int j = 0; j < (1 << RB); ++j) {
+                            const int bit = op.b == 0 ? ((j >> op.a) & 1)
+                                          : op.b == 1 ? ((tid >> op.a) & 1)
+                                                      : static_cast<int>((outer >> op.a) & 1ull);
+                            const double v = static_cast<double>(y[j].x) * x[j].y - static_cast<double>(y[j].y) * x[j].x;
+                            if (bit) h[1] += v; else h[0] += v;
+                        }
+                    }
+                    double s = warp_sum8(h, lane);
+                    if ((lane & 3) == 0 && (lane >> 2) < 4) sg[(op.gslot + (lane >> 2)) * nw + warp] += s;
+                }
+                break;
+            }
             case G_CROSSH: {  // (planned for JIT kernels; folded from the 8 components here)
                 if constexpr (BACK) {
                     double c[8] = {0, 0, 0, 0, 0, 0, 0, 0};

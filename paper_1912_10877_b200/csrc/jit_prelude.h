@@ -170,6 +170,20 @@ __device__ __forceinline__ void gcrossh(const V* p, const V* a, double* c) {
   c[2] += i01 + i10;
   c[3] += r01 - r10;
 }
+// diagonal run: c[b] += Σ Im(conj(a) p) over the elements whose run bit is b — register slot K
+template <class V, int R, int K>
+__device__ __forceinline__ void gcrossd_r(const V* p, const V* a, double* c) {
+#pragma unroll
+  for (int j = 0; j < R; ++j) c[(j >> K) & 1] = fma((double)a[j].x, (double)p[j].y, fma(-(double)a[j].y, (double)p[j].x, c[(j >> K) & 1]));
+}
+// ... or a bit uniform over the thread's elements (thread / tile bit)
+template <class V, int R>
+__device__ __forceinline__ void gcrossd_u(const V* p, const V* a, double* c, int bit) {
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < R; ++j) s = fma((double)a[j].x, (double)p[j].y, fma(-(double)a[j].y, (double)p[j].x, s));
+  if (bit) c[1] += s; else c[0] += s;
+}
 // global -> shared async copy of one element (LDGSTS); completion via cp_commit / cp_wait
 template <class V>
 __device__ __forceinline__ void cpa(V* sdst, const V* gsrc) {
