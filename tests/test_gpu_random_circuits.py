@@ -113,3 +113,32 @@ def test_random_circuit_c64(orc, n, seed):
     res = qb.expect_grad(h, (qb.Register(n, 1, dtype="c64").set_state(st), circ))
     assert np.abs(res.energies - e).max() < 1e-5 * max(1.0, np.abs(e).max())
     assert np.abs(res.param_grads - g).max() < 1e-5 * max(1.0, np.abs(g).max())
+
+
+def random_observable(n, nterms, seed):
+    """Σ c_t P_t with random real weights on random Pauli strings (1-4 non-identity factors)."""
+    rng = np.random.default_rng(seed)
+    terms = []
+    for _ in range(nterms):
+        k = int(rng.integers(1, 5))
+        qs = rng.choice(np.arange(1, n + 1), size=k, replace=False)
+        ps = [[B.X, B.Y, B.Z][int(rng.integers(0, 3))] for _ in range(k)]
+        terms.append(float(rng.normal()) * B.kron(n, *[((int(q),), p) for q, p in zip(qs, ps)]))
+    return qb.Add(terms)
+
+
+@pytest.mark.parametrize("n,nb,seed", [(12, 1, 31), (15, 2, 32), (18, 1, 33)])
+def test_random_observable_expect_and_grad(orc, n, nb, seed):
+    """The seed planner (Pauli groups by X support, Y phases, Z masks inside / outside the tile)."""
+    circ = random_circuit(n, 80, seed)
+    th = B.parameters(circ)
+    em = lowered(circ)
+    obs = random_observable(n, 25, seed)
+    st = orc.rand_state(n, nb, seed)
+    e, g, _, sg = orc.expect_grad(st, n, em, th, B.pauli_terms(obs))
+    res = qb.expect_grad(obs, (qb.Register(n, nb).set_state(st), circ), want_state_grad=True)
+    assert np.abs(res.energies - e).max() <= TOL * max(1.0, np.abs(e).max())
+    assert np.abs(res.param_grads - g).max() <= 1e-11 * max(1.0, np.abs(g).max())
+    assert rel(res.state_grad.state(), sg) < TOL
+    ex = qb.expect(obs, (qb.Register(n, nb).set_state(st), circ))
+    assert np.abs(ex - e).max() <= TOL * max(1.0, np.abs(e).max())
