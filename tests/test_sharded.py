@@ -176,3 +176,31 @@ def test_sharded_virtual_device(orc, n, g):
     terms = B.pauli_terms(C.heisenberg(n))
     _, e_ref = orc.obs_apply(want[None, :], terms)
     assert abs(st.expect_pauli(terms) - e_ref[0]) < 1e-12 * max(1, abs(e_ref[0])) * 10
+
+
+@pytest.mark.parametrize("g,seed", [(1, 41), (2, 42), (3, 43)])
+def test_sharded_random_circuits_numpy(orc, g, seed):
+    """Every gate form (controls on global qubits, 2-qubit gates straddling the rank bits, dense
+    4x4, diagonal gates on global qubits) through the swap schedule, vs the full-state oracle."""
+    from test_gpu_random_circuits import random_circuit
+    n = 9
+    circ = random_circuit(n, 90, seed)
+    want = orc.apply_program(O.Oracle.zero_state(n), n, _lowered(circ), B.parameters(circ))[0]
+    st = ShardedState(NumpyBackend(n, g, orc), n, g).apply(circ)
+    got = st.state()
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-12
+    terms = B.pauli_terms(C.heisenberg(n))
+    _, e_ref = orc.obs_apply(want[None, :], terms)
+    assert abs(st.expect_pauli(terms) - e_ref[0]) < 1e-11
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,g,seed", [(15, 3, 51), (17, 2, 52)])
+def test_sharded_random_circuits_device(orc, n, g, seed):
+    from paper_1912_10877_b200.sharded import DeviceVirtualBackend
+    from test_gpu_random_circuits import random_circuit
+    circ = random_circuit(n, 150, seed)
+    want = orc.apply_program(O.Oracle.zero_state(n), n, _lowered(circ), B.parameters(circ))[0]
+    st = ShardedState(DeviceVirtualBackend(n, g), n, g).apply(circ)
+    got = st.state()
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-12
