@@ -76,6 +76,10 @@ int consumer_groups() {
     return g;
 }
 constexpr int kProducerThreads = 128;
+bool perm_ctrl_regs() {
+    static const bool on = env_int("QBG_PERM_CTRL_REGS", 1) != 0;
+    return on;
+}
 constexpr int kProducerRegs = 40;
 // ring slots that fit next to the gradient cells and barriers (<= 220 KB, 2..6 slots)
 int pipe_slots(bool back, int M, bool c128, int ngrad, int nwt) {
@@ -414,6 +418,14 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
                     uint32_t need = 0;
                     if (!is_diagonal(g))
                         for (int q = 0; q < g.t; ++q) need |= 1u << tg.local[g.tbit[q]];
+                    // a permutation (CNOT, Toffoli, controlled SWAP) whose controls are register bits is
+                    // a compile-time register rename; a control on a thread bit would make it a
+                    // runtime conditional swap of the whole register tile (128 moves for 2 x 16 c128)
+                    // (measured: forward passes gain ~2%; reverse passes lose more to the extra
+                    // stages than the moves cost next to the FP64 work, so forward only)
+                    if (g.kind == QBG_MAT_PERMUTATION && !backward && perm_ctrl_regs())
+                        for (int q = 0; q < 64; ++q)
+                            if (((g.cmask >> q) & 1) && tg.local[q] >= 0) need |= 1u << tg.local[q];
                     bool conflict = (pg.nd() & ball) | (pg.all() & bnd);
                     if (!conflict && __builtin_popcount(cur.S | need) <= R) {
                         cur.S |= need;
