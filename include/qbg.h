@@ -237,6 +237,13 @@ int qbg_backward(qbg_reg* psi, qbg_reg* adj, const qbg_prog* prog, double* grads
 int qbg_expect_grad(qbg_reg* reg, const qbg_prog* prog, const qbg_obs* obs, int32_t inplace,
                     double* energies, double* grads, qbg_reg* state_grad);
 
+/* e^{-iHt}|reg> in place for a hermitian Pauli-sum H (SPEC.md:397-405 time_evolve; matrix.hpp:680-724
+   matvec_cols): Lanczos on the device with full re-orthogonalisation, subspace <= maxdim (<= 0:
+   30), residual estimate < tol (<= 0: 1e-12), the step halved until it converges.  Every batch
+   column evolves independently.  krylov_dim (may be NULL) receives the largest subspace used.
+   Errors: non-hermitian H -> QBG_ERR_VALIDATION; qubit mismatch -> QBG_ERR_SHAPE. */
+int qbg_time_evolve(qbg_reg* reg, const qbg_obs* h, double t, double tol, int32_t maxdim, int32_t* krylov_dim);
+
 /* ---- MMD loss (SPEC.md:446-449 MMDLoss, 497-505 mmd_expect / mmd_grad; §3.2,
    Listing 12 "expect'(mmd, zero_state(5)=>circuit)") -------------------------
    L_b = sum_{x,y} K(x,y) (p_b - q)_x (p_b - q)_y with p_b = |psi_b|^2 over the 2^n basis states

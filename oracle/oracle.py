@@ -278,3 +278,26 @@ def mmd_grad_dense(orc, st, n, em, theta, q, sigmas):
     g = np.zeros(max(1, len(theta)))
     orc.backward(psi, phi, n, em, theta, g)
     return L, g[: len(theta)]
+
+
+# ---- time evolution ("e^{-iHt}|ψ> equals dense matrix exponential") -----------
+def pauli_dense(terms, n):
+    """Dense 2^n x 2^n matrix of Σ c i^{nY} X^x Z^z for the (coef, xmask, zmask) triples of
+    blocks.pauli_terms (qubit 1 = bit 0; Y = iXZ), the convention of pauli_axpy in qbg_oracle.cpp:
+    (P ψ)[i] = c i^{nY} (-1)^{|(i^x) & z|} ψ[i^x]."""
+    N = 1 << n
+    H = np.zeros((N, N), dtype=np.complex128)
+    idx = np.arange(N)
+    for c, x, z in terms:
+        ny = bin(int(x) & int(z)).count("1") & 3
+        j = idx ^ int(x)
+        sign = 1 - 2 * (np.array([bin(int(v) & int(z)).count("1") for v in j]) & 1)
+        H[idx, j] += complex(c) * (1j ** ny) * sign
+    return H
+
+
+def expm_apply(st, terms, n, t):
+    """e^{-iHt} applied to every batch row of st (dense scipy expm: small n only)."""
+    import scipy.linalg
+    U = scipy.linalg.expm(-1j * t * pauli_dense(terms, n))
+    return (U @ np.asarray(st, dtype=np.complex128).T).T

@@ -110,6 +110,7 @@ def lib() -> ctypes.CDLL:
         "qbg_mmd_band": (c_int32, [P, POINTER(c_int32)]), "qbg_mmd_loss": (c_int32, [P, P, P]),
         "qbg_mmd_seed": (c_int32, [P, P, P, P]), "qbg_mmd_cross": (c_int32, [P, P, P, P]),
         "qbg_mmd_grad": (c_int32, [P, P, P, c_int32, P, P, P]),
+        "qbg_time_evolve": (c_int32, [P, P, c_double, c_double, c_int32, POINTER(c_int32)]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

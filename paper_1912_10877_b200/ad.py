@@ -61,6 +61,9 @@ def expect_grad(obs: Block, pair, want_state_grad: bool = False, inplace: bool =
     from .mmd import MMD, mmd_grad
     if isinstance(obs, MMD):
         return mmd_grad(obs, pair, "reverse", want_state_grad, inplace)
+    from .blocks import has_time_evolution
+    if has_time_evolution(pair[1]):
+        return _expect_grad_segmented(obs, pair, want_state_grad)
     reg, circuit = pair
     if circuit.nqubits != reg.nactive or obs.nqubits != reg.nactive:
         raise errors.ShapeError("expect': block qubit count differs from active qubits")
@@ -112,3 +115,37 @@ def backward(psi: Register, adj: Register, circuit: Block, grads: np.ndarray | N
     g = np.zeros(max(1, p.nparams)) if grads is None else np.ascontiguousarray(grads, dtype=np.float64)
     check(lib().qbg_backward(psi._h, adj._h, p._h, g.ctypes.data))
     return g[: p.nparams]
+
+
+def _expect_grad_segmented(obs: Block, pair, want_state_grad: bool) -> GradResult:
+    """expect' through circuits with time_evolve nodes (SPEC.md:479-487 + the TimeEvolution design
+    decision): the gate segments run the device reverse pass (qbg_backward); a TimeEvolution
+    e^{-iHt} contributes t̄ = 2 Im<φ̄|H|ψ> (taken after it, summed over the batch) and is then
+    uncomputed on ψ and φ̄ by e^{+iHt} (two more Krylov applications)."""
+    from .blocks import evolve, parameter_nodes, segments
+    reg, circuit = pair
+    if circuit.nqubits != reg.nactive or obs.nqubits != reg.nactive:
+        raise errors.ShapeError("expect': block qubit count differs from active qubits")
+    index = {id(nd): k for k, nd in enumerate(parameter_nodes(circuit))}
+    grads = np.zeros(len(index))
+    psi = reg.copy()
+    segs = segments(circuit)
+    for kind, seg in segs:
+        if kind == "te":
+            evolve(psi, seg.hamiltonian, seg.theta)
+        else:
+            check(lib().qbg_apply(psi._h, compile_block(seg)._h))
+    adj = obs_apply(obs, psi)
+    energies = np.real(psi.inner(adj))
+    tmp = None
+    for kind, seg in reversed(segs):
+        if kind == "te":
+            tmp = obs_apply(seg.hamiltonian, psi, tmp)
+            grads[index[id(seg)]] += 2.0 * float(np.sum(np.imag(adj.inner(tmp))))
+            evolve(psi, seg.hamiltonian, -seg.theta)
+            evolve(adj, seg.hamiltonian, -seg.theta)
+        else:
+            g = backward(psi, adj, seg)
+            for k, nd in enumerate(parameter_nodes(seg)):
+                grads[index[id(nd)]] += g[k]
+    return GradResult(energies, grads, adj if want_state_grad else None)

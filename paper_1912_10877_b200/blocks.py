@@ -98,6 +98,24 @@ class Phase(Primitive):
         return f"phase({self.theta})"
 
 
+class TimeEvolution(Primitive):
+    """e^{-iHt} for a hermitian Pauli-sum H (Listing 6 ``time_evolve``).  The
+    evolution time is the node's parameter (``theta``); applied on the device by a Krylov
+    (Lanczos) exponential, ``qbg_time_evolve``."""
+
+    def __init__(self, hamiltonian: Block, t: float):
+        self.hamiltonian = hamiltonian
+        self.theta = float(t)
+        self.nqubits = hamiltonian.nqubits
+
+    @property
+    def t(self) -> float:
+        return self.theta
+
+    def __repr__(self):
+        return f"time_evolve({self.hamiltonian!r}, {self.theta})"
+
+
 class GeneralMatrix(Primitive):
     def __init__(self, mat):
         self.mat = M.as_matrix(mat)
@@ -193,6 +211,18 @@ class Scale(Composite):
         return [self.block]
 
 
+class Cached(Composite):
+    """cache(b) (Listings 6-7): transparent — apply through it equals apply
+    without it.  The engine already keeps Pauli-sum operators as device programs."""
+
+    def __init__(self, block: Block):
+        self.block = block
+        self.nqubits = block.nqubits
+
+    def subblocks(self):
+        return [self.block]
+
+
 class Daggered(Composite):
     def __init__(self, block: Block):
         self.block = block
@@ -273,6 +303,16 @@ def matblock(m):
     return GeneralMatrix(m)
 
 
+def time_evolve(h: Block, t: float) -> TimeEvolution:
+    """time_evolve(h, t): h must be a hermitian Pauli expression."""
+    pauli_terms(h)  # raises UnsupportedError when h is not a Pauli expression
+    return TimeEvolution(h, t)
+
+
+def cache(b: Block) -> Cached:
+    return Cached(b)
+
+
 def _locs(l) -> tuple[int, ...]:
     return (int(l),) if isinstance(l, (int, np.integer)) else tuple(int(v) for v in l)
 
@@ -320,7 +360,7 @@ def repeat(n: int, block: Block, locs=None) -> Repeat:
 # parameters / dispatch / gatecount / dagger
 # ---------------------------------------------------------------------------------------------------
 def _param_nodes(b: Block, seen: dict, out: list):
-    if isinstance(b, (Rotation, Shift, Phase)):
+    if isinstance(b, (Rotation, Shift, Phase, TimeEvolution)):
         if id(b) not in seen:
             seen[id(b)] = len(out)
             out.append(b)
@@ -428,6 +468,10 @@ def dagger(b: Block) -> Block:
         return Phase(-b.theta)
     if isinstance(b, GeneralMatrix):
         return GeneralMatrix(b.mat.adjoint())
+    if isinstance(b, TimeEvolution):
+        return TimeEvolution(b.hamiltonian, -b.theta)
+    if isinstance(b, Cached):
+        return Cached(dagger(b.block))
     if isinstance(b, Chain):
         return Chain(b.nqubits, [dagger(c) for c in reversed(b.blocks)])
     if isinstance(b, Put):
@@ -598,6 +642,10 @@ def _lower(b: Block, qmap: tuple, ctrls: tuple, cfg: tuple, em: _Emitter, adjoin
             _lower(b.block, (qmap[l - 1],), ctrls, cfg, em, adjoint)
     elif isinstance(b, Daggered):
         _lower(b.block, qmap, ctrls, cfg, em, not adjoint)
+    elif isinstance(b, Cached):
+        _lower(b.block, qmap, ctrls, cfg, em, adjoint)
+    elif isinstance(b, TimeEvolution):
+        raise errors.UnsupportedError("time_evolve: not a gate program (applied by the Krylov engine)")
     else:
         raise errors.UnsupportedError(f"apply: {type(b).__name__} is not a circuit block (non-unitary)")
 
@@ -697,9 +745,76 @@ def apply(reg, b: Block):
             else:
                 reg.add_scaled(tmp, 1.0)
         return reg
+    if has_time_evolution(b):
+        for kind, seg in segments(b):
+            if kind == "te":
+                evolve(reg, seg.hamiltonian, seg.theta)
+            else:
+                check(lib().qbg_apply(reg._h, compile_block(seg)._h))
+        return reg
     p = compile_block(b)
     check(lib().qbg_apply(reg._h, p._h))
     return reg
+
+
+# ---------------------------------------------------------------------------------------------------
+# time evolution inside circuits: the circuit splits into gate-program segments and Krylov steps
+# ---------------------------------------------------------------------------------------------------
+def has_time_evolution(b: Block) -> bool:
+    v = getattr(b, "_qbg_has_te", None)
+    if v is None:
+        v = isinstance(b, TimeEvolution) or any(has_time_evolution(c) for c in b.subblocks())
+        try:
+            b._qbg_has_te = v
+        except AttributeError:
+            pass
+    return v
+
+
+def segments(b: Block) -> list:
+    """[("prog", chain) | ("te", TimeEvolution)] in application order, cached on the block (its
+    structure is immutable).  TimeEvolution may appear at the top level of (nested) chains and
+    inside cache(); under put / control / kron it is unsupported."""
+    segs = getattr(b, "_qbg_segments", None)
+    if segs is not None:
+        return segs
+    flat: list = []
+
+    def walk(x):
+        if isinstance(x, TimeEvolution):
+            flat.append(x)
+        elif isinstance(x, Cached):
+            walk(x.block)
+        elif isinstance(x, Chain) and has_time_evolution(x):
+            for c in x.blocks:
+                walk(c)
+        elif has_time_evolution(x):
+            raise errors.UnsupportedError("time_evolve: only inside chains (not under put / control / kron)")
+        else:
+            flat.append(x)
+
+    walk(b)
+    segs, run = [], []
+    for x in flat:
+        if isinstance(x, TimeEvolution):
+            if run:
+                segs.append(("prog", Chain(b.nqubits, run)))
+                run = []
+            segs.append(("te", x))
+        else:
+            run.append(x)
+    if run:
+        segs.append(("prog", Chain(b.nqubits, run)))
+    b._qbg_segments = segs
+    return segs
+
+
+def evolve(reg, H: Block, t: float, tol: float = 1e-12, maxdim: int = 30) -> int:
+    """|reg> <- e^{-iHt}|reg> on the device (qbg_time_evolve); returns the Krylov dimension used."""
+    used = ctypes.c_int32()
+    check(lib().qbg_time_evolve(reg._h, compile_observable(H)._h, float(t), float(tol), int(maxdim),
+                                ctypes.byref(used)))
+    return used.value
 
 
 # ---------------------------------------------------------------------------------------------------
@@ -744,6 +859,8 @@ def pauli_terms(b: Block, qmap=None) -> list[tuple[complex, int, int]]:
         return [(1 + 0j, bit if x else 0, bit if z else 0)]
     if isinstance(b, Add):
         return [t for c in b.blocks for t in pauli_terms(c, qmap)]
+    if isinstance(b, Cached):
+        return pauli_terms(b.block, qmap)
     if isinstance(b, Scale):
         return [(b.factor * c, x, z) for c, x, z in pauli_terms(b.block, qmap)]
     if isinstance(b, Put):

@@ -79,7 +79,7 @@ struct Scratch {
     void* p = nullptr;
     size_t bytes = 0;
 };
-Scratch g_scratch[16];
+Scratch g_scratch[24];  // slots: see the scratch(…, k) call sites (one owner each while live)
 
 uint64_t mix(uint64_t x) {
     x += 0x9e3779b97f4a7c15ULL;
@@ -1328,6 +1328,208 @@ int qbg_mmd_cross(const qbg_reg* a, const qbg_reg* r, const qbg_mmd* m, double* 
         double* e = static_cast<double*>(scratch(r->s.B * sizeof(double), 10));
         launch_mmd(2, r->s, &a->s, nullptr, m->q, m->w, m->D, e);
         mmd_to_host(out, e, r->s.B);
+    });
+}
+
+}  // extern "C"
+
+// ---- time evolution: e^{-iHt}|psi> by Lanczos on the device (matrix.hpp:680-724) --
+namespace qbg {
+namespace {
+
+// symmetric Jacobi eigen-decomposition of a small dense matrix (row-major, destroyed); Q columns
+// are the eigenvectors
+void jacobi_eig(int m, std::vector<double>& A, std::vector<double>& Q, std::vector<double>& lam) {
+    Q.assign(static_cast<size_t>(m) * m, 0.0);
+    for (int i = 0; i < m; ++i) Q[i * m + i] = 1.0;
+    for (int sweep = 0; sweep < 100; ++sweep) {
+        double off = 0.0;
+        for (int p = 0; p < m; ++p)
+            for (int q = p + 1; q < m; ++q) off += A[p * m + q] * A[p * m + q];
+        if (off < 1e-34) break;
+        for (int p = 0; p < m; ++p)
+            for (int q = p + 1; q < m; ++q) {
+                const double apq = A[p * m + q];
+                if (std::fabs(apq) < 1e-300) continue;
+                const double th = (A[q * m + q] - A[p * m + p]) / (2.0 * apq);
+                const double tt = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+                const double c = 1.0 / std::sqrt(tt * tt + 1.0), sn = tt * c;
+                for (int k = 0; k < m; ++k) {  // rotate columns p, q
+                    const double akp = A[k * m + p], akq = A[k * m + q];
+                    A[k * m + p] = c * akp - sn * akq;
+                    A[k * m + q] = sn * akp + c * akq;
+                }
+                for (int k = 0; k < m; ++k) {  // rotate rows p, q
+                    const double apk = A[p * m + k], aqk = A[q * m + k];
+                    A[p * m + k] = c * apk - sn * aqk;
+                    A[q * m + k] = sn * apk + c * aqk;
+                }
+                for (int k = 0; k < m; ++k) {
+                    const double qkp = Q[k * m + p], qkq = Q[k * m + q];
+                    Q[k * m + p] = c * qkp - sn * qkq;
+                    Q[k * m + q] = sn * qkp + c * qkq;
+                }
+            }
+    }
+    lam.resize(m);
+    for (int i = 0; i < m; ++i) lam[i] = A[i * m + i];
+}
+
+// y = exp(-i T t) e_1 for the symmetric tridiagonal T = tri(beta, alpha, beta)
+std::vector<std::complex<double>> tri_expm_e1(int k, const double* alpha, const double* beta, double t) {
+    std::vector<double> A(static_cast<size_t>(k) * k, 0.0), Q, lam;
+    for (int i = 0; i < k; ++i) {
+        A[i * k + i] = alpha[i];
+        if (i + 1 < k) A[i * k + i + 1] = A[(i + 1) * k + i] = beta[i];
+    }
+    jacobi_eig(k, A, Q, lam);
+    std::vector<std::complex<double>> y(k, 0.0);
+    for (int j = 0; j < k; ++j) {
+        const std::complex<double> ph = std::exp(std::complex<double>(0.0, -lam[j] * t)) * Q[0 * k + j];
+        for (int i = 0; i < k; ++i) y[i] += Q[i * k + j] * ph;
+    }
+    return y;
+}
+
+struct KrylovBuf {
+    std::vector<DevState> v;
+    ~KrylovBuf() {
+        for (auto& d : v)
+            if (d.ptr) cudaFree(d.ptr);
+    }
+};
+
+// one Lanczos step of length dt on every batch column; false when maxdim did not converge
+bool lanczos_step(const DevState& psi, Observable& H, double dt, double tol, int maxdim, KrylovBuf& kb,
+                  int* used) {
+    const int64_t B = psi.B;
+    kb.v.reserve(static_cast<size_t>(maxdim) + 2);
+    auto vec = [&](int i) -> DevState {  // by value: the buffer list grows while vectors are in use
+        while (static_cast<int>(kb.v.size()) <= i) {
+            DevState d = psi;
+            d.ptr = dev_alloc(psi.bytes(), true);
+            kb.v.push_back(d);
+        }
+        return kb.v[i];
+    };
+    double* d_ip = static_cast<double*>(scratch(2 * B * sizeof(double), 16));
+    double* d_cf = static_cast<double*>(scratch(2 * B * sizeof(double), 17));
+    std::vector<double> ip(2 * B), cf(2 * B);
+    auto inner = [&](const DevState& a, const DevState* c) {
+        reduce_inner(a, c, d_ip);
+        QBG_CUDA(cudaMemcpyAsync(ip.data(), d_ip, 2 * B * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        stream_sync();
+        return ip;
+    };
+    auto axpy = [&](const DevState& y, const DevState& x, bool overwrite) {
+        QBG_CUDA(cudaMemcpyAsync(d_cf, cf.data(), 2 * B * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+        launch_axpy_batch(y, x, d_cf, overwrite);
+    };
+    // W is slot 0, the basis v_i is slot i + 1
+    std::vector<double> beta0(B);
+    {
+        auto n2 = inner(psi, nullptr);
+        for (int64_t b = 0; b < B; ++b) {
+            beta0[b] = std::sqrt(std::max(0.0, n2[2 * b]));
+            cf[2 * b] = beta0[b] > 0 ? 1.0 / beta0[b] : 0.0;
+            cf[2 * b + 1] = 0.0;
+        }
+        axpy(vec(1), psi, true);
+    }
+    std::vector<std::vector<double>> alpha(B), beta(B);
+    int k = 0;
+    bool ok = false;
+    for (int j = 0; j < maxdim; ++j) {
+        const DevState W = vec(0);
+        run_obs(vec(j + 1), W, H, nullptr);
+        // full re-orthogonalisation, two classical Gram-Schmidt passes (keeps the basis orthonormal
+        // to rounding, so the small-matrix exponential is the exact projection)
+        for (int pass = 0; pass < 2; ++pass)
+            for (int i = 0; i <= j; ++i) {
+                auto h = inner(vec(i + 1), &W);
+                for (int64_t b = 0; b < B; ++b) {
+                    if (pass == 0 && i == j) alpha[b].push_back(h[2 * b]);
+                    cf[2 * b] = -h[2 * b];
+                    cf[2 * b + 1] = -h[2 * b + 1];
+                }
+                axpy(W, vec(i + 1), false);
+            }
+        auto n2 = inner(W, nullptr);
+        double err = 0.0;
+        bool breakdown = true;
+        for (int64_t b = 0; b < B; ++b) {
+            const double bj = std::sqrt(std::max(0.0, n2[2 * b]));
+            beta[b].push_back(bj);
+            if (bj > 1e-14 * std::max(1.0, std::fabs(alpha[b].back()))) breakdown = false;
+            auto y = tri_expm_e1(j + 1, alpha[b].data(), beta[b].data(), dt);
+            err = std::max(err, bj * std::abs(y[j]));
+        }
+        k = j + 1;
+        if (err < tol || breakdown) {
+            ok = true;
+            break;
+        }
+        if (j + 1 < maxdim) {
+            for (int64_t b = 0; b < B; ++b) {
+                cf[2 * b] = beta[b][j] > 0 ? 1.0 / beta[b][j] : 0.0;
+                cf[2 * b + 1] = 0.0;
+            }
+            axpy(vec(j + 2), W, true);
+        }
+    }
+    if (!ok) return false;
+    // psi = beta0 * V y
+    for (int i = 0; i < k; ++i) {
+        for (int64_t b = 0; b < B; ++b) {
+            auto y = tri_expm_e1(k, alpha[b].data(), beta[b].data(), dt);
+            cf[2 * b] = beta0[b] * y[i].real();
+            cf[2 * b + 1] = beta0[b] * y[i].imag();
+        }
+        axpy(psi, vec(i + 1), i == 0);
+    }
+    *used = std::max(*used, k);
+    return true;
+}
+
+}  // namespace
+}  // namespace qbg
+
+extern "C" {
+
+int qbg_time_evolve(qbg_reg* r, const qbg_obs* h, double t, double tol, int32_t maxdim, int32_t* krylov_dim) {
+    return guarded([&] {
+        check_reg(r);
+        if (!h) raise(QBG_ERR_VALIDATION, "time_evolve: null Hamiltonian");
+        auto& H = const_cast<qbg_obs*>(h)->o;
+        if (H.n != r->nactive) raise(QBG_ERR_SHAPE, "time_evolve: Hamiltonian qubit count differs from active qubits");
+        for (const auto& term : H.terms) {  // Hermitian: real coefficients once i^{nY} is divided out
+            const int ny = __builtin_popcountll(term.xmask & term.zmask);
+            std::complex<double> c(term.coef_re, term.coef_im);
+            for (int k = 0; k < ny; ++k) c *= std::complex<double>(0.0, -1.0);
+            if (std::fabs(c.imag()) > 1e-12 * std::max(1.0, std::abs(c)))
+                raise(QBG_ERR_VALIDATION, "time_evolve: the Hamiltonian is not hermitian");
+        }
+        if (!std::isfinite(t)) raise(QBG_ERR_VALIDATION, "time_evolve: non-finite time");
+        if (maxdim <= 0) maxdim = 30;
+        if (tol <= 0) tol = 1e-12;
+        int used = 0;
+        if (t != 0.0 && !H.terms.empty()) {
+            KrylovBuf kb;
+            double rem = t, dt = t;
+            int halvings = 0;
+            while (rem != 0.0) {
+                const double step = std::fabs(dt) < std::fabs(rem) ? dt : rem;
+                if (lanczos_step(r->s, H, step, tol, maxdim, kb, &used)) {
+                    rem -= step;
+                    if (std::fabs(rem) <= 1e-14 * std::fabs(t)) rem = 0.0;
+                } else {
+                    if (++halvings > 40) raise(QBG_ERR_INTERNAL, "time_evolve: Krylov iteration did not converge");
+                    dt *= 0.5;
+                }
+            }
+        }
+        if (krylov_dim) *krylov_dim = used;
+        stream_sync();
     });
 }
 

@@ -53,6 +53,8 @@ void accumulate_grads(const double* d_part, int64_t nslots, int64_t cap, const i
 // ---- elementwise -------------------------------------------------------------------------
 void launch_scale(const DevState& s, double re, double im);
 void launch_axpy(const DevState& y, const DevState& x, double re, double im);
+// y (+)= c_b x with c_b = (d_coef[2b], d_coef[2b+1]) per batch column (device array)
+void launch_axpy_batch(const DevState& y, const DevState& x, const double* d_coef, bool overwrite);
 void launch_set_basis(const DevState& s, const uint64_t* d_bits, int64_t nbits);
 void launch_transpose(const void* src, void* dst, uint64_t rows, int64_t B, int dtype, bool to_device_layout);
 void launch_pauli_axpy(const DevState& psi, const DevState& phi, uint64_t xmask, uint64_t zmask, double cre,

@@ -352,6 +352,17 @@ __global__ void k_axpy(V* y, const V* x, uint64_t n, double re, double im) {
         y[i] = cfma(y[i], mk<V>(re, im), x[i]);
 }
 
+// y[i, b] (+)= c_b x[i, b] with one complex coefficient per batch column (Krylov bases)
+template <typename V>
+__global__ void k_axpy_b(V* y, const V* x, uint64_t n, int64_t B, const double* __restrict__ coef, bool overwrite) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const int64_t b = B == 1 ? 0 : static_cast<int64_t>(i % static_cast<uint64_t>(B));
+        const V c = mk<V>(coef[2 * b], coef[2 * b + 1]);
+        y[i] = overwrite ? cmul(c, x[i]) : cfma(y[i], c, x[i]);
+    }
+}
+
 template <typename V>
 __global__ void k_set_basis(V* st, uint64_t rows, int64_t B, const uint64_t* bits, int64_t nbits) {
     uint64_t total = rows * B;
@@ -563,6 +574,19 @@ void launch_scale(const DevState& s, double re, double im) {
         k_scale<double2><<<egrid(s.count()), 256, 0, stream()>>>(static_cast<double2*>(s.ptr), s.count(), re, im);
     else
         k_scale<float2><<<egrid(s.count()), 256, 0, stream()>>>(static_cast<float2*>(s.ptr), s.count(), re, im);
+    QBG_CUDA(cudaGetLastError());
+}
+
+void launch_axpy_batch(const DevState& y, const DevState& x, const double* d_coef, bool overwrite) {
+    LaunchScope ls("axpy_batch", (overwrite ? 2.0 : 3.0) * y.bytes());
+    if (y.dtype == QBG_C128)
+        k_axpy_b<double2><<<egrid(y.count()), 256, 0, stream()>>>(static_cast<double2*>(y.ptr),
+                                                                  static_cast<const double2*>(x.ptr), y.count(), y.B,
+                                                                  d_coef, overwrite);
+    else
+        k_axpy_b<float2><<<egrid(y.count()), 256, 0, stream()>>>(static_cast<float2*>(y.ptr),
+                                                                 static_cast<const float2*>(x.ptr), y.count(), y.B,
+                                                                 d_coef, overwrite);
     QBG_CUDA(cudaGetLastError());
 }
 

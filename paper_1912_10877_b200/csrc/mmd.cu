@@ -113,7 +113,7 @@ void launch_mmd(int mode, const DevState& psi, const DevState* other, const DevS
     const uint64_t ntiles = (psi.rows() + TX - 1) / TX;
     const int64_t nbc = (psi.B + BC - 1) / BC;
     const uint64_t grid = ntiles * static_cast<uint64_t>(nbc);
-    double* part = static_cast<double*>(scratch(ntiles * psi.B * sizeof(double), 13));
+    double* part = static_cast<double*>(scratch(ntiles * psi.B * sizeof(double), 18));
     {
         const double reads = (mode == 2 ? 2.0 : 1.0) * psi.bytes() + (mode == 1 ? 1.0 : 0.0) * psi.bytes();
         LaunchScope ls(mode == 0 ? "mmd_loss" : mode == 1 ? "mmd_seed" : "mmd_cross", reads);

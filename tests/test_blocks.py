@@ -99,3 +99,24 @@ def test_lowering_matches_dense_operator(orc, seed):
 def test_observable_rejects_non_pauli():
     with pytest.raises(errors.UnsupportedError):
         B.pauli_terms(B.put(2, 1, B.H))
+
+
+def test_time_evolution_blocks_host():
+    """time_evolve / cache structure on the host: the evolution time is a
+    parameter, circuits split into gate segments and Krylov steps, dagger negates t."""
+    from paper_1912_10877_b200 import blocks as Bk
+    from paper_1912_10877_b200 import circuits as Cc
+    from paper_1912_10877_b200 import errors as Er
+    n = 5
+    h = Cc.heisenberg(n)
+    te = Bk.time_evolve(Bk.cache(h), 0.25)
+    circ = Bk.chain(n, Cc.variational_circuit(n, 1), te, Bk.put(n, 2, Bk.Rx(0.3)))
+    assert Bk.nparameters(circ) == Bk.nparameters(Cc.variational_circuit(n, 1)) + 2
+    assert [k for k, _ in Bk.segments(circ)] == ["prog", "te", "prog"]
+    assert Bk.dagger(te).theta == -0.25
+    assert len(Bk.pauli_terms(Bk.cache(h))) == len(Bk.pauli_terms(h))
+    import pytest as _pt
+    with _pt.raises(Er.UnsupportedError):
+        Bk.time_evolve(Bk.put(n, 1, Bk.H), 0.1)
+    with _pt.raises(Er.UnsupportedError):
+        Bk.segments(Bk.put(n, (1, 2), Bk.time_evolve(Cc.heisenberg(2), 0.1)))

@@ -198,3 +198,18 @@ def test_mmd_oracle_zero_and_fd(orc):
     assert np.isclose(kf(3, 5), np.exp(-4 / 8) + np.exp(-4 / (2 * 0.49)))
     with pytest.raises(Exception):
         brbf_kernel(-1.0)
+
+
+def test_pauli_dense_matches_oracle_obs_apply(orc):
+    """The dense Hamiltonian used as the time-evolution oracle applies like orc_obs_apply."""
+    from paper_1912_10877_b200 import blocks as Bk
+    n = 5
+    st = orc.rand_state(n, 2, 3)
+    for blk in (C.heisenberg(n), Bk.kron(n, ((1,), Bk.Y), ((4,), Bk.Y), ((2,), Bk.Z))):
+        t = Bk.pauli_terms(blk)
+        H = O.pauli_dense(t, n)
+        phi, _ = orc.obs_apply(st, t)
+        assert np.abs(phi - (H @ st.T).T).max() < 1e-14
+        assert np.abs(H - H.conj().T).max() == 0
+    U = O.expm_apply(np.eye(1 << 3), Bk.pauli_terms(C.heisenberg(3)), 3, 0.4)
+    assert np.abs(U @ U.conj().T - np.eye(8)).max() < 1e-13
