@@ -1391,17 +1391,30 @@ std::vector<std::complex<double>> tri_expm_e1(int k, const double* alpha, const 
     return y;
 }
 
+// Krylov basis buffers, kept between calls (cudaMalloc / cudaFree of tens of state-sized buffers
+// per evolve call would dominate); released when the state shape changes
 struct KrylovBuf {
     std::vector<DevState> v;
+    void fit(const DevState& s) {
+        if (!v.empty() && (v[0].bytes() != s.bytes() || v[0].dtype != s.dtype)) {
+            stream_sync();
+            for (auto& d : v)
+                if (d.ptr) cudaFree(d.ptr);
+            v.clear();
+        }
+    }
     ~KrylovBuf() {
         for (auto& d : v)
             if (d.ptr) cudaFree(d.ptr);
     }
 };
 
-// one Lanczos step of length dt on every batch column; false when maxdim did not converge
-bool lanczos_step(const DevState& psi, Observable& H, double dt, double tol, int maxdim, KrylovBuf& kb,
-                  int* used) {
+// Lanczos on every batch column: builds the Krylov basis of H at psi until the residual estimate
+// of e^{-iH dt} drops below tol (or maxdim vectors); when the full basis does not reach tol for dt,
+// the largest dt' <= dt it does reach is taken instead (no matvec is wasted).  psi advances by the
+// returned time.
+double lanczos_step(const DevState& psi, Observable& H, double dt, double tol, int maxdim, KrylovBuf& kb,
+                    int* used) {
     const int64_t B = psi.B;
     kb.v.reserve(static_cast<size_t>(maxdim) + 2);
     auto vec = [&](int i) -> DevState {  // by value: the buffer list grows while vectors are in use
@@ -1410,15 +1423,22 @@ bool lanczos_step(const DevState& psi, Observable& H, double dt, double tol, int
             d.ptr = dev_alloc(psi.bytes(), true);
             kb.v.push_back(d);
         }
-        return kb.v[i];
+        DevState d = kb.v[i];
+        d.n = psi.n;  // same bytes / dtype; the view follows the caller's shape
+        d.B = psi.B;
+        return d;
     };
-    double* d_ip = static_cast<double*>(scratch(2 * B * sizeof(double), 16));
-    double* d_cf = static_cast<double*>(scratch(2 * B * sizeof(double), 17));
-    std::vector<double> ip(2 * B), cf(2 * B);
+    const size_t nd = static_cast<size_t>(2 * std::max<int64_t>(B, maxdim + 2));
+    double* d_ip = static_cast<double*>(scratch(nd * sizeof(double), 16));
+    double* d_cf = static_cast<double*>(scratch(nd * sizeof(double), 17));
+    std::vector<double> ip(nd), cf(nd);
+    auto fetch = [&](size_t cnt) {
+        QBG_CUDA(cudaMemcpyAsync(ip.data(), d_ip, cnt * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+        stream_sync();
+    };
     auto inner = [&](const DevState& a, const DevState* c) {
         reduce_inner(a, c, d_ip);
-        QBG_CUDA(cudaMemcpyAsync(ip.data(), d_ip, 2 * B * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
-        stream_sync();
+        fetch(2 * B);
         return ip;
     };
     auto axpy = [&](const DevState& y, const DevState& x, bool overwrite) {
@@ -1437,36 +1457,64 @@ bool lanczos_step(const DevState& psi, Observable& H, double dt, double tol, int
         axpy(vec(1), psi, true);
     }
     std::vector<std::vector<double>> alpha(B), beta(B);
+    auto error_at = [&](int k, double t) {  // max over batch columns of beta_k |e_k^T exp(-iTt) e_1|
+        double err = 0.0;
+        for (int64_t b = 0; b < B; ++b) {
+            auto y = tri_expm_e1(k, alpha[b].data(), beta[b].data(), t);
+            err = std::max(err, beta[b][k - 1] * std::abs(y[k - 1]));
+        }
+        return err;
+    };
     int k = 0;
-    bool ok = false;
+    double adv = 0.0;
     for (int j = 0; j < maxdim; ++j) {
         const DevState W = vec(0);
         run_obs(vec(j + 1), W, H, nullptr);
         // full re-orthogonalisation, two classical Gram-Schmidt passes (keeps the basis orthonormal
         // to rounding, so the small-matrix exponential is the exact projection)
-        for (int pass = 0; pass < 2; ++pass)
-            for (int i = 0; i <= j; ++i) {
-                auto h = inner(vec(i + 1), &W);
-                for (int64_t b = 0; b < B; ++b) {
-                    if (pass == 0 && i == j) alpha[b].push_back(h[2 * b]);
-                    cf[2 * b] = -h[2 * b];
-                    cf[2 * b + 1] = -h[2 * b + 1];
+        if (B == 1) {
+            // first pass also measures ||W||^2 (W against itself); the second pass runs only when
+            // the projection removed more than half of it (DGKS criterion: cancellation)
+            std::vector<DevState> basis;
+            for (int i = 0; i <= j; ++i) basis.push_back(vec(i + 1));
+            for (int pass = 0; pass < 2; ++pass) {
+                std::vector<DevState> with_w = basis;
+                if (pass == 0) with_w.push_back(W);
+                multi_inner(W, with_w, d_ip);
+                fetch(2 * with_w.size());
+                if (pass == 0) alpha[0].push_back(ip[2 * j]);
+                std::vector<double> c(2 * (j + 1));
+                double proj = 0.0;
+                for (int i = 0; i <= j; ++i) {
+                    c[2 * i] = -ip[2 * i];
+                    c[2 * i + 1] = -ip[2 * i + 1];
+                    proj += ip[2 * i] * ip[2 * i] + ip[2 * i + 1] * ip[2 * i + 1];
                 }
-                axpy(W, vec(i + 1), false);
+                multi_axpy(W, basis, c);
+                if (pass == 0 && proj < 0.5 * ip[2 * (j + 1)]) break;
             }
+        } else {
+            for (int pass = 0; pass < 2; ++pass)
+                for (int i = 0; i <= j; ++i) {
+                    auto h = inner(vec(i + 1), &W);
+                    for (int64_t b = 0; b < B; ++b) {
+                        if (pass == 0 && i == j) alpha[b].push_back(h[2 * b]);
+                        cf[2 * b] = -h[2 * b];
+                        cf[2 * b + 1] = -h[2 * b + 1];
+                    }
+                    axpy(W, vec(i + 1), false);
+                }
+        }
         auto n2 = inner(W, nullptr);
-        double err = 0.0;
         bool breakdown = true;
         for (int64_t b = 0; b < B; ++b) {
             const double bj = std::sqrt(std::max(0.0, n2[2 * b]));
             beta[b].push_back(bj);
             if (bj > 1e-14 * std::max(1.0, std::fabs(alpha[b].back()))) breakdown = false;
-            auto y = tri_expm_e1(j + 1, alpha[b].data(), beta[b].data(), dt);
-            err = std::max(err, bj * std::abs(y[j]));
         }
         k = j + 1;
-        if (err < tol || breakdown) {
-            ok = true;
+        if (breakdown || error_at(k, dt) < tol) {
+            adv = dt;
             break;
         }
         if (j + 1 < maxdim) {
@@ -1477,18 +1525,42 @@ bool lanczos_step(const DevState& psi, Observable& H, double dt, double tol, int
             axpy(vec(j + 2), W, true);
         }
     }
-    if (!ok) return false;
-    // psi = beta0 * V y
-    for (int i = 0; i < k; ++i) {
-        for (int64_t b = 0; b < B; ++b) {
-            auto y = tri_expm_e1(k, alpha[b].data(), beta[b].data(), dt);
-            cf[2 * b] = beta0[b] * y[i].real();
-            cf[2 * b + 1] = beta0[b] * y[i].imag();
+    if (adv == 0.0) {  // the full basis: the largest step it resolves to tol (bisection on |t|)
+        double lo = 0.0, hi = dt;
+        for (int it = 0; it < 60; ++it) {
+            const double mid = 0.5 * (lo + hi);
+            if (error_at(k, mid) < tol)
+                lo = mid;
+            else
+                hi = mid;
         }
-        axpy(psi, vec(i + 1), i == 0);
+        adv = lo;
+        if (adv == 0.0) return 0.0;
+    }
+    // psi = beta0 * V y(adv)
+    std::vector<std::vector<std::complex<double>>> ys(B);
+    for (int64_t b = 0; b < B; ++b) ys[b] = tri_expm_e1(k, alpha[b].data(), beta[b].data(), adv);
+    if (B == 1) {
+        std::vector<DevState> basis;
+        std::vector<double> c(2 * k);
+        for (int i = 0; i < k; ++i) {
+            basis.push_back(vec(i + 1));
+            c[2 * i] = beta0[0] * ys[0][i].real();
+            c[2 * i + 1] = beta0[0] * ys[0][i].imag();
+        }
+        QBG_CUDA(cudaMemsetAsync(psi.ptr, 0, psi.bytes(), g_stream));
+        multi_axpy(psi, basis, c);
+    } else {
+        for (int i = 0; i < k; ++i) {
+            for (int64_t b = 0; b < B; ++b) {
+                cf[2 * b] = beta0[b] * ys[b][i].real();
+                cf[2 * b + 1] = beta0[b] * ys[b][i].imag();
+            }
+            axpy(psi, vec(i + 1), i == 0);
+        }
     }
     *used = std::max(*used, k);
-    return true;
+    return adv;
 }
 
 }  // namespace
@@ -1511,21 +1583,20 @@ int qbg_time_evolve(qbg_reg* r, const qbg_obs* h, double t, double tol, int32_t 
         }
         if (!std::isfinite(t)) raise(QBG_ERR_VALIDATION, "time_evolve: non-finite time");
         if (maxdim <= 0) maxdim = 30;
+        maxdim = std::min(maxdim, 60);
         if (tol <= 0) tol = 1e-12;
         int used = 0;
         if (t != 0.0 && !H.terms.empty()) {
-            KrylovBuf kb;
-            double rem = t, dt = t;
-            int halvings = 0;
+            static thread_local KrylovBuf kb;
+            kb.fit(r->s);
+            double rem = t;
+            int steps = 0;
             while (rem != 0.0) {
-                const double step = std::fabs(dt) < std::fabs(rem) ? dt : rem;
-                if (lanczos_step(r->s, H, step, tol, maxdim, kb, &used)) {
-                    rem -= step;
-                    if (std::fabs(rem) <= 1e-14 * std::fabs(t)) rem = 0.0;
-                } else {
-                    if (++halvings > 40) raise(QBG_ERR_INTERNAL, "time_evolve: Krylov iteration did not converge");
-                    dt *= 0.5;
-                }
+                const double adv = lanczos_step(r->s, H, rem, tol, maxdim, kb, &used);
+                if (adv == 0.0 || ++steps > 100000)
+                    raise(QBG_ERR_INTERNAL, "time_evolve: Krylov iteration made no progress");
+                rem -= adv;
+                if (std::fabs(rem) <= 1e-14 * std::fabs(t)) rem = 0.0;
             }
         }
         if (krylov_dim) *krylov_dim = used;

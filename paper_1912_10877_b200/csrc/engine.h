@@ -69,6 +69,11 @@ void launch_mmd(int mode, const DevState& psi, const DevState* other, const DevS
                 const double* d_w, int D, double* d_loss);
 bool mmd_geometry(uint64_t rows, int64_t B, int D, int* TX, int* BC, size_t* smem);
 
+// ---- Krylov multi-vector kernels (krylov.cu; one batch column) ----
+// d_out[2i], d_out[2i+1] = <vs[i] | w>;  w += Σ_i coef_i vs[i]
+void multi_inner(const DevState& w, const std::vector<DevState>& vs, double* d_out);
+void multi_axpy(const DevState& w, const std::vector<DevState>& vs, const std::vector<double>& coef);
+
 // scratch device memory owned by the library (grows; stream-ordered reuse)
 void* scratch(size_t bytes, int slot);
 
