@@ -270,24 +270,24 @@ struct FusedPlan {
     SGroup* d_groups = nullptr;
     STerm* d_terms = nullptr;
     ~FusedPlan() {
-        cudaFree(d_ops);
-        cudaFree(d_mats);
-        cudaFree(d_epi);
-        cudaFree(d_ptr);
-        cudaFree(d_idx);
-        cudaFree(d_groups);
-        cudaFree(d_terms);
+        for (void* p : {static_cast<void*>(d_ops), static_cast<void*>(d_mats), static_cast<void*>(d_epi),
+                        static_cast<void*>(d_ptr), static_cast<void*>(d_idx), static_cast<void*>(d_groups),
+                        static_cast<void*>(d_terms)})
+            if (p) cudaFreeAsync(p, stream());
     }
 };
 
 namespace {
 
+// Plan tables are small and re-made for every new parameter vector: stream-ordered allocation,
+// copy and free (cudaMalloc / cudaMemcpy / cudaFree would synchronise the device and serialise
+// the host planning of the reverse pass behind the forward passes already queued).
 template <class T>
 T* upload(const std::vector<T>& v) {
     T* d = nullptr;
     if (v.empty()) return nullptr;
-    QBG_CUDA(cudaMalloc(&d, v.size() * sizeof(T)));
-    QBG_CUDA(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    QBG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), v.size() * sizeof(T), stream()));
+    QBG_CUDA(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, stream()));
     return d;
 }
 
