@@ -76,6 +76,11 @@ int consumer_groups() {
     return g;
 }
 constexpr int kProducerThreads = 128;
+// producer threads of a pass (one warpgroup; QBG_FWD_PRODUCERS=256 gives the forward passes two)
+int producer_threads(bool back) {
+    static const int f = env_int("QBG_FWD_PRODUCERS", kProducerThreads);
+    return back ? kProducerThreads : (f == 256 ? 256 : kProducerThreads);
+}
 bool perm_ctrl_regs() {
     static const bool on = env_int("QBG_PERM_CTRL_REGS", 1) != 0;
     return on;
@@ -733,7 +738,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
     const size_t tile_bytes = tile_elems * elem;
     const std::string SYNC = pipe ? "group_bar<" + std::to_string(TH) + ">(1 + cg);\n" : "__syncthreads();\n";
     std::ostringstream s;
-    const int NP = pipe ? kProducerThreads : 0;
+    const int NP = pipe ? producer_threads(back) : 0;
     s << "extern \"C\" __global__ void __launch_bounds__(" << NG * TH + NP << ", "
       << (pipe ? 1 : ctas_per_sm(back, TH)) << ") __NAME__(" << (c128 ? "c128" : "c64") << "* __restrict__ psi, "
       << (c128 ? "c128" : "c64")
@@ -1281,7 +1286,7 @@ void launch_jit(V* psi, V* adj, Step& st, FusedPlan& pl, double* gpart, int64_t 
     int gbase = P.grad_base;
     void* args[] = {&psi, &adj, &gpart, &gcols, &gbase, st.blob.data()};
     LaunchScope ls(BACK ? "fused_bwd" : "fused_fwd", bytes, st.flops);
-    jit::launch(pl.jk[st.jk], static_cast<unsigned>(grid), pipe ? consumer_groups() * T + kProducerThreads : T, st.smem,
+    jit::launch(pl.jk[st.jk], static_cast<unsigned>(grid), pipe ? consumer_groups() * T + producer_threads(BACK) : T, st.smem,
                 args);
 }
 
