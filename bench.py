@@ -163,6 +163,20 @@ def fp64_roofline(top, per_launch_ms):
             "flops_per_launch": top["flops"] / top["launches"], "peak_source": src}
 
 
+def per_gate_roofline(top, per_launch_ms, G, S, peak):
+    """SURVEY §8(d)'s algorithmic unit: one gate on one state = 2S bytes, a reverse-pass gate = 2
+    units.  The fused launches of a step together apply every gate once, so one launch of the
+    dominant kernel stands for (gates x bytes per gate) / (its launches per step); above 1.0 means
+    fusion beat the per-gate roofline."""
+    if not top or top["name"] not in ("fused_bwd", "fused_fwd"):
+        return None
+    per_gate = (4 if top["name"] == "fused_bwd" else 2) * S
+    bpl = G * per_gate / (top["launches"] / 2)
+    ach = bpl / (per_launch_ms / 1e3) / 1e9
+    return {"achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak, "bytes_per_launch": bpl,
+            "unit_definition": "2S per gate per state pass (forward 2S, reverse 4S), SURVEY 8(d)"}
+
+
 def workload_config(args):
     n, d = args.qubits, args.depth
     G, P, T = n * (1 + 4 * d), n * (1 + 3 * d), 3 * (n - 1)
@@ -315,6 +329,7 @@ def main():
                     "bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms, "share_of_step": share,
                     "peak_source": peak_src,
                     "fp64": fp64_roofline(top, per_launch_ms),
+                    "per_gate_convention": per_gate_roofline(top, per_launch_ms, G, S, peak),
                     "kernels": [{k2: (round(v, 6) if isinstance(v, float) else v) for k2, v in kk.items()}
                                 for kk in kernels[:8]]}
 
