@@ -886,7 +886,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         s << "V* sx = ring + (size_t)slot * " << tile_elems << "u; V* sy = sx + " << (1 << M) << ";\n";
         s << "u64 outer; i64 tb; tile_geo(tile, outer, tb);\n";
         for (int j = 0; j < R; ++j) {  // stage 0 from the linear (copied) layout
-            if (exp_mode == 5) {  // (diagnostics: synthetic tile, no slot reads / global stores)
+            if (exp_mode == 5 || exp_mode == 6) {  // (diagnostics: synthetic tile, no slot reads / global stores)
                 s << "x[" << j << "] = mk<V>((double)(tid + " << j << ") * 1e-3, (double)tile * 1e-9);";
                 if (back) s << " y[" << j << "] = mk<V>((double)(tid - " << j << ") * 1e-3, 1e-9);";
             } else {
@@ -899,7 +899,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
     }
     for (int st = 0; st < P.nstages; ++st) {
         const DStage& S = P.st[st];
-        if (st > 0 && exp_mode != 4) {  // (QBG_EXP=4, diagnostics: no transposes)
+        if (st > 0 && exp_mode != 4 && exp_mode != 6) {  // (QBG_EXP=4/6, diagnostics: no transposes)
             const DStage& Sp = P.st[st - 1];
             for (int j = 0; j < R; ++j) {
                 s << "sx[st" << st - 1 << " ^ " << soff(Sp, j) << "u] = x[" << j << "];";
@@ -1090,13 +1090,13 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         }
         s << SYNC << "if (tid == 0) mbar_arrive(done + slot);\n";
     } else {
-        if (exp_mode == 1 || exp_mode == 5) s << "if (outer == ~0ull) {\n";
+        if (exp_mode == 1 || exp_mode == 5 || exp_mode == 6) s << "if (outer == ~0ull) {\n";
         for (int j = 0; j < R; ++j) {
             s << "psi[tb + gL + " << goff(SL, j) << "ll] = x[" << j << "];";
             if (back) s << " adj[tb + gL + " << goff(SL, j) << "ll] = y[" << j << "];";
             s << "\n";
         }
-        if (exp_mode == 1 || exp_mode == 5) s << "}\n";
+        if (exp_mode == 1 || exp_mode == 5 || exp_mode == 6) s << "}\n";
         if (pipe) s << SYNC << "if (tid == 0) mbar_arrive(done + slot);\n";
     }
     s << "}\n";  // tile loop
