@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--no-fusion", action="store_true")
+    ap.add_argument("--dtype", default="c128", choices=["c128", "c64"])
     a = ap.parse_args()
     qb.set_fusion(not a.no_fusion)
     if a.qubits > qb.qubit_cap():
@@ -26,7 +27,7 @@ def main():
     circ = qb.variational_circuit(a.qubits, a.depth)
     qb.dispatch(circ, "random")
     h = qb.heisenberg(a.qubits)
-    reg = qb.zero_state(a.qubits, a.batch)
+    reg = qb.zero_state(a.qubits, a.batch, dtype=a.dtype)
     for _ in range(a.steps):
         t0 = time.perf_counter()
         r = qb.expect_grad(h, (reg, circ))
