@@ -165,7 +165,6 @@ M2 m2_mul(const M2& A, const M2& Bm) {
     return r;
 }
 M2 m2_dag(const M2& A) { return {cc(A[0]), cc(A[2]), cc(A[1]), cc(A[3])}; }
-M2 m2_id() { return {cdbl{1, 0}, cdbl{0, 0}, cdbl{0, 0}, cdbl{1, 0}}; }
 
 // new ∘ old for two 1-qubit gates on the same qubit
 Gate compose1(const Gate& nw, const Gate& old) {
