@@ -154,21 +154,26 @@ __device__ __forceinline__ void gcross1(const V* p, const V* a, double* c) {
 // c[0] = Im C00, c[1] = Im C11, c[2] = Im(C01 + C10), c[3] = Re(C01 − C10): 12 DFMA per pair.
 template <class V, int R, int K>
 __device__ __forceinline__ void gcrossh(const V* p, const V* a, double* c) {
-  double i01 = 0.0, i10 = 0.0, r01 = 0.0, r10 = 0.0;
+  // the in-thread sum over the R/2 pairs runs in the element type (complex64: FP32 — 8 terms,
+  // far inside its 1e-5 tolerance); the warp and tile reductions that follow are in double
+  typedef typename RT<V>::T T;
+  T c0 = 0, c1 = 0, i01 = 0, i10 = 0, r01 = 0, r10 = 0;
 #pragma unroll
   for (int j = 0; j < R; ++j) {
     if (j & (1 << K)) continue;
-    const double a0x = a[j].x, a0y = a[j].y, a1x = a[j | (1 << K)].x, a1y = a[j | (1 << K)].y;
-    const double p0x = p[j].x, p0y = p[j].y, p1x = p[j | (1 << K)].x, p1y = p[j | (1 << K)].y;
-    c[0] = fma(a0x, p0y, fma(-a0y, p0x, c[0]));
-    c[1] = fma(a1x, p1y, fma(-a1y, p1x, c[1]));
+    const T a0x = a[j].x, a0y = a[j].y, a1x = a[j | (1 << K)].x, a1y = a[j | (1 << K)].y;
+    const T p0x = p[j].x, p0y = p[j].y, p1x = p[j | (1 << K)].x, p1y = p[j | (1 << K)].y;
+    c0 = fma(a0x, p0y, fma(-a0y, p0x, c0));
+    c1 = fma(a1x, p1y, fma(-a1y, p1x, c1));
     i01 = fma(a0x, p1y, fma(-a0y, p1x, i01));
     i10 = fma(a1x, p0y, fma(-a1y, p0x, i10));
     r01 = fma(a0x, p1x, fma(a0y, p1y, r01));
     r10 = fma(a1x, p0x, fma(a1y, p0y, r10));
   }
-  c[2] += i01 + i10;
-  c[3] += r01 - r10;
+  c[0] += (double)c0;
+  c[1] += (double)c1;
+  c[2] += (double)i01 + (double)i10;
+  c[3] += (double)r01 - (double)r10;
 }
 // diagonal run: c[b] += Σ Im(conj(a) p) over the elements whose run bit is b — register slot K
 template <class V, int R, int K>
