@@ -81,6 +81,10 @@ int producer_threads(bool back) {
     static const int f = env_int("QBG_FWD_PRODUCERS", kProducerThreads);
     return back ? kProducerThreads : (f == 256 ? 256 : kProducerThreads);
 }
+bool dense_pair() {  // reverse 2x2 uncomputes of ψ and φ̄ interleaved in one template (QBG_DENSE_PAIR)
+    static const bool on = env_int("QBG_DENSE_PAIR", 0) != 0;  // measured slower (register pressure)
+    return on;
+}
 bool perm_ctrl_regs() {
     static const bool on = env_int("QBG_PERM_CTRL_REGS", 1) != 0;
     return on;
@@ -943,7 +947,10 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                     s << "if (" << cond << ") { const V m00 = MV(" << o << "), m10 = MV(" << o + 1 << "), m01 = MV(" << o + 2
                       << "), m11 = MV(" << o + 3 << "); ";
                     std::string tp = "<V, R, " + std::to_string(op.a) + ", " + t5 + ">";
-                    both("dense1" + tp + "(x, m00, m10, m01, m11);", "dense1" + tp + "(y, m00, m10, m01, m11);");
+                    if (back && dense_pair())
+                        s << "dense1x2" << tp << "(x, y, m00, m10, m01, m11);";
+                    else
+                        both("dense1" + tp + "(x, m00, m10, m01, m11);", "dense1" + tp + "(y, m00, m10, m01, m11);");
                     s << " }\n";
                     break;
                 }

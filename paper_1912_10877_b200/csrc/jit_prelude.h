@@ -34,6 +34,20 @@ __device__ __forceinline__ void dense1(V* x, V m00, V m10, V m01, V m11) {
     x[j | (1 << K)] = cfma(cmul(m10, a), m11, b);
   }
 }
+// the same 2x2 on two register tiles at once (reverse pass: ψ and φ̄), pairs interleaved
+template <class V, int R, int K, int CM, int CV>
+__device__ __forceinline__ void dense1x2(V* x, V* y, V m00, V m10, V m01, V m11) {
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    if (j & (1 << K)) continue;
+    if ((j & CM) != CV) continue;
+    V a = x[j], b = x[j | (1 << K)], c = y[j], d = y[j | (1 << K)];
+    x[j] = cfma(cmul(m00, a), m01, b);
+    y[j] = cfma(cmul(m00, c), m01, d);
+    x[j | (1 << K)] = cfma(cmul(m10, a), m11, b);
+    y[j | (1 << K)] = cfma(cmul(m10, c), m11, d);
+  }
+}
 template <class V, int R, int K, int CM, int CV>
 __device__ __forceinline__ void swap1(V* x) {
 #pragma unroll
