@@ -81,6 +81,10 @@ int producer_threads(bool back) {
     static const int f = env_int("QBG_FWD_PRODUCERS", kProducerThreads);
     return back ? kProducerThreads : (f == 256 ? 256 : kProducerThreads);
 }
+int seed_minb() {  // CTAs per SM the seed kernels are compiled for (2: 128 registers, a few spills)
+    static const int m = std::max(1, env_int("QBG_SEED_MINB", 2));  // measured: 2 (0.343 vs 0.373 ms)
+    return m;
+}
 bool dense_pair() {  // reverse 2x2 uncomputes of ψ and φ̄ interleaved in one template (QBG_DENSE_PAIR)
     static const bool on = env_int("QBG_DENSE_PAIR", 0) != 0;  // measured slower (register pressure)
     return on;
@@ -1630,7 +1634,7 @@ std::string gen_seed(const SPass& sp, const std::vector<SGroup>& groups, const s
     std::ostringstream s;
     int nterm = 0;
     for (int gi = sp.g0; gi < sp.g1; ++gi) nterm += groups[gi].term_end - groups[gi].term_begin;
-    s << "extern \"C\" __global__ void __launch_bounds__(" << T << ", 2) __NAME__(const " << (c128 ? "c128" : "c64")
+    s << "extern \"C\" __global__ void __launch_bounds__(" << T << ", " << seed_minb() << ") __NAME__(const " << (c128 ? "c128" : "c64")
       << "* __restrict__ psi, " << (c128 ? "c128" : "c64")
       << "* __restrict__ phi, double* __restrict__ epart, const __grid_constant__ PM<" << (c128 ? "double" : "float")
       << ", " << std::max(2, 2 * nterm) << "> pm) {\n";
