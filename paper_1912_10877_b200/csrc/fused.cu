@@ -783,7 +783,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         s << "if (tid_all == 0) { for (int i = 0; i < " << nbuf << "; ++i) { mbar_init(full + i, " << NP
           << "); mbar_init(done + i, 1); } }\n";
         if (back) s << "for (int i = tid_all; i < " << P.ngrad * CS << "; i += " << NG * TH + NP << ") sg[i] = 0.0;\n";
-        s << "__syncthreads();\n";
+        s << "__syncthreads();\npdl_wait();\n";  // the previous pass's writes are visible after this
         s << "if (tid_all >= " << NG * TH << ") {  // producer warpgroup\n";
         if (NG > 1 && 65536 / (NG * TH + NP) / 8 * 8 > kProducerRegs) s << "reg_dealloc<" << kProducerRegs << ">();\n";
         s << "const int lane = tid_all - " << NG * TH << ";\n";
@@ -873,6 +873,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
     // 2 = no gate ops (pure load / transpose / store) — splits a pass into compute and memory time
     const int exp_mode = env_int("QBG_EXP", 0);
     if (!pipe) {
+        s << "pdl_wait();\n";
         s << "for (u64 tile = blockIdx.x; tile < " << P.ntiles << "ull; tile += gridDim.x) {\n";
         s << "u64 outer; i64 tb; tile_geo(tile, outer, tb);\n";
         for (int j = 0; j < R; ++j) {
@@ -1652,6 +1653,7 @@ std::string gen_seed(const SPass& sp, const std::vector<SGroup>& groups, const s
     for (int p = 0; p < TB; ++p) wt[p] = goff(1u << p);
     s << "const i64 gt = " << tid_sum(wt, TB, false) << ";\n";
     s << "V acc[" << R << "];\n";
+    s << "pdl_wait();\n";  // launched with programmatic stream serialisation (jit::launch)
     s << "for (u64 tile = blockIdx.x; tile < " << sp.ntiles << "ull; tile += gridDim.x) {\n";
     if (sp.nchunks == 1)
         s << "const u64 o = tile; const u64 c = 0;\n";

@@ -250,7 +250,24 @@ void launch(Kernel& k, unsigned grid, unsigned block, size_t smem, void** args) 
         QBG_CUDA(cudaKernelSetAttributeForDevice(k.k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem), dev));
         k.max_dyn_smem = static_cast<int>(smem);
     }
-    QBG_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(k.k), dim3(grid), dim3(block), args, smem, stream()));
+    // programmatic dependent launch: the next pass's launch and prologue (barrier init, gradient
+    // cells) overlap this pass's tail; the generated kernels wait (griddepcontrol.wait) before
+    // touching global memory
+    static const bool pdl = [] {
+        const char* e = std::getenv("QBG_PDL");
+        return !(e && e[0] == '0');
+    }();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream();
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    QBG_CUDA(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k.k), args));
 }
 
 }  // namespace jit

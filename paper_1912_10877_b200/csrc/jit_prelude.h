@@ -247,6 +247,9 @@ template <int NT>
 __device__ __forceinline__ void named_bar() { asm volatile("bar.sync 1, %0;\n" :: "n"(NT) : "memory"); }
 // shared-memory swizzle of a tile-local element index (same as the host planner's swz)
 __device__ __forceinline__ unsigned swz(unsigned l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9) ^ (l >> 12) ^ (l >> 15)) & 7u); }
+// programmatic dependent launch: block until the preceding grid in the stream has completed and
+// its memory is visible (every specialised kernel calls this before touching global memory)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 // barrier over NT threads with a runtime id (one id per consumer group)
 template <int NT>
 __device__ __forceinline__ void group_bar(int id) { asm volatile("bar.sync %0, %1;\n" :: "r"(id), "n"(NT) : "memory"); }
