@@ -72,6 +72,7 @@ bool pipeline_enabled() {
     return on;
 }
 int consumer_groups() {
+    // (4 groups of 64 threads with 2^10 tiles measured slower per gate; 2 is the design point)
     static const int g = std::min(2, std::max(1, env_int("QBG_PIPE", 2)));
     return g;
 }
@@ -740,7 +741,8 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
     // who writes the results: with a deep ring the producer drains each computed slot to global
     // memory (consumers only compute); with a shallow one (reverse pass: 3 slots of 2 states) the
     // drain would delay the refill, so the consumers store from registers and release the slot
-    const bool pstore = pipe && nbuf >= 2 * NG + 2;
+    static const int pstore_extra = env_int("QBG_PSTORE_EXTRA", NG + 2);  // spare slots the drain needs
+    const bool pstore = pipe && nbuf >= NG + pstore_extra;
     const size_t tile_elems = static_cast<size_t>(back ? 2 : 1) << M;
     const size_t tile_bytes = tile_elems * elem;
     const std::string SYNC = pipe ? "group_bar<" + std::to_string(TH) + ">(1 + cg);\n" : "__syncthreads();\n";
