@@ -244,6 +244,18 @@ int qbg_expect_grad(qbg_reg* reg, const qbg_prog* prog, const qbg_obs* obs, int3
    Errors: non-hermitian H -> QBG_ERR_VALIDATION; qubit mismatch -> QBG_ERR_SHAPE. */
 int qbg_time_evolve(qbg_reg* reg, const qbg_obs* h, double t, double tol, int32_t maxdim, int32_t* krylov_dim);
 
+/* ---- one-call forms named in SURVEY §8(b) (thin wrappers over the handle API above) --------- */
+/* apply a flat program once: create (theta: nparams values, may be NULL when none), apply,
+   destroy.  Re-used circuits should keep a qbg_prog (plans and specialised kernels are cached on it). */
+int qbg_run_program(qbg_reg* reg, const qbg_op* ops, int64_t nops, const double* vals, int64_t nvals,
+                    const int64_t* perms, int64_t nperms, const double* theta, int64_t nparams);
+/* <O>_b for a Pauli sum given as terms (one call: create, expect, destroy) */
+int qbg_expect_pauli_sum(const qbg_reg* reg, const qbg_pauli_term* terms, int64_t nterms, double* out);
+/* y += (re + i im) x   (= qbg_add_scaled, register.hpp:130-133) */
+int qbg_axpy(qbg_reg* y, const qbg_reg* x, double re, double im);
+/* = qbg_measure_collapse (register.hpp:470-493) */
+int qbg_collapse(qbg_reg* reg, qbg_rng* rng, uint64_t* out);
+
 /* ---- MMD loss (SPEC.md:446-449 MMDLoss, 497-505 mmd_expect / mmd_grad; §3.2,
    Listing 12 "expect'(mmd, zero_state(5)=>circuit)") -------------------------
    L_b = sum_{x,y} K(x,y) (p_b - q)_x (p_b - q)_y with p_b = |psi_b|^2 over the 2^n basis states

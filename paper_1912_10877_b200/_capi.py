@@ -111,6 +111,9 @@ def lib() -> ctypes.CDLL:
         "qbg_mmd_seed": (c_int32, [P, P, P, P]), "qbg_mmd_cross": (c_int32, [P, P, P, P]),
         "qbg_mmd_grad": (c_int32, [P, P, P, c_int32, P, P, P]),
         "qbg_time_evolve": (c_int32, [P, P, c_double, c_double, c_int32, POINTER(c_int32)]),
+        "qbg_run_program": (c_int32, [P, P, c_int64, P, c_int64, P, c_int64, P, c_int64]),
+        "qbg_expect_pauli_sum": (c_int32, [P, POINTER(QbgPauliTerm), c_int64, P]),
+        "qbg_axpy": (c_int32, [P, P, c_double, c_double]), "qbg_collapse": (c_int32, [P, P, P]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

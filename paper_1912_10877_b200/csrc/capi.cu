@@ -1214,6 +1214,34 @@ int qbg_expect_grad(qbg_reg* r, const qbg_prog* prog, const qbg_obs* o, int32_t 
     });
 }
 
+int qbg_run_program(qbg_reg* reg, const qbg_op* ops, int64_t nops, const double* vals, int64_t nvals,
+                    const int64_t* perms, int64_t nperms, const double* theta, int64_t nparams) {
+    qbg_prog* p = nullptr;
+    int rc = qbg_prog_create(reg ? reg->nactive : 0, ops, nops, vals, nvals, perms, nperms, &p);
+    if (rc) return rc;
+    if (nparams > 0) rc = qbg_prog_set_params(p, theta, nparams);
+    if (!rc) rc = qbg_apply(reg, p);
+    const std::string err = g_err;
+    qbg_prog_destroy(p);
+    if (rc) g_err = err;
+    return rc;
+}
+
+int qbg_expect_pauli_sum(const qbg_reg* reg, const qbg_pauli_term* terms, int64_t nterms, double* out) {
+    qbg_obs* o = nullptr;
+    int rc = qbg_obs_create(reg ? reg->nactive : 0, terms, nterms, &o);
+    if (rc) return rc;
+    rc = qbg_expect(reg, o, out);
+    const std::string err = g_err;
+    qbg_obs_destroy(o);
+    if (rc) g_err = err;
+    return rc;
+}
+
+int qbg_axpy(qbg_reg* y, const qbg_reg* x, double re, double im) { return qbg_add_scaled(y, x, re, im); }
+
+int qbg_collapse(qbg_reg* reg, qbg_rng* rng, uint64_t* out) { return qbg_measure_collapse(reg, rng, out); }
+
 int qbg_mmd_create(int32_t n, const double* target_p, const double* sigmas, int32_t nsigma, qbg_mmd** out) {
     return guarded([&] {
         ensure_device();

@@ -304,3 +304,41 @@ def test_25q_properties(fusion):
     qb.apply(reg, B.dagger(circ))
     p = qb.probabilities(reg, 0)
     assert abs(p[0] - 1) < 1e-10
+
+
+def test_one_call_forms(orc):
+    """SURVEY §8(b) one-call forms: qbg_run_program / qbg_expect_pauli_sum / qbg_axpy / qbg_collapse
+    equal the handle API."""
+    import ctypes
+    from paper_1912_10877_b200._capi import QbgOp, QbgPauliTerm, check, lib
+    n = 12
+    circ = C.variational_circuit(n, 2)
+    B.dispatch(circ, "random")
+    th = np.ascontiguousarray(B.parameters(circ))
+    em = lowered(circ)
+    st = orc.rand_state(n, 2, 8)
+    want = qb.Register(n, 2).set_state(st)
+    qb.apply(want, circ)
+    got = qb.Register(n, 2).set_state(st)
+    ops = (QbgOp * len(em.ops))(*em.ops)
+    vals = np.ascontiguousarray(np.array(em.vals or [0j], dtype=np.complex128))
+    perms = np.ascontiguousarray(np.array(em.perms or [0], dtype=np.int64))
+    check(lib().qbg_run_program(got._h, ops, len(em.ops), vals.ctypes.data, len(em.vals), perms.ctypes.data,
+                                len(em.perms), th.ctypes.data, th.size))
+    assert rel(got.state(), want.state()) < 1e-14
+    h = C.heisenberg(n)
+    terms = B.pauli_terms(h)
+    arr = (QbgPauliTerm * len(terms))(*[QbgPauliTerm(complex(c).real, complex(c).imag, x, z) for c, x, z in terms])
+    e = np.empty(2)
+    check(lib().qbg_expect_pauli_sum(got._h, arr, len(terms), e.ctypes.data))
+    assert relinf(e, qb.expect(h, got)) < 1e-14
+    a = got.copy()
+    check(lib().qbg_axpy(a._h, got._h, 0.5, -0.25))
+    assert rel(a.state(), got.state() * (1.5 - 0.25j)) < 1e-14
+    out1 = np.empty(2, dtype=np.uint64)
+    out2 = np.empty(2, dtype=np.uint64)
+    r1, r2 = got.copy(), got.copy()
+    g1, g2 = qb.Rng(5), qb.Rng(5)  # keep the handles alive across the calls
+    check(lib().qbg_collapse(r1._h, g1._h, out1.ctypes.data))
+    check(lib().qbg_measure_collapse(r2._h, g2._h, out2.ctypes.data))
+    assert np.array_equal(out1, out2) and rel(r1.state(), r2.state()) == 0
