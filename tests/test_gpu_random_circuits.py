@@ -66,7 +66,7 @@ def random_circuit(n, ngates, seed):
     return B.chain(n, *blocks)
 
 
-CASES = [(5, 60, 1, 1), (9, 120, 2, 2), (12, 150, 1, 3), (14, 200, 4, 4), (20, 250, 1, 5)] + \
+CASES = [(5, 60, 1, 1), (9, 120, 2, 2), (12, 150, 1, 3), (14, 200, 4, 4), (20, 250, 1, 5), (22, 160, 1, 6)] + \
     [(n, 120, nb, 10 + s) for s, (n, nb) in enumerate([(12, 1), (13, 2), (14, 1), (15, 3), (16, 1), (16, 8),
                                                       (17, 1), (12, 32), (11, 1), (11, 4), (13, 6)])]
 
