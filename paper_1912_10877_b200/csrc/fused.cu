@@ -86,6 +86,10 @@ int seed_minb() {  // CTAs per SM the seed kernels are compiled for (2: 128 regi
     static const int m = std::max(1, env_int("QBG_SEED_MINB", 2));  // measured: 2 (0.343 vs 0.373 ms)
     return m;
 }
+bool split_acc() {  // two accumulator sets in the Hermitian cross statistics (QBG_SPLIT_ACC)
+    static const bool on = env_int("QBG_SPLIT_ACC", 0) != 0;  // measured slower (registers)
+    return on;
+}
 bool dense_pair() {  // reverse 2x2 uncomputes of ψ and φ̄ interleaved in one template (QBG_DENSE_PAIR)
     static const bool on = env_int("QBG_DENSE_PAIR", 0) != 0;  // measured slower (register pressure)
     return on;
@@ -94,7 +98,11 @@ bool perm_ctrl_regs() {
     static const bool on = env_int("QBG_PERM_CTRL_REGS", 1) != 0;
     return on;
 }
-constexpr int kProducerRegs = 40;
+constexpr int kProducerRegsDefault = 40;
+int producer_regs() {  // registers the producer warpgroup keeps after setmaxnreg.dec (QBG_PRODUCER_REGS)
+    static const int r = std::min(64, std::max(24, env_int("QBG_PRODUCER_REGS", kProducerRegsDefault) / 8 * 8));
+    return r;
+}
 // ring slots that fit next to the gradient cells and barriers (<= 220 KB, 2..6 slots)
 int pipe_slots(bool back, int M, bool c128, int ngrad, int nwt) {
     const size_t tile = (static_cast<size_t>(back ? 2 : 1) << M) * (c128 ? 16 : 8);
@@ -787,7 +795,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         if (back) s << "for (int i = tid_all; i < " << P.ngrad * CS << "; i += " << NG * TH + NP << ") sg[i] = 0.0;\n";
         s << "__syncthreads();\npdl_wait();\n";  // the previous pass's writes are visible after this
         s << "if (tid_all >= " << NG * TH << ") {  // producer warpgroup\n";
-        if (NG > 1 && 65536 / (NG * TH + NP) / 8 * 8 > kProducerRegs) s << "reg_dealloc<" << kProducerRegs << ">();\n";
+        if (NG > 1 && 65536 / (NG * TH + NP) / 8 * 8 > producer_regs()) s << "reg_dealloc<" << producer_regs() << ">();\n";
         s << "const int lane = tid_all - " << NG * TH << ";\n";
         // iteration it: store the results of tile it - nbuf (slot computed), then load tile it
         s << "const u64 nt = (" << P.ntiles << "ull - blockIdx.x + gridDim.x - 1) / gridDim.x;\n";
@@ -832,7 +840,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             // ptxas gives a setmaxnreg kernel the launch-bound register count L per thread; the
             // consumers may grow only into what the producer frees (else TRY_ALLOC never succeeds)
             const int L = 65536 / (NG * TH + NP) / 8 * 8;
-            const int inc = ((NG * TH + NP) * L - NP * kProducerRegs) / (NG * TH) / 8 * 8;
+            const int inc = ((NG * TH + NP) * L - NP * producer_regs()) / (NG * TH) / 8 * 8;
             if (inc > L) s << "reg_alloc<" << std::min(inc, 248) << ">();\n";
         }
         s << "const int cg = tid_all / " << TH << ", tid = tid_all & " << TH - 1 << ";\n";
@@ -1062,7 +1070,8 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                           << ">(x, y, c); if (c[0] + c[1] + c[2] + c[3] == 1.2345) sg[" << op.gslot * CS << " + warp] += 1.0; }\n";
                         break;
                     }
-                    s << "{ double c[4] = {0, 0, 0, 0}; if (" << cond << ") gcrossh<V, R, " << int(op.a)
+                    s << "{ double c[4] = {0, 0, 0, 0}; if (" << cond << ") " << (split_acc() ? "gcrossh2" : "gcrossh1")
+                      << "<V, R, " << int(op.a)
                       << ">(x, y, c); const double v = warp_sum4(c, lane); if ((lane & 7) == 0) sg[(" << op.gslot
                       << " + (lane >> 3)) * " << CS << " + warp] += v; }\n";
                     break;

@@ -167,9 +167,33 @@ __device__ __forceinline__ void gcross1(const V* p, const V* a, double* c) {
 //   Im Σ_ab M_ab C_ab = M00 Im C00 + M11 Im C11 + Re M01 Im(C01 + C10) + Im M01 Re(C01 − C10)
 // c[0] = Im C00, c[1] = Im C11, c[2] = Im(C01 + C10), c[3] = Re(C01 − C10): 12 DFMA per pair.
 template <class V, int R, int K>
-__device__ __forceinline__ void gcrossh(const V* p, const V* a, double* c) {
+__device__ __forceinline__ void gcrossh2(const V* p, const V* a, double* c) {
   // the in-thread sum over the R/2 pairs runs in the element type (complex64: FP32 — 8 terms,
   // far inside its 1e-5 tolerance); the warp and tile reductions that follow are in double
+  typedef typename RT<V>::T T;
+  // two accumulator sets (alternating pairs) halve the dependent FMA chains
+  T c0[2] = {0, 0}, c1[2] = {0, 0}, i01[2] = {0, 0}, i10[2] = {0, 0}, r01[2] = {0, 0}, r10[2] = {0, 0};
+  int h = 0;
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    if (j & (1 << K)) continue;
+    const T a0x = a[j].x, a0y = a[j].y, a1x = a[j | (1 << K)].x, a1y = a[j | (1 << K)].y;
+    const T p0x = p[j].x, p0y = p[j].y, p1x = p[j | (1 << K)].x, p1y = p[j | (1 << K)].y;
+    c0[h] = fma(a0x, p0y, fma(-a0y, p0x, c0[h]));
+    c1[h] = fma(a1x, p1y, fma(-a1y, p1x, c1[h]));
+    i01[h] = fma(a0x, p1y, fma(-a0y, p1x, i01[h]));
+    i10[h] = fma(a1x, p0y, fma(-a1y, p0x, i10[h]));
+    r01[h] = fma(a0x, p1x, fma(a0y, p1y, r01[h]));
+    r10[h] = fma(a1x, p0x, fma(a1y, p0y, r10[h]));
+    h ^= 1;
+  }
+  c[0] += (double)c0[0] + (double)c0[1];
+  c[1] += (double)c1[0] + (double)c1[1];
+  c[2] += ((double)i01[0] + (double)i01[1]) + ((double)i10[0] + (double)i10[1]);
+  c[3] += ((double)r01[0] + (double)r01[1]) - ((double)r10[0] + (double)r10[1]);
+}
+template <class V, int R, int K>
+__device__ __forceinline__ void gcrossh1(const V* p, const V* a, double* c) {
   typedef typename RT<V>::T T;
   T c0 = 0, c1 = 0, i01 = 0, i10 = 0, r01 = 0, r10 = 0;
 #pragma unroll
