@@ -948,6 +948,19 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             }
             const std::string cond = has_ctl ? ctl.str() : "true";
             const std::string t5 = std::to_string(op.creg_mask) + ", " + std::to_string(op.creg_val);
+            // planner invariants the templates rely on (a violation is a planner bug: fail at plan
+            // time, on the host, instead of generating undefined register indexing)
+            {
+                const bool reg_a = op.code == OP_DENSE1 || op.code == OP_X1 || op.code == OP_PERM1 ||
+                                   op.code == OP_DIAG1R || op.code == OP_DENSE2 || op.code == G_DENSE1 ||
+                                   op.code == G_DIAG1R || op.code == G_DENSE2 || op.code == G_CROSS1 ||
+                                   op.code == G_CROSSH || (op.code == G_CROSSD && op.b == LOC_REG);
+                const bool reg_b = op.code == OP_DENSE2 || op.code == G_DENSE2;
+                if ((reg_a && op.a >= RB) || (reg_b && op.b >= RB) || (op.creg_mask >> RB) != 0 ||
+                    (op.cthr_mask >> W) != 0 || ((op.code == OP_DIAG1T || (op.code == G_CROSSD && op.b == LOC_THR)) && op.a >= W))
+                    raise(QBG_ERR_INTERNAL, "fused plan: op " + std::to_string(op.code) + " refers to a register / thread slot "
+                                            "outside the stage layout");
+            }
             auto both = [&](const std::string& call_x, const std::string& call_y) {
                 s << call_x;
                 if (back) s << " " << call_y;
@@ -1283,9 +1296,7 @@ void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128, bool check_
         for (auto& b : bodies) f << b << "\n";
     }
     if (check_only) {
-        std::string src;
-        for (auto& b : bodies) src += b;
-        jit::compile_only(src);
+        jit::compile_only_parallel(bodies);
         return;
     }
     pl.jk = jit::compile_parallel(bodies, names);
@@ -1775,7 +1786,7 @@ void seed_jit_prepare(FusedPlan& pl, bool c128, bool check_only) {
         pl.sblob.push_back(std::move(blob));
     }
     if (check_only)
-        jit::compile_only(src);
+        jit::compile_only_parallel(sbodies);
     else
         pl.jk = jit::compile_parallel(sbodies, names);
 }

@@ -243,6 +243,33 @@ std::vector<Kernel> compile_parallel(const std::vector<std::string>& bodies, con
     return out;
 }
 
+size_t compile_only_parallel(const std::vector<std::string>& bodies) {
+    const size_t nk = bodies.size();
+    if (nk == 0) return 0;
+    unsigned hw = std::thread::hardware_concurrency();
+    const size_t nchunk = std::max<size_t>(1, std::min<size_t>({nk, hw ? hw : 4, 16}));
+    std::vector<std::string> srcs(nchunk);
+    for (size_t i = 0; i < nk; ++i) srcs[i * nchunk / nk] += bodies[i];
+    std::vector<size_t> sizes(nchunk, 0);
+    std::vector<std::string> errs(nchunk);
+    std::vector<std::thread> th;
+    for (size_t c = 0; c < nchunk; ++c)
+        th.emplace_back([&, c] {
+            try {
+                sizes[c] = compile_only(srcs[c]);
+            } catch (const std::exception& e) {
+                errs[c] = e.what();
+            }
+        });
+    for (auto& t : th) t.join();
+    size_t total = 0;
+    for (size_t c = 0; c < nchunk; ++c) {
+        if (!errs[c].empty()) raise(QBG_ERR_INTERNAL, errs[c]);
+        total += sizes[c];
+    }
+    return total;
+}
+
 void launch(Kernel& k, unsigned grid, unsigned block, size_t smem, void** args) {
     if (static_cast<int>(smem) > k.max_dyn_smem) {
         int dev = 0;

@@ -33,6 +33,8 @@ std::vector<Kernel> compile_parallel(const std::vector<std::string>& bodies, con
 
 // NVRTC only (no device): compiles `src` to an sm_100a cubin and returns its size.
 size_t compile_only(const std::string& src);
+// ... one kernel body per entry, compiled in concurrent chunks; total cubin bytes
+size_t compile_only_parallel(const std::vector<std::string>& bodies);
 
 // Enabled unless QBG_JIT=0 or NVRTC cannot be loaded.
 bool enabled();

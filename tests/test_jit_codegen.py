@@ -49,3 +49,20 @@ def test_generic_gates_plan():
     k = ctypes.c_int64()
     check(lib().qbg_jit_check(p._h, None, 1, 0, ctypes.byref(k)))
     assert k.value > 0
+
+
+@pytest.mark.parametrize("n,seed", [(12, 3), (14, 11), (13, 19)])
+def test_random_circuit_kernels_generate_and_compile(n, seed):
+    """Planner invariants (register / thread slots inside the stage layout, checked while the
+    kernels are generated) and NVRTC compilation for random circuits over every gate form —
+    a CPU-side guard for planner bugs such as a run left off the register slots."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from test_gpu_random_circuits import random_circuit
+    c = random_circuit(n, 120, seed)
+    p = qb.compile_block(c)
+    o = qb.compile_observable(qb.heisenberg(n))
+    k = ctypes.c_int64()
+    check(lib().qbg_jit_check(p._h, o._h, 1, 0, ctypes.byref(k)))
+    assert k.value > 0
