@@ -819,11 +819,22 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             return gk;
         };
         if (pstore) {
-            for (int k = 0; k < (1 << M) / NP; ++k) {
-                const uint32_t sk = swz(static_cast<uint32_t>(k * NP));
-                s << "psi[tb + gp + " << kgo(k) << "ll] = buf[sl ^ " << sk << "u];";
-                if (back) s << " adj[tb + gp + " << kgo(k) << "ll] = buf[" << (1 << M) << " + (sl ^ " << sk << "u)];";
-                s << "\n";
+            // drain in batches of QBG_DRAIN_BATCH shared-memory reads, then their stores
+            static const int dbat = std::max(1, env_int("QBG_DRAIN_BATCH", 1));
+            const int per = (1 << M) / NP;
+            for (int k0 = 0; k0 < per; k0 += dbat) {
+                const int k1 = std::min(per, k0 + dbat);
+                for (int k = k0; k < k1; ++k) {
+                    const uint32_t sk = swz(static_cast<uint32_t>(k * NP));
+                    s << "const V d" << k << " = buf[sl ^ " << sk << "u];";
+                    if (back) s << " const V e" << k << " = buf[" << (1 << M) << " + (sl ^ " << sk << "u)];";
+                    s << "\n";
+                }
+                for (int k = k0; k < k1; ++k) {
+                    s << "psi[tb + gp + " << kgo(k) << "ll] = d" << k << ";";
+                    if (back) s << " adj[tb + gp + " << kgo(k) << "ll] = e" << k << ";";
+                    s << "\n";
+                }
             }
             s << "group_bar<" << NP << ">(" << 2 + NG << ");\n";  // slot read out before it is refilled
         }
