@@ -106,6 +106,7 @@ typedef struct qbg_prog qbg_prog; /* compiled gate program (fusion plan + realis
 typedef struct qbg_obs qbg_obs;   /* compiled observable (sum of Pauli terms) */
 typedef struct qbg_rng qbg_rng;   /* host RNG: replaces qblock::Rng (rng.hpp:25-66) */
 typedef struct qbg_mmd qbg_mmd;   /* MMD loss: target distribution + RBF-mixture kernel */
+typedef struct qbg_sparse qbg_sparse; /* full-register sparse operator: the Cached block's matrix */
 
 /* ---- library ------------------------------------------------------------------------- */
 const char* qbg_last_error(void);
@@ -243,6 +244,19 @@ int qbg_expect_grad(qbg_reg* reg, const qbg_prog* prog, const qbg_obs* obs, int3
    column evolves independently.  krylov_dim (may be NULL) receives the largest subspace used.
    Errors: non-hermitian H -> QBG_ERR_VALIDATION; qubit mismatch -> QBG_ERR_SHAPE. */
 int qbg_time_evolve(qbg_reg* reg, const qbg_obs* h, double t, double tol, int32_t maxdim, int32_t* krylov_dim);
+
+/* ---- sparse operators (SPEC.md:397 cache(b); matrix.hpp:680-724 matvec_cols over SparseColumns) ----
+   A is given like the reference's SparseColumns (CSC): colptr[2^n + 1], rows[nnz], vals[2*nnz]
+   (complex interleaved); kept on the device in CSR.  Errors: malformed CSC -> QBG_ERR_VALIDATION /
+   QBG_ERR_RANGE / QBG_ERR_SHAPE. */
+int qbg_sparse_create(int32_t nqubits, int64_t nnz, const int64_t* colptr, const int64_t* rows, const double* vals,
+                      qbg_sparse** out);
+int qbg_sparse_destroy(qbg_sparse* a);
+/* out = A in, every batch column (the register must be relaxed; out != in) */
+int qbg_sparse_apply(const qbg_reg* in, const qbg_sparse* a, qbg_reg* out);
+/* e^{-iAt}|reg> for a hermitian sparse A (Lanczos as qbg_time_evolve); non-hermitian -> QBG_ERR_VALIDATION */
+int qbg_time_evolve_sparse(qbg_reg* reg, const qbg_sparse* a, double t, double tol, int32_t maxdim,
+                           int32_t* krylov_dim);
 
 /* ---- one-call forms named in SURVEY §8(b) (thin wrappers over the handle API above) --------- */
 /* apply a flat program once: create (theta: nparams values, may be NULL when none), apply,

@@ -11,7 +11,7 @@ from .blocks import (CNOT, CZ, SWAP, Add, Block, Chain, Control, Daggered, Gener
                      Toffoli, X, Y, Z, apply, chain, compile_block, compile_observable, control, dagger,
                      define_const_gate, dispatch, gatecount, kron, mat, matblock, nparameters, parameters,
                      pauli_terms, phase, put, repeat, rot, shift, time_evolve, cache, evolve, TimeEvolution,
-                     Cached)
+                     Cached, SparseOperator, sparse_operator, apply_hamiltonian)
 from .circuits import heisenberg, variational_circuit
 from .mmd import MMD, RBFKernel, brbf_kernel, mmd_cross, mmd_expect, mmd_grad, mmd_seed
 from .register import (Register, Rng, instruct, measure, measure_collapse, probabilities, product_state, qubit_cap,

@@ -114,6 +114,9 @@ def lib() -> ctypes.CDLL:
         "qbg_run_program": (c_int32, [P, P, c_int64, P, c_int64, P, c_int64, P, c_int64]),
         "qbg_expect_pauli_sum": (c_int32, [P, POINTER(QbgPauliTerm), c_int64, P]),
         "qbg_axpy": (c_int32, [P, P, c_double, c_double]), "qbg_collapse": (c_int32, [P, P, P]),
+        "qbg_sparse_create": (c_int32, [c_int32, c_int64, P, P, P, POINTER(P)]),
+        "qbg_sparse_destroy": (c_int32, [P]), "qbg_sparse_apply": (c_int32, [P, P, P]),
+        "qbg_time_evolve_sparse": (c_int32, [P, P, c_double, c_double, c_int32, POINTER(c_int32)]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)

@@ -122,7 +122,7 @@ def _expect_grad_segmented(obs: Block, pair, want_state_grad: bool) -> GradResul
     decision): the gate segments run the device reverse pass (qbg_backward); a TimeEvolution
     e^{-iHt} contributes t̄ = 2 Im<φ̄|H|ψ> (taken after it, summed over the batch) and is then
     uncomputed on ψ and φ̄ by e^{+iHt} (two more Krylov applications)."""
-    from .blocks import evolve, parameter_nodes, segments
+    from .blocks import apply_hamiltonian, evolve, parameter_nodes, segments
     reg, circuit = pair
     if circuit.nqubits != reg.nactive or obs.nqubits != reg.nactive:
         raise errors.ShapeError("expect': block qubit count differs from active qubits")
@@ -140,7 +140,7 @@ def _expect_grad_segmented(obs: Block, pair, want_state_grad: bool) -> GradResul
     tmp = None
     for kind, seg in reversed(segs):
         if kind == "te":
-            tmp = obs_apply(seg.hamiltonian, psi, tmp)
+            tmp = apply_hamiltonian(seg.hamiltonian, psi, tmp)
             grads[index[id(seg)]] += 2.0 * float(np.sum(np.imag(adj.inner(tmp))))
             evolve(psi, seg.hamiltonian, -seg.theta)
             evolve(adj, seg.hamiltonian, -seg.theta)

@@ -304,9 +304,19 @@ def matblock(m):
 
 
 def time_evolve(h: Block, t: float) -> TimeEvolution:
-    """time_evolve(h, t): h must be a hermitian Pauli expression."""
-    pauli_terms(h)  # raises UnsupportedError when h is not a Pauli expression
+    """time_evolve(h, t) (SPEC.md:397-405).  A Pauli expression is applied as a device Pauli sum;
+    any other hermitian block through its sparse matrix (the Cached path, built once from mat(h))."""
+    if not is_pauli_expression(h) and (h.nqubits > 16 or isinstance(h, TimeEvolution)):
+        raise errors.UnsupportedError("time_evolve: h must be a Pauli expression or a small (n <= 16) block")
     return TimeEvolution(h, t)
+
+
+def is_pauli_expression(b: Block) -> bool:
+    try:
+        pauli_terms(b)
+        return True
+    except errors.UnsupportedError:
+        return False
 
 
 def cache(b: Block) -> Cached:
@@ -554,6 +564,11 @@ def mat(b: Block) -> np.ndarray:
         return b.factor * mat(b.block)
     if isinstance(b, Daggered):
         return mat(b.block).conj().T
+    if isinstance(b, Cached):
+        return mat(b.block)
+    if isinstance(b, TimeEvolution):
+        import scipy.linalg
+        return scipy.linalg.expm(-1j * b.theta * mat(b.hamiltonian))
     raise errors.UnsupportedError(f"mat: unsupported block {type(b).__name__}")
 
 
@@ -810,11 +825,74 @@ def segments(b: Block) -> list:
 
 
 def evolve(reg, H: Block, t: float, tol: float = 1e-12, maxdim: int = 30) -> int:
-    """|reg> <- e^{-iHt}|reg> on the device (qbg_time_evolve); returns the Krylov dimension used."""
+    """|reg> <- e^{-iHt}|reg> on the device (qbg_time_evolve for a Pauli sum, qbg_time_evolve_sparse
+    otherwise); returns the Krylov dimension used."""
     used = ctypes.c_int32()
-    check(lib().qbg_time_evolve(reg._h, compile_observable(H)._h, float(t), float(tol), int(maxdim),
-                                ctypes.byref(used)))
+    if is_pauli_expression(H):
+        check(lib().qbg_time_evolve(reg._h, compile_observable(H)._h, float(t), float(tol), int(maxdim),
+                                    ctypes.byref(used)))
+    else:
+        check(lib().qbg_time_evolve_sparse(reg._h, sparse_operator(H)._h, float(t), float(tol), int(maxdim),
+                                           ctypes.byref(used)))
     return used.value
+
+
+def apply_hamiltonian(H: Block, reg, out=None):
+    """out = H|reg> (Pauli sum or sparse operator), on the device."""
+    from .register import Register
+    if out is None:
+        out = Register(reg.nqubits, reg.nbatch, dtype=reg.dtype)
+    if is_pauli_expression(H):
+        check(lib().qbg_obs_apply(reg._h, compile_observable(H)._h, out._h))
+    else:
+        check(lib().qbg_sparse_apply(reg._h, sparse_operator(H)._h, out._h))
+    return out
+
+
+class SparseOperator:
+    """A full-register sparse operator on the device (the reference's Cached matrix,
+    SparseColumns + matvec_cols): built from a matrix (dense / scipy.sparse) of dimension 2^n."""
+
+    def __init__(self, m):
+        import scipy.sparse as sp
+        a = sp.csc_matrix(m, dtype=np.complex128)
+        a.sum_duplicates()
+        a.sort_indices()
+        d = a.shape[0]
+        n = int(d).bit_length() - 1
+        if a.shape != (d, d) or d != (1 << n):
+            raise errors.ShapeError("sparse operator: matrix must be 2^n x 2^n")
+        colptr = np.ascontiguousarray(a.indptr, dtype=np.int64)
+        rows = np.ascontiguousarray(a.indices, dtype=np.int64)
+        vals = np.ascontiguousarray(a.data, dtype=np.complex128)
+        h = ctypes.c_void_p()
+        check(lib().qbg_sparse_create(n, a.nnz, colptr.ctypes.data, rows.ctypes.data if a.nnz else None,
+                                      vals.ctypes.data if a.nnz else None, ctypes.byref(h)))
+        self._h, self.nqubits, self.nnz = h, n, a.nnz
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                lib().qbg_sparse_destroy(h)
+            except Exception:
+                pass
+
+    def apply(self, reg, out=None):
+        from .register import Register
+        if out is None:
+            out = Register(reg.nqubits, reg.nbatch, dtype=reg.dtype)
+        check(lib().qbg_sparse_apply(reg._h, self._h, out._h))
+        return out
+
+
+def sparse_operator(b: Block) -> SparseOperator:
+    """The sparse operator of a block, built once from mat(b) and cached on the block."""
+    op = getattr(b, "_qbg_sparse", None)
+    if op is None:
+        op = SparseOperator(mat(b))
+        b._qbg_sparse = op
+    return op
 
 
 # ---------------------------------------------------------------------------------------------------

@@ -10,6 +10,7 @@
 #include <complex>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <numbers>
@@ -1441,7 +1442,9 @@ struct KrylovBuf {
 // of e^{-iH dt} drops below tol (or maxdim vectors); when the full basis does not reach tol for dt,
 // the largest dt' <= dt it does reach is taken instead (no matvec is wasted).  psi advances by the
 // returned time.
-double lanczos_step(const DevState& psi, Observable& H, double dt, double tol, int maxdim, KrylovBuf& kb,
+using MatVec = std::function<void(const DevState& in, const DevState& out)>;
+
+double lanczos_step(const DevState& psi, const MatVec& matvec, double dt, double tol, int maxdim, KrylovBuf& kb,
                     int* used) {
     const int64_t B = psi.B;
     kb.v.reserve(static_cast<size_t>(maxdim) + 2);
@@ -1497,7 +1500,7 @@ double lanczos_step(const DevState& psi, Observable& H, double dt, double tol, i
     double adv = 0.0;
     for (int j = 0; j < maxdim; ++j) {
         const DevState W = vec(0);
-        run_obs(vec(j + 1), W, H, nullptr);
+        matvec(vec(j + 1), W);
         // full re-orthogonalisation, two classical Gram-Schmidt passes (keeps the basis orthonormal
         // to rounding, so the small-matrix exponential is the exact projection)
         if (B == 1) {
@@ -1596,6 +1599,46 @@ double lanczos_step(const DevState& psi, Observable& H, double dt, double tol, i
 
 extern "C" {
 
+}  // extern "C"
+
+namespace qbg {
+namespace {
+// e^{-iHt} on the register by Lanczos steps (the step advances as far as the basis resolves)
+void evolve_driver(qbg_reg* r, const MatVec& matvec, double t, double tol, int32_t maxdim, int32_t* krylov_dim) {
+    if (!std::isfinite(t)) raise(QBG_ERR_VALIDATION, "time_evolve: non-finite time");
+    if (maxdim <= 0) maxdim = 30;
+    maxdim = std::min(maxdim, 60);
+    if (tol <= 0) tol = 1e-12;
+    int used = 0;
+    if (t != 0.0) {
+        static thread_local KrylovBuf kb;
+        kb.fit(r->s);
+        double rem = t;
+        int steps = 0;
+        while (rem != 0.0) {
+            const double adv = lanczos_step(r->s, matvec, rem, tol, maxdim, kb, &used);
+            if (adv == 0.0 || ++steps > 100000) raise(QBG_ERR_INTERNAL, "time_evolve: Krylov iteration made no progress");
+            rem -= adv;
+            if (std::fabs(rem) <= 1e-14 * std::fabs(t)) rem = 0.0;
+        }
+    }
+    if (krylov_dim) *krylov_dim = used;
+    stream_sync();
+}
+}  // namespace
+}  // namespace qbg
+
+struct qbg_sparse {
+    int n = 0;
+    int64_t nnz = 0;
+    int64_t* rowptr = nullptr;  // device CSR
+    int32_t* col = nullptr;
+    double* val = nullptr;  // complex, interleaved
+    bool hermitian = false;
+};
+
+extern "C" {
+
 int qbg_time_evolve(qbg_reg* r, const qbg_obs* h, double t, double tol, int32_t maxdim, int32_t* krylov_dim) {
     return guarded([&] {
         check_reg(r);
@@ -1609,26 +1652,114 @@ int qbg_time_evolve(qbg_reg* r, const qbg_obs* h, double t, double tol, int32_t 
             if (std::fabs(c.imag()) > 1e-12 * std::max(1.0, std::abs(c)))
                 raise(QBG_ERR_VALIDATION, "time_evolve: the Hamiltonian is not hermitian");
         }
-        if (!std::isfinite(t)) raise(QBG_ERR_VALIDATION, "time_evolve: non-finite time");
-        if (maxdim <= 0) maxdim = 30;
-        maxdim = std::min(maxdim, 60);
-        if (tol <= 0) tol = 1e-12;
-        int used = 0;
-        if (t != 0.0 && !H.terms.empty()) {
-            static thread_local KrylovBuf kb;
-            kb.fit(r->s);
-            double rem = t;
-            int steps = 0;
-            while (rem != 0.0) {
-                const double adv = lanczos_step(r->s, H, rem, tol, maxdim, kb, &used);
-                if (adv == 0.0 || ++steps > 100000)
-                    raise(QBG_ERR_INTERNAL, "time_evolve: Krylov iteration made no progress");
-                rem -= adv;
-                if (std::fabs(rem) <= 1e-14 * std::fabs(t)) rem = 0.0;
+        if (H.terms.empty()) {
+            if (krylov_dim) *krylov_dim = 0;
+            return;
+        }
+        evolve_driver(r, [&](const DevState& in, const DevState& out) { run_obs(in, out, H, nullptr); }, t, tol,
+                      maxdim, krylov_dim);
+    });
+}
+
+int qbg_sparse_create(int32_t n, int64_t nnz, const int64_t* colptr, const int64_t* rows, const double* vals,
+                      qbg_sparse** out) {
+    return guarded([&] {
+        ensure_device();
+        if (!out || !colptr || (nnz > 0 && (!rows || !vals))) raise(QBG_ERR_VALIDATION, "sparse: null argument");
+        if (n < 1 || n > g_cap.load()) raise(QBG_ERR_RANGE, "sparse: qubit count out of range");
+        const int64_t d = int64_t{1} << n;
+        if (colptr[0] != 0 || colptr[d] != nnz) raise(QBG_ERR_SHAPE, "sparse: colptr does not span nnz entries");
+        // CSC (the reference's SparseColumns, matrix.hpp) -> CSR for the row-gather kernel
+        std::vector<int64_t> rp(d + 1, 0);
+        for (int64_t c = 0; c < d; ++c) {
+            if (colptr[c + 1] < colptr[c]) raise(QBG_ERR_VALIDATION, "sparse: colptr not monotone");
+            for (int64_t k = colptr[c]; k < colptr[c + 1]; ++k) {
+                if (rows[k] < 0 || rows[k] >= d) raise(QBG_ERR_RANGE, "sparse: row index out of range");
+                rp[rows[k] + 1]++;
             }
         }
-        if (krylov_dim) *krylov_dim = used;
+        for (int64_t r = 0; r < d; ++r) rp[r + 1] += rp[r];
+        std::vector<int32_t> ci(nnz);
+        std::vector<double> cv(2 * nnz);
+        std::vector<int64_t> cur(rp.begin(), rp.end() - 1);
+        std::map<std::pair<int64_t, int64_t>, std::complex<double>> entries;
+        for (int64_t c = 0; c < d; ++c)
+            for (int64_t k = colptr[c]; k < colptr[c + 1]; ++k) {
+                const int64_t at = cur[rows[k]]++;
+                ci[at] = static_cast<int32_t>(c);
+                cv[2 * at] = vals[2 * k];
+                cv[2 * at + 1] = vals[2 * k + 1];
+                entries[{rows[k], c}] += std::complex<double>(vals[2 * k], vals[2 * k + 1]);
+            }
+        bool herm = true;
+        double scale = 0.0;
+        for (auto& [rc, v] : entries) scale = std::max(scale, std::abs(v));
+        for (auto& [rc, v] : entries) {
+            auto it = entries.find({rc.second, rc.first});
+            const std::complex<double> w = it == entries.end() ? 0.0 : it->second;
+            if (std::abs(v - std::conj(w)) > 1e-12 * std::max(1.0, scale)) {
+                herm = false;
+                break;
+            }
+        }
+        auto* m = new qbg_sparse;
+        m->n = n;
+        m->nnz = nnz;
+        m->hermitian = herm;
+        try {
+            m->rowptr = static_cast<int64_t*>(dev_alloc((d + 1) * sizeof(int64_t), false));
+            m->col = static_cast<int32_t*>(dev_alloc(std::max<int64_t>(1, nnz) * sizeof(int32_t), false));
+            m->val = static_cast<double*>(dev_alloc(std::max<int64_t>(1, nnz) * 2 * sizeof(double), false));
+            QBG_CUDA(cudaMemcpyAsync(m->rowptr, rp.data(), (d + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, g_stream));
+            if (nnz) {
+                QBG_CUDA(cudaMemcpyAsync(m->col, ci.data(), nnz * sizeof(int32_t), cudaMemcpyHostToDevice, g_stream));
+                QBG_CUDA(cudaMemcpyAsync(m->val, cv.data(), 2 * nnz * sizeof(double), cudaMemcpyHostToDevice, g_stream));
+            }
+            stream_sync();
+        } catch (...) {
+            if (m->rowptr) cudaFree(m->rowptr);
+            if (m->col) cudaFree(m->col);
+            if (m->val) cudaFree(m->val);
+            delete m;
+            throw;
+        }
+        *out = m;
+    });
+}
+
+int qbg_sparse_destroy(qbg_sparse* m) {
+    return guarded([&] {
+        if (!m) return;
         stream_sync();
+        cudaFree(m->rowptr);
+        cudaFree(m->col);
+        cudaFree(m->val);
+        delete m;
+    });
+}
+
+int qbg_sparse_apply(const qbg_reg* in, const qbg_sparse* m, qbg_reg* out) {
+    return guarded([&] {
+        check_reg(in);
+        if (!m) raise(QBG_ERR_VALIDATION, "sparse: null operator");
+        same_shape(in, out, "sparse apply");
+        if (in == out) raise(QBG_ERR_VALIDATION, "sparse apply: input and output must differ");
+        if (m->n != in->s.n || in->nactive != in->s.n) raise(QBG_ERR_SHAPE, "sparse apply: dimension mismatch");
+        launch_spmv(in->s, out->s, m->rowptr, m->col, m->val, m->nnz);
+        stream_sync();
+    });
+}
+
+int qbg_time_evolve_sparse(qbg_reg* r, const qbg_sparse* m, double t, double tol, int32_t maxdim,
+                           int32_t* krylov_dim) {
+    return guarded([&] {
+        check_reg(r);
+        if (!m) raise(QBG_ERR_VALIDATION, "time_evolve: null operator");
+        if (m->n != r->s.n || r->nactive != r->s.n) raise(QBG_ERR_SHAPE, "time_evolve: dimension mismatch");
+        if (!m->hermitian) raise(QBG_ERR_VALIDATION, "time_evolve: the Hamiltonian is not hermitian");
+        evolve_driver(r, [&](const DevState& in, const DevState& out) {
+            launch_spmv(in, out, m->rowptr, m->col, m->val, m->nnz);
+        }, t, tol, maxdim, krylov_dim);
     });
 }
 

@@ -74,6 +74,10 @@ bool mmd_geometry(uint64_t rows, int64_t B, int D, int* TX, int* BC, size_t* sme
 void multi_inner(const DevState& w, const std::vector<DevState>& vs, double* d_out);
 void multi_axpy(const DevState& w, const std::vector<DevState>& vs, const std::vector<double>& coef);
 
+// ---- sparse operator (sparse.cu): y = A x, A in CSR (complex values interleaved) ----
+void launch_spmv(const DevState& x, const DevState& y, const int64_t* d_rowptr, const int32_t* d_col,
+                 const double* d_val, int64_t nnz);
+
 // scratch device memory owned by the library (grows; stream-ordered reuse)
 void* scratch(size_t bytes, int slot);
 

@@ -116,7 +116,9 @@ def test_time_evolution_blocks_host():
     assert Bk.dagger(te).theta == -0.25
     assert len(Bk.pauli_terms(Bk.cache(h))) == len(Bk.pauli_terms(h))
     import pytest as _pt
+    assert not Bk.is_pauli_expression(Bk.put(n, 1, Bk.H))
+    Bk.time_evolve(Bk.put(n, 1, Bk.H), 0.1)  # non-Pauli: the sparse (Cached) path
     with _pt.raises(Er.UnsupportedError):
-        Bk.time_evolve(Bk.put(n, 1, Bk.H), 0.1)
+        Bk.time_evolve(Bk.put(20, 1, Bk.H), 0.1)  # too large for a materialised matrix
     with _pt.raises(Er.UnsupportedError):
         Bk.segments(Bk.put(n, (1, 2), Bk.time_evolve(Cc.heisenberg(2), 0.1)))

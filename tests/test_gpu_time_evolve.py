@@ -85,6 +85,60 @@ def test_errors():
     with pytest.raises(errors.ValidationError):
         qb.apply(reg, qb.time_evolve(1j * B.put(n, 1, B.X), 0.2))  # non-hermitian
     with pytest.raises(errors.UnsupportedError):
-        qb.time_evolve(B.put(n, 1, B.H), 0.2)  # not a Pauli expression
+        qb.time_evolve(B.put(20, 1, B.H), 0.2)  # not a Pauli expression and too large to materialise
     with pytest.raises(errors.UnsupportedError):
         qb.apply(reg, B.put(n, (1, 2), qb.time_evolve(C.heisenberg(2), 0.1)))
+
+
+def _herm_block(n, seed):
+    """A hermitian non-Pauli Hamiltonian: Σ of random hermitian 2-qubit matrices on random pairs."""
+    rng = np.random.default_rng(seed)
+    terms = []
+    for _ in range(6):
+        a, b = (int(v) for v in rng.choice(np.arange(1, n + 1), 2, replace=False))
+        z = rng.normal(size=(4, 4)) + 1j * rng.normal(size=(4, 4))
+        terms.append(B.put(n, (a, b), B.matblock((z + z.conj().T) / 2)))
+    return qb.Add(terms)
+
+
+@pytest.mark.parametrize("n,nb", [(6, 1), (8, 3)])
+def test_sparse_operator_apply_and_evolve(orc, n, nb):
+    """The Cached / sparse path (matrix.hpp:680-724 matvec_cols): A|ψ> and e^{-iAt}|ψ>
+    for a hermitian non-Pauli block vs dense numpy / expm."""
+    import scipy.linalg
+    h = _herm_block(n, n)
+    A = B.mat(h)
+    st = orc.rand_state(n, nb, 2)
+    reg = qb.Register(n, nb).set_state(st)
+    out = qb.sparse_operator(h).apply(reg)
+    assert rel(out.state(), (A @ st.T).T) < 1e-13
+    qb.apply(reg, qb.time_evolve(qb.cache(h), 0.6))
+    want = (scipy.linalg.expm(-0.6j * A) @ st.T).T
+    assert rel(reg.state(), want) < 1e-11
+
+
+def test_sparse_time_evolution_grad_vs_fd():
+    n = 6
+    h = _herm_block(n, 3)
+    circ = B.chain(n, C.variational_circuit(n, 1), qb.time_evolve(h, 0.45), B.put(n, 2, B.Ry(0.2)))
+    B.dispatch(circ, np.random.default_rng(2).uniform(0, 2 * np.pi, B.nparameters(circ)))
+    obs = C.heisenberg(n)
+    reg = qb.zero_state(n)
+    res = qb.expect_grad(obs, (reg, circ))
+    th = B.parameters(circ)
+    for k in range(th.size):
+        tp, tm = th.copy(), th.copy()
+        tp[k] += 1e-5
+        tm[k] -= 1e-5
+        B.dispatch(circ, tp)
+        ep = qb.expect(obs, (reg, circ))[0]
+        B.dispatch(circ, tm)
+        em = qb.expect(obs, (reg, circ))[0]
+        assert abs((ep - em) / 2e-5 - res.param_grads[k]) < 1e-7, k
+    B.dispatch(circ, th)
+
+
+def test_sparse_errors():
+    n = 4
+    with pytest.raises(errors.ValidationError):  # non-hermitian
+        qb.apply(qb.zero_state(n), qb.time_evolve(B.put(n, 1, B.S), 0.3))
