@@ -90,6 +90,10 @@ bool split_acc() {  // two accumulator sets in the Hermitian cross statistics (Q
     static const bool on = env_int("QBG_SPLIT_ACC", 0) != 0;  // measured slower (registers)
     return on;
 }
+bool jit_check_mode() {
+    static const bool on = env_int("QBG_JIT_CHECK", 0) != 0;
+    return on;
+}
 bool dense_pair() {  // reverse 2x2 uncomputes of ψ and φ̄ interleaved in one template (QBG_DENSE_PAIR)
     static const bool on = env_int("QBG_DENSE_PAIR", 0) != 0;  // measured slower (register pressure)
     return on;
@@ -764,6 +768,14 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
     s << "typedef " << (c128 ? "c128" : "c64") << " V;\nconstexpr int R = " << R << ";\n";
     s << (pipe ? "const int tid_all = threadIdx.x;\n" : "const int tid = threadIdx.x;\n");
     s << "#define MV(i) mk<V>(pm.m[2 * (i)], pm.m[2 * (i) + 1])\n";
+    // index checks (QBG_JIT_CHECK=1: every global / shared tile index is bounds-checked and traps;
+    // the stand-in for memcheck where compute-sanitizer is unavailable)
+    if (jit_check_mode()) {
+        s << "#define GI(e) qchk((i64)(e), " << static_cast<int64_t>(P.ntiles) * (int64_t{1} << M) << "ll)\n";
+        s << "#define SI(e) (unsigned)qchk((i64)(e), " << static_cast<int64_t>(tile_elems) << "ll)\n";
+    } else {
+        s << "#define GI(e) (e)\n#define SI(e) (e)\n";
+    }
     s << "extern __shared__ __align__(128) unsigned char smraw[];\n";
     const size_t cells_off = nbuf * tile_bytes;
     const size_t bar_off = (cells_off + (back ? static_cast<size_t>(P.ngrad) * CS * 8 : 0) + 15) & ~size_t{15};
@@ -826,13 +838,13 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                 const int k1 = std::min(per, k0 + dbat);
                 for (int k = k0; k < k1; ++k) {
                     const uint32_t sk = swz(static_cast<uint32_t>(k * NP));
-                    s << "const V d" << k << " = buf[sl ^ " << sk << "u];";
-                    if (back) s << " const V e" << k << " = buf[" << (1 << M) << " + (sl ^ " << sk << "u)];";
+                    s << "const V d" << k << " = buf[SI(sl ^ " << sk << "u)];";
+                    if (back) s << " const V e" << k << " = buf[SI(" << (1 << M) << " + (sl ^ " << sk << "u))];";
                     s << "\n";
                 }
                 for (int k = k0; k < k1; ++k) {
-                    s << "psi[tb + gp + " << kgo(k) << "ll] = d" << k << ";";
-                    if (back) s << " adj[tb + gp + " << kgo(k) << "ll] = e" << k << ";";
+                    s << "psi[GI(tb + gp + " << kgo(k) << "ll)] = d" << k << ";";
+                    if (back) s << " adj[GI(tb + gp + " << kgo(k) << "ll)] = e" << k << ";";
                     s << "\n";
                 }
             }
@@ -841,8 +853,8 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         s << "}\n";
         s << "if (it < nt) {\nu64 outer; i64 tb; tile_geo(blockIdx.x + it * gridDim.x, outer, tb);\n";
         for (int k = 0; k < (1 << M) / NP; ++k) {
-            s << "cpa(buf + lane + " << k * NP << ", psi + tb + gp + " << kgo(k) << "ll);";
-            if (back) s << " cpa(buf + " << (1 << M) << " + lane + " << k * NP << ", adj + tb + gp + " << kgo(k) << "ll);";
+            s << "cpa(buf + SI(lane + " << k * NP << "), psi + GI(tb + gp + " << kgo(k) << "ll));";
+            if (back) s << " cpa(buf + SI(" << (1 << M) << " + lane + " << k * NP << "), adj + GI(tb + gp + " << kgo(k) << "ll));";
             s << "\n";
         }
         s << "cp_arrive_noinc(full + slot);\n}\n";
@@ -902,8 +914,8 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                 s << "x[" << j << "] = mk<V>((double)(tid + " << j << ") * 1e-3, (double)tile * 1e-9);";
                 if (back) s << " y[" << j << "] = mk<V>((double)(tid - " << j << ") * 1e-3, 1e-9);";
             } else {
-                s << "x[" << j << "] = psi[tb + g0 + " << goff(S0, j) << "ll];";
-                if (back) s << " y[" << j << "] = adj[tb + g0 + " << goff(S0, j) << "ll];";
+                s << "x[" << j << "] = psi[GI(tb + g0 + " << goff(S0, j) << "ll)];";
+                if (back) s << " y[" << j << "] = adj[GI(tb + g0 + " << goff(S0, j) << "ll)];";
             }
             s << "\n";
         }
@@ -919,8 +931,8 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                 s << "x[" << j << "] = mk<V>((double)(tid + " << j << ") * 1e-3, (double)tile * 1e-9);";
                 if (back) s << " y[" << j << "] = mk<V>((double)(tid - " << j << ") * 1e-3, 1e-9);";
             } else {
-                s << "x[" << j << "] = sx[lin0 | " << loff(S0, j) << "u];";
-                if (back) s << " y[" << j << "] = sy[lin0 | " << loff(S0, j) << "u];";
+                s << "x[" << j << "] = sx[SI(lin0 | " << loff(S0, j) << "u)];";
+                if (back) s << " y[" << j << "] = sy[SI(lin0 | " << loff(S0, j) << "u)];";
             }
             s << "\n";
         }
@@ -931,14 +943,14 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         if (st > 0 && exp_mode != 4 && exp_mode != 6) {  // (QBG_EXP=4/6, diagnostics: no transposes)
             const DStage& Sp = P.st[st - 1];
             for (int j = 0; j < R; ++j) {
-                s << "sx[st" << st - 1 << " ^ " << soff(Sp, j) << "u] = x[" << j << "];";
-                if (back) s << " sy[st" << st - 1 << " ^ " << soff(Sp, j) << "u] = y[" << j << "];";
+                s << "sx[SI(st" << st - 1 << " ^ " << soff(Sp, j) << "u)] = x[" << j << "];";
+                if (back) s << " sy[SI(st" << st - 1 << " ^ " << soff(Sp, j) << "u)] = y[" << j << "];";
                 s << "\n";
             }
             s << SYNC;
             for (int j = 0; j < R; ++j) {
-                s << "x[" << j << "] = sx[st" << st << " ^ " << soff(S, j) << "u];";
-                if (back) s << " y[" << j << "] = sy[st" << st << " ^ " << soff(S, j) << "u];";
+                s << "x[" << j << "] = sx[SI(st" << st << " ^ " << soff(S, j) << "u)];";
+                if (back) s << " y[" << j << "] = sy[SI(st" << st << " ^ " << soff(S, j) << "u)];";
                 s << "\n";
             }
             s << SYNC;
@@ -1130,16 +1142,16 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         const int ls = P.nstages - 1;
         if (P.nstages == 1) s << SYNC;  // other threads may still read stage 0 from the slot
         for (int j = 0; j < R; ++j) {
-            s << "sx[st" << ls << " ^ " << soff(SL, j) << "u] = x[" << j << "];";
-            if (back) s << " sy[st" << ls << " ^ " << soff(SL, j) << "u] = y[" << j << "];";
+            s << "sx[SI(st" << ls << " ^ " << soff(SL, j) << "u)] = x[" << j << "];";
+            if (back) s << " sy[SI(st" << ls << " ^ " << soff(SL, j) << "u)] = y[" << j << "];";
             s << "\n";
         }
         s << SYNC << "if (tid == 0) mbar_arrive(done + slot);\n";
     } else {
         if (exp_mode == 1 || exp_mode == 5 || exp_mode == 6) s << "if (outer == ~0ull) {\n";
         for (int j = 0; j < R; ++j) {
-            s << "psi[tb + gL + " << goff(SL, j) << "ll] = x[" << j << "];";
-            if (back) s << " adj[tb + gL + " << goff(SL, j) << "ll] = y[" << j << "];";
+            s << "psi[GI(tb + gL + " << goff(SL, j) << "ll)] = x[" << j << "];";
+            if (back) s << " adj[GI(tb + gL + " << goff(SL, j) << "ll)] = y[" << j << "];";
             s << "\n";
         }
         if (exp_mode == 1 || exp_mode == 5 || exp_mode == 6) s << "}\n";
@@ -1155,7 +1167,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
           << ") { double a = 0.0; for (int w = 0; w < " << NWT << "; ++w) a += sg[sl * " << CS
           << " + w]; gpart[(i64)(gbase + sl) * gcols + blockIdx.x] = a; }\n";
     }
-    s << "#undef MV\n}\n";
+    s << "#undef MV\n#undef GI\n#undef SI\n}\n";
     return s.str();
 }
 

@@ -269,6 +269,11 @@ __device__ __forceinline__ void cp_arrive_noinc(unsigned long long* b) {
 }
 template <int NT>
 __device__ __forceinline__ void named_bar() { asm volatile("bar.sync 1, %0;\n" :: "n"(NT) : "memory"); }
+// bounds check of a generated index (QBG_JIT_CHECK builds): trap instead of reading / writing out of range
+__device__ __forceinline__ long long qchk(long long i, long long n) {
+  if ((unsigned long long)i >= (unsigned long long)n) __trap();
+  return i;
+}
 // shared-memory swizzle of a tile-local element index (same as the host planner's swz)
 __device__ __forceinline__ unsigned swz(unsigned l) { return l ^ (((l >> 3) ^ (l >> 6) ^ (l >> 9) ^ (l >> 12) ^ (l >> 15)) & 7u); }
 // programmatic dependent launch: block until the preceding grid in the stream has completed and
