@@ -740,6 +740,76 @@ std::string tid_sum(const W* w, int nbits, bool xr) {
     return s.str();
 }
 
+// ---- TMA tile loads (QBG_TMA=1): the tile as a <= 5-D box of the state -------------------------
+bool tma_enabled() {
+    static const bool on = env_int("QBG_TMA", 0) != 0;
+    return on;
+}
+struct TmaDim {
+    uint64_t size;    // in FP64 units for dim 0, elements otherwise... (see tma_layout)
+    uint64_t stride;  // bytes (ignored for dim 0)
+    uint32_t box;
+    int coord;        // 0: zero; 1: the batch chunk c; 2: (outer >> shift) & mask
+    int shift;
+    uint64_t mask;
+};
+// The element index splits into runs of bits that are all in the tile (box = run) or all outside
+// (box 1, coordinate from the tile's outer index).  FP64 data type; the (re, im) pair folds into
+// the innermost run when it is in the tile and contiguous, else it is its own dimension.
+bool tma_layout(const DPass& P, int M, bool c128, std::vector<TmaDim>& dims) {
+    dims.clear();
+    if (!c128) return false;
+    int n = P.mq;
+    for (uint64_t t = P.ntiles / static_cast<uint64_t>(P.nchunks); t > 1; t >>= 1) ++n;
+    uint64_t Q = 0;
+    for (int k = 0; k < P.mq; ++k) Q |= uint64_t{1} << P.qpos[k];
+    struct Run { uint64_t elems_w; int len; bool in; int coord; int shift; };
+    std::vector<Run> runs;
+    if (P.B > 1) {
+        if (P.nb > 0) runs.push_back({1, P.nb, true, 0, 0});
+        if (P.nchunks > 1) runs.push_back({uint64_t{1} << P.nb, -static_cast<int>(P.nchunks), false, 1, 0});
+    }
+    for (int q = 0; q < n;) {
+        const bool in = (Q >> q) & 1;
+        int e = q;
+        while (e < n && (((Q >> e) & 1) != 0) == in) ++e;
+        runs.push_back({static_cast<uint64_t>(P.B) << q, e - q, in, in ? 0 : 2, q});
+        q = e;
+    }
+    bool folded = false;
+    for (size_t i = 0; i < runs.size(); ++i) {
+        const Run& r = runs[i];
+        const uint64_t size = r.len < 0 ? static_cast<uint64_t>(-r.len) : (uint64_t{1} << r.len);
+        if (r.in) {  // split into pieces of <= 8 bits (box limit 256; 7 bits when it carries (re, im))
+            int done = 0;
+            while (done < r.len) {
+                const bool first = dims.empty() && r.elems_w == 1 && done == 0;
+                const int piece = std::min(r.len - done, first ? 7 : 8);
+                TmaDim d{};
+                d.size = (uint64_t{1} << piece) * (first ? 2 : 1);
+                d.stride = (r.elems_w << done) * 16;
+                d.box = static_cast<uint32_t>(d.size);
+                d.coord = 0;
+                if (first) folded = true;
+                dims.push_back(d);
+                done += piece;
+            }
+        } else {
+            if (dims.empty()) dims.push_back({2, 8, 2, 0, 0, 0});  // (re, im) on its own
+            TmaDim d{};
+            d.size = size;
+            d.stride = r.elems_w * 16;
+            d.box = 1;
+            d.coord = r.coord;
+            d.shift = r.shift;
+            d.mask = size - 1;
+            dims.push_back(d);
+        }
+    }
+    (void)folded;
+    return dims.size() <= 5;
+}
+
 std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, bool back, bool c128) {
     const int R = 1 << RB, W = M - RB, TH = 1 << W, NW = TH / 32;
     const size_t elem = c128 ? 16 : 8;
@@ -760,11 +830,14 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
     const std::string SYNC = pipe ? "group_bar<" + std::to_string(TH) + ">(1 + cg);\n" : "__syncthreads();\n";
     std::ostringstream s;
     const int NP = pipe ? producer_threads(back) : 0;
+    std::vector<TmaDim> td;
+    const bool use_tma = pipe && tma_enabled() && tma_layout(P, M, c128, td);
     s << "extern \"C\" __global__ void __launch_bounds__(" << NG * TH + NP << ", "
       << (pipe ? 1 : ctas_per_sm(back, TH)) << ") __NAME__(" << (c128 ? "c128" : "c64") << "* __restrict__ psi, "
       << (c128 ? "c128" : "c64")
       << "* __restrict__ adj, double* __restrict__ gpart, long long gcols, int gbase, const __grid_constant__ PM<"
-      << (c128 ? "double" : "float") << ", " << std::max(2, 2 * nmats) << "> pm) {\n";
+      << (c128 ? "double" : "float") << ", " << std::max(2, 2 * nmats)
+      << "> pm, const __grid_constant__ TMap tmp, const __grid_constant__ TMap tma) {\n";
     s << "typedef " << (c128 ? "c128" : "c64") << " V;\nconstexpr int R = " << R << ";\n";
     s << (pipe ? "const int tid_all = threadIdx.x;\n" : "const int tid = threadIdx.x;\n");
     s << "#define MV(i) mk<V>(pm.m[2 * (i)], pm.m[2 * (i) + 1])\n";
@@ -799,10 +872,12 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         s << "outer = ((outer >> " << p << ") << " << p + 1 << ") | (outer & " << hex((uint64_t{1} << p) - 1) << ");\n";
     }
     s << "tb = (i64)outer * " << P.B << "ll + (i64)c * " << (int64_t{1} << P.nb) << "ll;\n};\n";
+    s << "auto c_of = [&](u64 tile) -> u64 { return " << (P.nchunks == 1 ? std::string("0ull") : "tile % " + std::to_string(P.nchunks) + "ull")
+      << "; };\n";
     if (pipe) {
         int64_t gw[32];
         for (int b = 0; b < M; ++b) gw[b] = b < P.nb ? (int64_t{1} << b) : (P.B << P.qpos[b - P.nb]);
-        s << "if (tid_all == 0) { for (int i = 0; i < " << nbuf << "; ++i) { mbar_init(full + i, " << NP
+        s << "if (tid_all == 0) { for (int i = 0; i < " << nbuf << "; ++i) { mbar_init(full + i, " << (use_tma ? 1 : NP)
           << "); mbar_init(done + i, 1); } }\n";
         if (back) s << "for (int i = tid_all; i < " << P.ngrad * CS << "; i += " << NG * TH + NP << ") sg[i] = 0.0;\n";
         s << "__syncthreads();\npdl_wait();\n";  // the previous pass's writes are visible after this
@@ -848,16 +923,33 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                     s << "\n";
                 }
             }
+            if (use_tma) s << "fence_proxy_async();\n";
             s << "group_bar<" << NP << ">(" << 2 + NG << ");\n";  // slot read out before it is refilled
         }
         s << "}\n";
         s << "if (it < nt) {\nu64 outer; i64 tb; tile_geo(blockIdx.x + it * gridDim.x, outer, tb);\n";
-        for (int k = 0; k < (1 << M) / NP; ++k) {
-            s << "cpa(buf + SI(lane + " << k * NP << "), psi + GI(tb + gp + " << kgo(k) << "ll));";
-            if (back) s << " cpa(buf + SI(" << (1 << M) << " + lane + " << k * NP << "), adj + GI(tb + gp + " << kgo(k) << "ll));";
-            s << "\n";
+        if (use_tma) {
+            // one thread: expect the tile's bytes, then one (two) bulk tensor copies
+            s << "if (lane == 0) {\nmbar_arrive_tx(full + slot, " << tile_bytes << "u);\n";
+            std::ostringstream co;
+            for (size_t d = 0; d < td.size(); ++d) {
+                if (td[d].coord == 0) co << "0";
+                else if (td[d].coord == 1) co << "(int)c_of(blockIdx.x + it * gridDim.x)";
+                else co << "(int)((outer >> " << td[d].shift << ") & " << td[d].mask << "ull)";
+                if (d + 1 < td.size()) co << ", ";
+            }
+            s << "tma_load" << td.size() << "(buf, &tmp, full + slot, " << co.str() << ");\n";
+            if (back) s << "tma_load" << td.size() << "(buf + " << (1 << M) << ", &tma, full + slot, " << co.str() << ");\n";
+            s << "}\n}\n";
         }
-        s << "cp_arrive_noinc(full + slot);\n}\n";
+        if (!use_tma) {
+            for (int k = 0; k < (1 << M) / NP; ++k) {
+                s << "cpa(buf + SI(lane + " << k * NP << "), psi + GI(tb + gp + " << kgo(k) << "ll));";
+                if (back) s << " cpa(buf + SI(" << (1 << M) << " + lane + " << k * NP << "), adj + GI(tb + gp + " << kgo(k) << "ll));";
+                s << "\n";
+            }
+            s << "cp_arrive_noinc(full + slot);\n}\n";
+        }
         s << "}\nreturn;\n}\n";
         if (NG > 1) {
             // ptxas gives a setmaxnreg kernel the launch-bound register count L per thread; the
@@ -1146,6 +1238,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             if (back) s << " sy[SI(st" << ls << " ^ " << soff(SL, j) << "u)] = y[" << j << "];";
             s << "\n";
         }
+        if (use_tma) s << "fence_proxy_async();\n";
         s << SYNC << "if (tid == 0) mbar_arrive(done + slot);\n";
     } else {
         if (exp_mode == 1 || exp_mode == 5 || exp_mode == 6) s << "if (outer == ~0ull) {\n";
@@ -1155,7 +1248,10 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             s << "\n";
         }
         if (exp_mode == 1 || exp_mode == 5 || exp_mode == 6) s << "}\n";
-        if (pipe) s << SYNC << "if (tid == 0) mbar_arrive(done + slot);\n";
+        if (pipe) {
+            if (use_tma) s << "fence_proxy_async();\n";
+            s << SYNC << "if (tid == 0) mbar_arrive(done + slot);\n";
+        }
     }
     s << "}\n";  // tile loop
     if (back) {
@@ -1340,7 +1436,22 @@ void launch_jit(V* psi, V* adj, Step& st, FusedPlan& pl, double* gpart, int64_t 
     if (BACK) grid = std::min<int64_t>(grid, gcols);
     double bytes = static_cast<double>(P.ntiles) * (int64_t{1} << pl.M) * sizeof(V) * (BACK ? 4.0 : 2.0);
     int gbase = P.grad_base;
-    void* args[] = {&psi, &adj, &gpart, &gcols, &gbase, st.blob.data()};
+    alignas(64) unsigned char tmp[128] = {0}, tma[128] = {0};
+    if (pipe && tma_enabled()) {
+        std::vector<TmaDim> td;
+        if (tma_layout(P, pl.M, sizeof(V) == 16, td)) {
+            uint64_t sz[5], st[5];
+            uint32_t bx[5];
+            for (size_t d = 0; d < td.size(); ++d) {
+                sz[d] = td[d].size;
+                st[d] = td[d].stride;
+                bx[d] = td[d].box;
+            }
+            jit::encode_tensor_map(tmp, psi, static_cast<int>(td.size()), sz, st, bx);
+            if (BACK) jit::encode_tensor_map(tma, adj, static_cast<int>(td.size()), sz, st, bx);
+        }
+    }
+    void* args[] = {&psi, &adj, &gpart, &gcols, &gbase, st.blob.data(), tmp, tma};
     LaunchScope ls(BACK ? "fused_bwd" : "fused_fwd", bytes, st.flops);
     jit::launch(pl.jk[st.jk], static_cast<unsigned>(grid), pipe ? consumer_groups() * T + producer_threads(BACK) : T, st.smem,
                 args);

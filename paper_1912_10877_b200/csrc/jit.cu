@@ -1,6 +1,8 @@
 // jit.cu — NVRTC compile + cudaLibrary load + caches for the specialised tile kernels.
 #include "jit.h"
 
+#include <cuda.h>
+
 #include <dlfcn.h>
 #include <sys/stat.h>
 #include <unistd.h>
@@ -268,6 +270,34 @@ size_t compile_only_parallel(const std::vector<std::string>& bodies) {
         total += sizes[c];
     }
     return total;
+}
+
+void encode_tensor_map(void* map, const void* gaddr, int rank, const uint64_t* sizes, const uint64_t* strides,
+                       const uint32_t* box) {
+    typedef CUresult (*Encode)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Encode fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<Encode>(f);
+    }();
+    if (!fn) raise(QBG_ERR_INTERNAL, "tma: cuTensorMapEncodeTiled is not available");
+    cuuint64_t dims[5], str[5];
+    cuuint32_t bx[5], es[5];
+    for (int d = 0; d < rank; ++d) {
+        dims[d] = sizes[d];
+        bx[d] = box[d];
+        es[d] = 1;
+        if (d > 0) str[d - 1] = strides[d];
+    }
+    CUresult r = fn(static_cast<CUtensorMap*>(map), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, static_cast<cuuint32_t>(rank),
+                    const_cast<void*>(gaddr), dims, str, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) raise(QBG_ERR_INTERNAL, "tma: cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
 }
 
 void launch(Kernel& k, unsigned grid, unsigned block, size_t smem, void** args) {

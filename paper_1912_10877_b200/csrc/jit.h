@@ -39,6 +39,12 @@ size_t compile_only_parallel(const std::vector<std::string>& bodies);
 // Enabled unless QBG_JIT=0 or NVRTC cannot be loaded.
 bool enabled();
 
+// A 128-byte CUtensorMap for an FP64 tensor of `rank` dims: sizes[d] (d = 0 innermost), byte
+// strides[d] for d >= 1, box[d]; no swizzle / interleave (cuTensorMapEncodeTiled via the driver
+// entry point, so libqbg.so does not link libcuda directly).
+void encode_tensor_map(void* map, const void* gaddr, int rank, const uint64_t* sizes, const uint64_t* strides,
+                       const uint32_t* box);
+
 // Launch a JIT kernel with `args` (pointers to each argument) on the library stream.
 void launch(Kernel& k, unsigned grid, unsigned block, size_t smem, void** args);
 

@@ -269,6 +269,29 @@ __device__ __forceinline__ void cp_arrive_noinc(unsigned long long* b) {
 }
 template <int NT>
 __device__ __forceinline__ void named_bar() { asm volatile("bar.sync 1, %0;\n" :: "n"(NT) : "memory"); }
+// tensor-memory-access (TMA) tile loads: one elected thread copies the tile box into the slot and
+// the transfer completes the slot's mbarrier (the map is a __grid_constant__ kernel parameter)
+struct __align__(64) TMap { unsigned long long w[16]; };
+__device__ __forceinline__ void tma_load1(void* dst, const TMap* m, unsigned long long* bar, int c0) {
+  asm volatile("cp.async.bulk.tensor.1d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];\n"
+               :: "r"(smem_u32(dst)), "l"(m), "r"(c0), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_load2(void* dst, const TMap* m, unsigned long long* bar, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n"
+               :: "r"(smem_u32(dst)), "l"(m), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_load3(void* dst, const TMap* m, unsigned long long* bar, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n"
+               :: "r"(smem_u32(dst)), "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_load4(void* dst, const TMap* m, unsigned long long* bar, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n"
+               :: "r"(smem_u32(dst)), "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_load5(void* dst, const TMap* m, unsigned long long* bar, int c0, int c1, int c2, int c3, int c4) {
+  asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n"
+               :: "r"(smem_u32(dst)), "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar)) : "memory");
+}
 // bounds check of a generated index (QBG_JIT_CHECK builds): trap instead of reading / writing out of range
 __device__ __forceinline__ long long qchk(long long i, long long n) {
   if ((unsigned long long)i >= (unsigned long long)n) __trap();
