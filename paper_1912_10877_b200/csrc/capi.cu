@@ -18,6 +18,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "engine.h"
 #include "program.h"
 
@@ -380,7 +382,14 @@ void realise(Program& p) {
 
 namespace {
 
+// NVTX ranges around the engine's phases (visible to ncu --nvtx / nsys; no cost without a tool)
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+};
+
 void run_program(const DevState& s, Program& p, bool adjoint) {
+    Nvtx r(adjoint ? "qbg.apply_adjoint" : "qbg.apply");
     if (!p.realised) realise(p);
     if (g_fusion && fused_forward(s, p, adjoint)) return;
     size_t N = p.real.size();
@@ -391,6 +400,7 @@ void run_program(const DevState& s, Program& p, bool adjoint) {
 }
 
 void run_obs(const DevState& psi, const DevState& phi, Observable& o, double* d_energy) {
+    Nvtx r("qbg.observable");
     if (g_fusion && fused_obs_apply(psi, phi, o, d_energy)) return;
     if (o.terms.empty()) {
         QBG_CUDA(cudaMemsetAsync(phi.ptr, 0, phi.bytes(), g_stream));
@@ -409,6 +419,7 @@ void run_obs(const DevState& psi, const DevState& phi, Observable& o, double* d_
 
 // reverse pass; d_grads (device, nparams) receives the accumulated gradient
 void run_backward(const DevState& psi, const DevState& adj, Program& p, double* d_grads) {
+    Nvtx r("qbg.backward");
     if (!p.realised) realise(p);
     if (g_fusion && fused_backward(psi, adj, p, d_grads)) return;
     size_t N = p.real.size();
