@@ -1455,6 +1455,23 @@ void launch_jit(V* psi, V* adj, Step& st, FusedPlan& pl, double* gpart, int64_t 
     LaunchScope ls(BACK ? "fused_bwd" : "fused_fwd", bytes, st.flops);
     jit::launch(pl.jk[st.jk], static_cast<unsigned>(grid), pipe ? consumer_groups() * T + producer_threads(BACK) : T, st.smem,
                 args);
+    static const bool sync_each = env_int("QBG_SYNC_EACH", 0) != 0;  // diagnostics: localise a failing pass
+    if (sync_each) {
+        cudaError_t e = cudaStreamSynchronize(stream());
+        if (e != cudaSuccess) {
+            std::ostringstream m;
+            m << "pass failed (" << (BACK ? "reverse" : "forward") << ", tile Q=";
+            for (int k = 0; k < P.mq; ++k) m << (k ? "," : "") << int(P.qpos[k]);
+            m << ", stages " << P.nstages << ", ops " << P.nops << ", ntiles " << P.ntiles << ", grid " << grid
+              << ", smem " << st.smem << "): " << cudaGetErrorString(e);
+            std::vector<TmaDim> td;
+            if (tma_enabled() && tma_layout(P, pl.M, sizeof(V) == 16, td)) {
+                m << "; tma rank " << td.size() << ":";
+                for (auto& d : td) m << " [" << d.size << " x" << d.stride << "B box " << d.box << " c" << d.coord << "]";
+            }
+            raise(QBG_ERR_CUDA, m.str());
+        }
+    }
 }
 
 int batch_bits(int64_t B) {
