@@ -111,7 +111,8 @@ int producer_regs() {  // registers the producer warpgroup keeps after setmaxnre
 int pipe_slots(bool back, int M, bool c128, int ngrad, int nwt) {
     const size_t tile = (static_cast<size_t>(back ? 2 : 1) << M) * (c128 ? 16 : 8);
     const size_t cells = back ? static_cast<size_t>(ngrad) * (nwt + 1) * 8 : 0;
-    int n = 6;
+    static const int cap_b = env_int("QBG_BWD_SLOTS", 6), cap_f = env_int("QBG_FWD_SLOTS", 6);
+    int n = std::max(2, back ? cap_b : cap_f);
     while (n > 2 && n * tile + cells + 128 > 220 * 1024) --n;
     return n;
 }
@@ -740,9 +741,10 @@ std::string tid_sum(const W* w, int nbits, bool xr) {
     return s.str();
 }
 
-// ---- TMA tile loads (QBG_TMA=1): the tile as a <= 5-D box of the state -------------------------
-bool tma_enabled() {
-    static const bool on = env_int("QBG_TMA", 0) != 0;
+// ---- TMA tile loads (default; QBG_TMA=0 disables): the tile as a <= 5-D box of the state -------
+// (passes whose layout needs more than 5 dimensions keep the cp.async producer)
+bool tma_enabled() {  // default on; QBG_TMA=0 selects the cp.async producer
+    static const bool on = env_int("QBG_TMA", 1) != 0;
     return on;
 }
 struct TmaDim {
@@ -1015,6 +1017,11 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         s << "for (u64 it = cg;; it += " << NG << ") {\n";
         s << "const u64 tile = blockIdx.x + it * gridDim.x;\nif (tile >= " << P.ntiles << "ull) break;\n";
         s << "const unsigned slot = (unsigned)(it % " << nbuf << "), use = (unsigned)(it / " << nbuf << ");\n";
+        // A slot alternates between the two consumer groups (nbuf odd): the previous use of this slot
+        // belongs to the other group, whose fill may still be in flight when this group gets here.
+        // A parity wait two phases ahead would pass at once, so first wait until that previous use
+        // has been released (done[slot] phase use-1); then the full-phase parity is unambiguous.
+        if (NG > 1 && nbuf % NG != 0) s << "if (use > 0) mbar_wait(done + slot, (use - 1u) & 1u);\n";
         s << "mbar_wait(full + slot, use & 1u);\n";
         s << "V* sx = ring + (size_t)slot * " << tile_elems << "u; V* sy = sx + " << (1 << M) << ";\n";
         s << "u64 outer; i64 tb; tile_geo(tile, outer, tb);\n";

@@ -14,8 +14,9 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("env", [{"QBG_PIPE": "0"}, {"QBG_PIPE": "1"}, {"QBG_JIT": "0"}, {"QBG_JIT_CHECK": "1"}],
-                         ids=["plain-jit", "one-group", "interpreter", "bounds-checked"])
+@pytest.mark.parametrize("env", [{"QBG_PIPE": "0"}, {"QBG_PIPE": "1"}, {"QBG_JIT": "0"}, {"QBG_JIT_CHECK": "1"},
+                                 {"QBG_TMA": "0"}],
+                         ids=["plain-jit", "one-group", "interpreter", "bounds-checked", "cp-async-producer"])
 def test_mode_parity(env):
     e = dict(os.environ, **env)
     r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
@@ -23,3 +24,16 @@ def test_mode_parity(env):
                         "vs_oracle or goldens or c64 or triangle"],
                        env=e, cwd=ROOT, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("tma", ["1", "0"])
+def test_fast_consumers_slot_protocol(tma):
+    """Regression for the slot hand-over race: with the gate ops removed (QBG_EXP=2) the consumer
+    groups outrun the producer, which exposed a group waiting on a slot whose previous fill (the
+    other group's tile) was still in flight.  Must run to completion (values are not meaningful)."""
+    code = ("import sys; sys.path.insert(0, '.'); import paper_1912_10877_b200 as qb; "
+            "c = qb.variational_circuit(25, 2); qb.dispatch(c, 'random'); "
+            "r = qb.expect_grad(qb.heisenberg(25), (qb.zero_state(25), c)); qb.synchronize(); print('ok')")
+    e = dict(os.environ, QBG_EXP="2", QBG_TMA=tma)
+    r = subprocess.run([sys.executable, "-c", code], env=e, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
