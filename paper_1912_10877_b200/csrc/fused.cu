@@ -743,6 +743,10 @@ std::string tid_sum(const W* w, int nbits, bool xr) {
 
 // ---- TMA tile loads (default; QBG_TMA=0 disables): the tile as a <= 5-D box of the state -------
 // (passes whose layout needs more than 5 dimensions keep the cp.async producer)
+bool tma_store_enabled() {  // forward drain by one TMA tensor store per tile (QBG_TMA_STORE)
+    static const bool on = env_int("QBG_TMA_STORE", 1) != 0;
+    return on;
+}
 bool tma_enabled() {  // default on; QBG_TMA=0 selects the cp.async producer
     static const bool on = env_int("QBG_TMA", 1) != 0;
     return on;
@@ -834,6 +838,17 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
     const int NP = pipe ? producer_threads(back) : 0;
     std::vector<TmaDim> td;
     const bool use_tma = pipe && tma_enabled() && tma_layout(P, M, c128, td);
+    const bool tstore = use_tma && !back && tma_store_enabled();  // (decided with pstore below)
+    auto tma_coords = [&](const std::string& outer, const std::string& tile) {
+        std::ostringstream co;
+        for (size_t d = 0; d < td.size(); ++d) {
+            if (td[d].coord == 0) co << "0";
+            else if (td[d].coord == 1) co << "(int)c_of(" << tile << ")";
+            else co << "(int)((" << outer << " >> " << td[d].shift << ") & " << td[d].mask << "ull)";
+            if (d + 1 < td.size()) co << ", ";
+        }
+        return co.str();
+    };
     s << "extern \"C\" __global__ void __launch_bounds__(" << NG * TH + NP << ", "
       << (pipe ? 1 : ctas_per_sm(back, TH)) << ") __NAME__(" << (c128 ? "c128" : "c64") << "* __restrict__ psi, "
       << (c128 ? "c128" : "c64")
@@ -907,7 +922,13 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                 if (((static_cast<int64_t>(k) * NP) >> b) & 1) gk += gw[b];
             return gk;
         };
-        if (pstore) {
+        if (pstore && tstore) {
+            // one elected thread: the computed tile (linear layout) back as one TMA tensor store, and
+            // its shared-memory reads retired before the slot is refilled
+            s << "if (lane == 0) {\nconst u64 ptile = blockIdx.x + (it - " << nbuf << ") * gridDim.x;\n";
+            s << "tma_store" << td.size() << "(&tmp, buf, " << tma_coords("outer", "ptile") << ");\n";
+            s << "tma_commit();\ntma_wait_read0();\n}\n";
+        } else if (pstore) {
             // drain in batches of QBG_DRAIN_BATCH shared-memory reads, then their stores
             static const int dbat = std::max(1, env_int("QBG_DRAIN_BATCH", 1));
             const int per = (1 << M) / NP;
@@ -933,15 +954,9 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         if (use_tma) {
             // one thread: expect the tile's bytes, then one (two) bulk tensor copies
             s << "if (lane == 0) {\nmbar_arrive_tx(full + slot, " << tile_bytes << "u);\n";
-            std::ostringstream co;
-            for (size_t d = 0; d < td.size(); ++d) {
-                if (td[d].coord == 0) co << "0";
-                else if (td[d].coord == 1) co << "(int)c_of(blockIdx.x + it * gridDim.x)";
-                else co << "(int)((outer >> " << td[d].shift << ") & " << td[d].mask << "ull)";
-                if (d + 1 < td.size()) co << ", ";
-            }
-            s << "tma_load" << td.size() << "(buf, &tmp, full + slot, " << co.str() << ");\n";
-            if (back) s << "tma_load" << td.size() << "(buf + " << (1 << M) << ", &tma, full + slot, " << co.str() << ");\n";
+            const std::string co = tma_coords("outer", "(blockIdx.x + it * gridDim.x)");
+            s << "tma_load" << td.size() << "(buf, &tmp, full + slot, " << co << ");\n";
+            if (back) s << "tma_load" << td.size() << "(buf + " << (1 << M) << ", &tma, full + slot, " << co << ");\n";
             s << "}\n}\n";
         }
         if (!use_tma) {
@@ -952,7 +967,8 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             }
             s << "cp_arrive_noinc(full + slot);\n}\n";
         }
-        s << "}\nreturn;\n}\n";
+        if (tstore) s << "}\nif (lane == 0) tma_wait0();\nreturn;\n}\n";
+        else s << "}\nreturn;\n}\n";
         if (NG > 1) {
             // ptxas gives a setmaxnreg kernel the launch-bound register count L per thread; the
             // consumers may grow only into what the producer frees (else TRY_ALLOC never succeeds)
@@ -1240,10 +1256,18 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         // them to global memory while this group computes its next tile
         const int ls = P.nstages - 1;
         if (P.nstages == 1) s << SYNC;  // other threads may still read stage 0 from the slot
-        for (int j = 0; j < R; ++j) {
-            s << "sx[SI(st" << ls << " ^ " << soff(SL, j) << "u)] = x[" << j << "];";
-            if (back) s << " sy[SI(st" << ls << " ^ " << soff(SL, j) << "u)] = y[" << j << "];";
-            s << "\n";
+        if (tstore) {  // linear layout (the TMA box order); the last stage's thread bits hold the low qubits
+            uint32_t lwl[kMaxW];
+            for (int p = 0; p < W; ++p) lwl[p] = 1u << SL.lthr[p];
+            s << "{ const unsigned linL = " << tid_sum(lwl, W, true) << ";\n";
+            for (int j = 0; j < R; ++j) s << "sx[SI(linL | " << loff(SL, j) << "u)] = x[" << j << "];\n";
+            s << "}\n";
+        } else {
+            for (int j = 0; j < R; ++j) {
+                s << "sx[SI(st" << ls << " ^ " << soff(SL, j) << "u)] = x[" << j << "];";
+                if (back) s << " sy[SI(st" << ls << " ^ " << soff(SL, j) << "u)] = y[" << j << "];";
+                s << "\n";
+            }
         }
         if (use_tma) s << "fence_proxy_async();\n";
         s << SYNC << "if (tid == 0) mbar_arrive(done + slot);\n";
