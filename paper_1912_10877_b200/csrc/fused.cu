@@ -838,7 +838,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
     const int NP = pipe ? producer_threads(back) : 0;
     std::vector<TmaDim> td;
     const bool use_tma = pipe && tma_enabled() && tma_layout(P, M, c128, td);
-    const bool tstore = use_tma && !back && tma_store_enabled();  // (decided with pstore below)
+    const bool tstore = use_tma && tma_store_enabled();  // (used where the producer drains: pstore)
     auto tma_coords = [&](const std::string& outer, const std::string& tile) {
         std::ostringstream co;
         for (size_t d = 0; d < td.size(); ++d) {
@@ -927,6 +927,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             // its shared-memory reads retired before the slot is refilled
             s << "if (lane == 0) {\nconst u64 ptile = blockIdx.x + (it - " << nbuf << ") * gridDim.x;\n";
             s << "tma_store" << td.size() << "(&tmp, buf, " << tma_coords("outer", "ptile") << ");\n";
+            if (back) s << "tma_store" << td.size() << "(&tma, buf + " << (1 << M) << ", " << tma_coords("outer", "ptile") << ");\n";
             s << "tma_commit();\ntma_wait_read0();\n}\n";
         } else if (pstore) {
             // drain in batches of QBG_DRAIN_BATCH shared-memory reads, then their stores
@@ -1260,7 +1261,11 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             uint32_t lwl[kMaxW];
             for (int p = 0; p < W; ++p) lwl[p] = 1u << SL.lthr[p];
             s << "{ const unsigned linL = " << tid_sum(lwl, W, true) << ";\n";
-            for (int j = 0; j < R; ++j) s << "sx[SI(linL | " << loff(SL, j) << "u)] = x[" << j << "];\n";
+            for (int j = 0; j < R; ++j) {
+                s << "sx[SI(linL | " << loff(SL, j) << "u)] = x[" << j << "];";
+                if (back) s << " sy[SI(linL | " << loff(SL, j) << "u)] = y[" << j << "];";
+                s << "\n";
+            }
             s << "}\n";
         } else {
             for (int j = 0; j < R; ++j) {
