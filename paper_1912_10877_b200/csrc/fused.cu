@@ -14,6 +14,13 @@
 // with W_k the product of the run's gates after k (derivation in DESIGN.md §AD).  Gradients
 // are reduced per warp into shared cells, per CTA into a partials buffer, then in a fixed
 // order: deterministic for a given grid.
+//
+// Execution (gen_pass, default): one persistent CTA per SM, warp-specialised.  A producer
+// warpgroup streams tiles into a ring of shared-memory slots — one TMA tensor box per tile
+// (cp.async fallback for layouts beyond 5 dimensions) completing the slot's `full` mbarrier —
+// and, in the forward pass, drains computed slots back with one TMA tensor store.  Two consumer
+// groups take alternate tiles; a slot's previous use may belong to the other group, so a group
+// waits for that release (`done`) before the fill's parity wait.
 // See fused.h for the tile/stage vocabulary and DESIGN.md for the roofline numbers.
 #include <algorithm>
 #include <cmath>
