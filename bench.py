@@ -67,16 +67,33 @@ class Clocks:
         self.idx = vis.split(",")[local_rank] if vis else str(local_rank)
         self.proc = None
         self.path = None
+        self.skip = 0
 
     def start(self):
+        """Start sampling every 20 ms and return once the sampler has produced its first line, so
+        the timed region that follows is covered from its first step."""
         try:
             fd, self.path = tempfile.mkstemp(suffix=".csv")
             os.close(fd)
+            import shutil
+            pre = ["stdbuf", "-oL"] if shutil.which("stdbuf") else []  # line-buffered into the file
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", self.idx, f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                pre + ["nvidia-smi", "-i", self.idx, f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "20"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            t0 = time.perf_counter()
+            while time.perf_counter() - t0 < 10.0 and self.proc.poll() is None:
+                if os.path.getsize(self.path) > 0:
+                    break
+                time.sleep(0.01)
         except Exception:
             self.proc = None
+
+    def mark(self):
+        """Line count at the start of the timed region: samples before it are not reported."""
+        if self.proc is None:
+            return
+        with open(self.path) as f:
+            self.skip = sum(1 for _ in f)
 
     def stop(self):
         if self.proc is None:
@@ -88,7 +105,9 @@ class Clocks:
             self.proc.kill()
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
+        for i, line in enumerate(open(self.path)):
+            if i < self.skip:
+                continue
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 8:
                 continue
@@ -240,6 +259,8 @@ def main():
     barrier()
     torch.cuda.synchronize()
     clocks.start()
+    torch.cuda.synchronize()
+    clocks.mark()
     L.qbg_launch_count_reset()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
