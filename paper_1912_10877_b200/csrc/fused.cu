@@ -105,6 +105,14 @@ bool dense_pair() {  // reverse 2x2 uncomputes of ψ and φ̄ interleaved in one
     static const bool on = env_int("QBG_DENSE_PAIR", 0) != 0;  // measured slower (register pressure)
     return on;
 }
+// Statistic stores without a lane branch (QBG_SG_BRANCHFREE, default on): after the butterfly
+// reductions every lane of a group holds the bitwise-identical sum (commutative adds), so all of
+// them may store it — same address, same value.  Dropping the `if (lane ...)` keeps a stage one
+// basic block, so ptxas can overlap a run's shuffle chain with the next run's FP64 work.
+bool sg_branchfree() {
+    static const bool on = env_int("QBG_SG_BRANCHFREE", 1) != 0;
+    return on;
+}
 bool perm_ctrl_regs() {
     static const bool on = env_int("QBG_PERM_CTRL_REGS", 1) != 0;
     return on;
@@ -1200,13 +1208,13 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                         }
                     }
                     s << " }";
-                    if (grad) s << " g = warp_sum(g); if (lane == 0) sg[" << op.gslot * CS << " + warp] += g;";
+                    if (grad) s << " g = warp_sum(g); " << (sg_branchfree() ? "" : "if (lane == 0) ") << "sg[" << op.gslot * CS << " + warp] += g;";
                     s << " }\n";
                     break;
                 }
                 case G_CROSS1: {
                     s << "{ double c[8] = {0, 0, 0, 0, 0, 0, 0, 0}; if (" << cond << ") gcross1<V, R, " << int(op.a)
-                      << ">(x, y, c); const double v = warp_sum8(c, lane); if ((lane & 3) == 0) sg[(" << op.gslot
+                      << ">(x, y, c); const double v = warp_sum8(c, lane); " << (sg_branchfree() ? "" : "if ((lane & 3) == 0) ") << "sg[(" << op.gslot
                       << " + (lane >> 2)) * " << CS << " + warp] += v; }\n";
                     break;
                 }
@@ -1219,7 +1227,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                     else
                         call = "gcrossd_u<V, R>(x, y, c, (int)((outer >> " + std::to_string(op.a) + ") & 1ull));";
                     s << "{ double c[4] = {0, 0, 0, 0}; if (" << cond << ") " << call
-                      << " const double v = warp_sum4(c, lane); if ((lane & 7) == 0) sg[(" << op.gslot
+                      << " const double v = warp_sum4(c, lane); " << (sg_branchfree() ? "" : "if ((lane & 7) == 0) ") << "sg[(" << op.gslot
                       << " + (lane >> 3)) * " << CS << " + warp] += v; }\n";
                     break;
                 }
@@ -1231,7 +1239,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                     }
                     s << "{ double c[4] = {0, 0, 0, 0}; if (" << cond << ") " << (split_acc() ? "gcrossh2" : "gcrossh1")
                       << "<V, R, " << int(op.a)
-                      << ">(x, y, c); const double v = warp_sum4(c, lane); if ((lane & 7) == 0) sg[(" << op.gslot
+                      << ">(x, y, c); const double v = warp_sum4(c, lane); " << (sg_branchfree() ? "" : "if ((lane & 7) == 0) ") << "sg[(" << op.gslot
                       << " + (lane >> 3)) * " << CS << " + warp] += v; }\n";
                     break;
                 }
@@ -1251,7 +1259,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                     else
                         s << "const V m[16] = {" << mvs(o, 16) << "}; g = gdense2<V, R, " << int(op.a) << ", " << int(op.b)
                           << ", " << t5 << ">(x, y, m);";
-                    s << " } g = warp_sum(g); if (lane == 0) sg[" << op.gslot * CS << " + warp] += g; }\n";
+                    s << " } g = warp_sum(g); " << (sg_branchfree() ? "" : "if (lane == 0) ") << "sg[" << op.gslot * CS << " + warp] += g; }\n";
                     break;
                 }
                 default:
