@@ -113,6 +113,12 @@ bool sg_branchfree() {
     static const bool on = env_int("QBG_SG_BRANCHFREE", 1) != 0;
     return on;
 }
+// Thread- / tile-controlled register swaps (CNOT with a thread-bit control) by selects instead
+// of a branch (QBG_CSWAP_SEL=1; measured slower: reverse pass 0.615 -> 0.645 ms, so off)
+bool cswap_sel() {
+    static const bool on = env_int("QBG_CSWAP_SEL", 0) != 0;
+    return on;
+}
 bool perm_ctrl_regs() {
     static const bool on = env_int("QBG_PERM_CTRL_REGS", 1) != 0;
     return on;
@@ -1138,6 +1144,12 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                 }
                 case OP_X1: {
                     std::string tp = "<V, R, " + std::to_string(op.a) + ", " + t5 + ">";
+                    if (has_ctl && cswap_sel()) {
+                        s << "{ const bool p = " << cond << "; ";
+                        both("cswap1" + tp + "(x, p);", "cswap1" + tp + "(y, p);");
+                        s << " }\n";
+                        break;
+                    }
                     s << "if (" << cond << ") { ";
                     both("swap1" + tp + "(x);", "swap1" + tp + "(y);");
                     s << " }\n";

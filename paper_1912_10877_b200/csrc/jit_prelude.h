@@ -57,6 +57,18 @@ __device__ __forceinline__ void swap1(V* x) {
     V a = x[j]; x[j] = x[j | (1 << K)]; x[j | (1 << K)] = a;
   }
 }
+// swap1 under a per-thread predicate, by selects instead of a branch (keeps the stage one basic block)
+template <class V, int R, int K, int CM, int CV>
+__device__ __forceinline__ void cswap1(V* x, bool p) {
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    if (j & (1 << K)) continue;
+    if ((j & CM) != CV) continue;
+    const V a = x[j], b = x[j | (1 << K)];
+    x[j].x = p ? b.x : a.x; x[j].y = p ? b.y : a.y;
+    x[j | (1 << K)].x = p ? a.x : b.x; x[j | (1 << K)].y = p ? a.y : b.y;
+  }
+}
 template <class V, int R, int K, int CM, int CV>
 __device__ __forceinline__ void diag1(V* x, V d0, V d1) {
 #pragma unroll
