@@ -199,10 +199,11 @@ __device__ __forceinline__ void gcrossh2(const V* p, const V* a, double* c) {
     r10[h] = fma(a1x, p0x, fma(a1y, p0y, r10[h]));
     h ^= 1;
   }
-  c[0] += (double)c0[0] + (double)c0[1];
-  c[1] += (double)c1[0] + (double)c1[1];
-  c[2] += ((double)i01[0] + (double)i01[1]) + ((double)i10[0] + (double)i10[1]);
-  c[3] += ((double)r01[0] + (double)r01[1]) - ((double)r10[0] + (double)r10[1]);
+  // assigned, not accumulated: every caller hands in a fresh c (0 + s costs a DADD, -0 rules)
+  c[0] = (double)c0[0] + (double)c0[1];
+  c[1] = (double)c1[0] + (double)c1[1];
+  c[2] = ((double)i01[0] + (double)i01[1]) + ((double)i10[0] + (double)i10[1]);
+  c[3] = ((double)r01[0] + (double)r01[1]) - ((double)r10[0] + (double)r10[1]);
 }
 template <class V, int R, int K>
 __device__ __forceinline__ void gcrossh1(const V* p, const V* a, double* c) {
@@ -220,10 +221,10 @@ __device__ __forceinline__ void gcrossh1(const V* p, const V* a, double* c) {
     r01 = fma(a0x, p1x, fma(a0y, p1y, r01));
     r10 = fma(a1x, p0x, fma(a1y, p0y, r10));
   }
-  c[0] += (double)c0;
-  c[1] += (double)c1;
-  c[2] += (double)i01 + (double)i10;
-  c[3] += (double)r01 - (double)r10;
+  c[0] = (double)c0;  // assigned: every caller hands in a fresh c
+  c[1] = (double)c1;
+  c[2] = (double)i01 + (double)i10;
+  c[3] = (double)r01 - (double)r10;
 }
 // diagonal run: c[b] += Σ Im(conj(a) p) over the elements whose run bit is b — register slot K
 template <class V, int R, int K>
