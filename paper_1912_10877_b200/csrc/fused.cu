@@ -78,10 +78,13 @@ bool pipeline_enabled() {
     static const bool on = jit::enabled() && env_int("QBG_PIPE", 2) > 0;
     return on;
 }
-int consumer_groups() {
+int consumer_groups(bool back) {
     // (4 groups of 64 threads with 2^10 tiles measured slower per gate; 2 is the design point)
+    // QBG_FWD_GROUPS / QBG_BWD_GROUPS (1..4) override per direction
     static const int g = std::min(2, std::max(1, env_int("QBG_PIPE", 2)));
-    return g;
+    static const int f = std::min(4, std::max(1, env_int("QBG_FWD_GROUPS", g)));
+    static const int b = std::min(4, std::max(1, env_int("QBG_BWD_GROUPS", g)));
+    return back ? b : f;
 }
 constexpr int kProducerThreads = 128;
 // producer threads of a pass (one warpgroup; QBG_FWD_PRODUCERS=256 gives the forward passes two)
@@ -843,7 +846,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
     // pipe mode (warp-specialised, see pipeline_enabled): NG consumer groups of TH threads take
     // alternate tiles from a ring of nbuf shared-memory slots filled by a cp.async producer warpgroup
     const bool pipe = pipeline_enabled();
-    const int NG = pipe ? consumer_groups() : 1;
+    const int NG = pipe ? consumer_groups(back) : 1;
     const int NWT = NG * NW;  // consumer warps
     const int CS = NWT + 1;   // gradient cell stride (odd: the lanes of a warp_sum hit distinct banks)
     const int nbuf = pipe ? pipe_slots(back, M, c128, P.ngrad, NWT) : 1;
@@ -1421,7 +1424,7 @@ void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128, bool check_
             }
         }
         const size_t tile_bytes = (back ? 2 : 1) * (elem << M);
-        const int nwt = (pipeline_enabled() ? consumer_groups() : 1) * NW;
+        const int nwt = (pipeline_enabled() ? consumer_groups(back) : 1) * NW;
         const size_t cells = back ? static_cast<size_t>(P.ngrad) * (nwt + 1) * 8 : 0;
         if (pipeline_enabled()) {
             const int nbuf = pipe_slots(back, M, c128, P.ngrad, nwt);
@@ -1516,7 +1519,7 @@ void launch_jit(V* psi, V* adj, Step& st, FusedPlan& pl, double* gpart, int64_t 
     }
     void* args[] = {&psi, &adj, &gpart, &gcols, &gbase, st.blob.data(), tmp, tma};
     LaunchScope ls(BACK ? "fused_bwd" : "fused_fwd", bytes, st.flops);
-    jit::launch(pl.jk[st.jk], static_cast<unsigned>(grid), pipe ? consumer_groups() * T + producer_threads(BACK) : T, st.smem,
+    jit::launch(pl.jk[st.jk], static_cast<unsigned>(grid), pipe ? consumer_groups(BACK) * T + producer_threads(BACK) : T, st.smem,
                 args);
     static const bool sync_each = env_int("QBG_SYNC_EACH", 0) != 0;  // diagnostics: localise a failing pass
     if (sync_each) {
