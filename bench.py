@@ -38,6 +38,8 @@ def parse():
     ap.add_argument("--qubits", type=int, default=25)
     ap.add_argument("--depth", type=int, default=10)
     ap.add_argument("--no-fusion", action="store_true")
+    ap.add_argument("--dtype", default="c128", choices=["c128", "c64"],
+                    help="register precision (the metric is quoted in c128; c64 is reported beside it)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU sample for cpu_baseline")
     return ap.parse_args()
@@ -199,11 +201,13 @@ def per_gate_roofline(top, per_launch_ms, G, S, peak):
 def workload_config(args):
     n, d = args.qubits, args.depth
     G, P, T = n * (1 + 4 * d), n * (1 + 3 * d), 3 * (n - 1)
+    cplx = "complex128" if args.dtype == "c128" else "complex64"
     return {"workload": f"expect'(heisenberg({n}) open, zero_state({n}) => variational_circuit({n},{d})) "
-                        "apply+grad, complex128",
+                        f"apply+grad, {cplx}",
             "qubits": n, "depth": d, "gates_fwd": G, "gates_per_step": 2 * G, "params": P, "terms": T,
-            "batch": 1, "state_bytes": 16 << n,
-            "l2": f"state {16 << n >> 20} MiB > 126 MB L2: inputs larger than L2, no flush",
+            "batch": 1, "state_bytes": (16 if args.dtype == "c128" else 8) << n,
+            "l2": f"state {(16 if args.dtype == 'c128' else 8) << n >> 20} MiB > 126 MB L2: inputs larger than L2, "
+                  "no flush",
             "parallelism": f"replicas x{args.gpus}"}
 
 
@@ -238,8 +242,8 @@ def main():
     qb.dispatch(circ, "random", rng=qb.Rng(42 + rank))
     h = qb.heisenberg(n)
     G, T = n * (1 + 4 * d), 3 * (n - 1)
-    S = 16 << n
-    reg = qb.zero_state(n)
+    S = (16 if args.dtype == "c128" else 8) << n
+    reg = qb.zero_state(n, dtype=args.dtype)
     prog = qb.compile_block(circ)
     qb.compile_observable(h)
 
@@ -303,12 +307,15 @@ def main():
            "path": "dispatch(θ from pinned host) + zero_state + expect' + energies/grads to host, per step"}
 
     # variant: input state uploaded from pinned host memory every step (qbg_upload)
-    host_state = torch.zeros(2 << n, dtype=torch.float64).pin_memory()
+    host_state = torch.zeros(2 << n, dtype=torch.float64 if args.dtype == "c128" else torch.float32).pin_memory()
     host_state[0] = 1.0
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(max(1, args.steps // 2)):
-        check(L.qbg_upload(reg._h, host_state.data_ptr(), 1 << n))
+        if args.dtype == "c128":
+            check(L.qbg_upload(reg._h, host_state.data_ptr(), 1 << n))
+        else:  # the device's own element type, no host-side conversion
+            check(L.qbg_upload_raw(reg._h, host_state.data_ptr(), S))
         r3 = step()
     torch.cuda.synchronize()
     e2e_state_ms = (time.perf_counter() - t0) * 1e3 / max(1, args.steps // 2)
@@ -339,7 +346,7 @@ def main():
         achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tp):
+        if os.path.exists(tp) and args.dtype == "c128":  # the committed capture is of the c128 metric run
             try:
                 traffic = json.load(open(tp)).get(top["name"])
             except Exception:
@@ -349,7 +356,7 @@ def main():
                     "traffic": traffic, "kernel": top["name"], "launches_per_step": top["launches"] / 2,
                     "bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms, "share_of_step": share,
                     "peak_source": peak_src,
-                    "fp64": fp64_roofline(top, per_launch_ms),
+                    "fp64": fp64_roofline(top, per_launch_ms) if args.dtype == "c128" else None,
                     "per_gate_convention": per_gate_roofline(top, per_launch_ms, G, S, peak),
                     "kernels": [{k2: (round(v, 6) if isinstance(v, float) else v) for k2, v in kk.items()}
                                 for kk in kernels[:8]]}
@@ -373,7 +380,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "c128", "data": "synthetic (zero_state, θ ~ U(0,2π) from Rng(42+rank))",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (zero_state, θ ~ U(0,2π) from Rng(42+rank))",
             "config": workload_config(args),
             "hbm_gbs_algorithmic": hbm_alg, "hbm_frac_algorithmic": hbm_alg / peak,
             "energy": float(res.energies[0]),
