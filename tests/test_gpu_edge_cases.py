@@ -1,0 +1,106 @@
+"""Edge cases of the device engine vs the CPU oracle, through the C-ABI: the smallest registers
+(1-2 qubits, below the 3 coalescing qubits of a tile), an empty circuit, registers at and around
+the tile sizes (2^10 / 2^11 / 2^12 elements) where the planner switches between the per-gate
+and the tiled passes, wide batches of tiny states, and run-to-run determinism of the gradient
+reductions (fixed reduction order).  Tolerances as in test_gpu_parity.py."""
+import numpy as np
+import pytest
+
+import paper_1912_10877_b200 as qb
+from paper_1912_10877_b200 import blocks as B
+from paper_1912_10877_b200 import circuits as C
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def relinf(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    if a.size == 0 and b.size == 0:
+        return 0.0
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-300)
+
+
+def lowered(block):
+    nodes = B.parameter_nodes(block)
+    em = B._Emitter({id(p): k for k, p in enumerate(nodes)})
+    B._lower(block, tuple(range(1, block.nqubits + 1)), (), (), em)
+    return em
+
+
+@pytest.fixture(params=[True, False], ids=["fused", "pergate"])
+def fusion(request):
+    qb.set_fusion(request.param)
+    yield request.param
+    qb.set_fusion(True)
+
+
+def check_expect_grad(orc, n, circ, obs, nb, seed=5):
+    st = orc.rand_state(n, nb, seed)
+    e, g, _, sg = orc.expect_grad(st, n, lowered(circ), B.parameters(circ), B.pauli_terms(obs))
+    reg = qb.Register(n, nb).set_state(st)
+    res = qb.expect_grad(obs, (reg, circ), want_state_grad=True)
+    assert relinf(res.energies, e) < TOL
+    assert relinf(res.param_grads, g) < TOL
+    assert rel(res.state_grad.state(), sg) < TOL
+    return res
+
+
+@pytest.mark.parametrize("nb", [1, 3])
+def test_one_qubit_register(orc, fusion, nb):
+    circ = B.chain(B.put(1, 1, B.Rx(0.3)), B.put(1, 1, B.Rz(0.7)), B.put(1, 1, B.Ry(-1.1)),
+                   B.put(1, 1, B.shift(0.4)), B.put(1, 1, B.H))
+    check_expect_grad(orc, 1, circ, B.put(1, 1, B.Z), nb)
+    check_expect_grad(orc, 1, circ, B.Add([B.put(1, 1, B.X), B.Scale(0.5, B.put(1, 1, B.Y))]), nb)
+
+
+@pytest.mark.parametrize("nb", [1, 2])
+def test_two_qubit_register(orc, fusion, nb):
+    circ = C.variational_circuit(2, 3)
+    B.dispatch(circ, np.random.default_rng(2).uniform(0, 2 * np.pi, B.nparameters(circ)))
+    check_expect_grad(orc, 2, circ, C.heisenberg(2), nb)
+
+
+def test_empty_circuit(orc, fusion):
+    n = 5
+    circ = B.chain(n)
+    assert B.nparameters(circ) == 0
+    reg = qb.Register(n, 2).set_state(orc.rand_state(n, 2, 1))
+    before = reg.state()
+    qb.apply(reg, circ)
+    assert np.array_equal(reg.state(), before)  # identity, bit for bit
+    res = check_expect_grad(orc, n, circ, C.heisenberg(n), 2, seed=1)
+    assert res.param_grads.shape == (0,)
+
+
+@pytest.mark.parametrize("n", [10, 11, 12])
+def test_tile_boundary_sizes(orc, fusion, n):
+    circ = C.variational_circuit(n, 1)
+    B.dispatch(circ, np.random.default_rng(n).uniform(0, 2 * np.pi, B.nparameters(circ)))
+    check_expect_grad(orc, n, circ, C.heisenberg(n), 1, seed=n)
+
+
+def test_wide_batch_of_tiny_states(orc, fusion):
+    n, nb = 3, 64
+    circ = C.variational_circuit(n, 2)
+    B.dispatch(circ, np.random.default_rng(9).uniform(0, 2 * np.pi, B.nparameters(circ)))
+    check_expect_grad(orc, n, circ, C.heisenberg(n, periodic=True), nb, seed=9)
+
+
+def test_gradients_are_deterministic():
+    """Same inputs, same grid: the two-level gradient reductions run in a fixed order, so repeated
+    runs agree bit for bit (no atomics on the gradient path)."""
+    n = 16
+    circ = C.variational_circuit(n, 2)
+    B.dispatch(circ, np.random.default_rng(4).uniform(0, 2 * np.pi, B.nparameters(circ)))
+    h = C.heisenberg(n)
+    runs = [qb.expect_grad(h, (qb.zero_state(n), circ)) for _ in range(3)]
+    for r in runs[1:]:
+        assert np.array_equal(r.energies, runs[0].energies)
+        assert np.array_equal(r.param_grads, runs[0].param_grads)
