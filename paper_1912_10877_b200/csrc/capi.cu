@@ -380,6 +380,71 @@ void realise(Program& p) {
     p.realised = true;
 }
 
+// A new parameter vector on an already realised program: only the parameterised ops change, and
+// only their matrix values (kind, placement and generator stay), so they are rewritten in place —
+// the same arithmetic as realise(), without its per-op allocations (dispatch → apply is on the
+// end-to-end path of every optimiser step).
+void realise_params(Program& p) {
+    const cd I(0.0, 1.0);
+    for (size_t k = 0; k < p.ops.size(); ++k) {
+        const qbg_op& op = p.ops[k];
+        if (op.gen == QBG_GEN_NONE) continue;
+        RealOp& ro = p.real[k];
+        const int dim = op.dim;
+        const cdbl* src = p.vals.data() + op.data;
+        const double th = p.theta[op.param];
+        std::vector<cdbl>& u = ro.u.m;
+        if (op.gen == QBG_GEN_ROTATION) {
+            const double c = std::cos(th / 2), s = std::sin(th / 2);
+            if (op.kind == QBG_MAT_IDENTITY || op.kind == QBG_MAT_DIAGONAL) {
+                for (int r = 0; r < dim; ++r) {
+                    const cd g = op.kind == QBG_MAT_IDENTITY ? cd(1.0) : cd(src[r].re, src[r].im);
+                    const cd d = cd(c) - I * cd(s) * g;
+                    u[r] = cdbl{d.real(), d.imag()};
+                }
+            } else {
+                const cd f = -I * s;
+                for (auto& e : u) e = cdbl{0.0, 0.0};
+                if (op.kind == QBG_MAT_PERMUTATION) {
+                    for (int r = 0; r < dim; ++r) {
+                        const size_t at = static_cast<size_t>(p.perms[op.perm + r]) * dim + r;
+                        cd e(u[at].re, u[at].im);
+                        e += cd(src[r].re, src[r].im);
+                        u[at] = cdbl{e.real(), e.imag()};
+                    }
+                } else {
+                    for (int r = 0; r < dim * dim; ++r) u[r] = src[r];
+                }
+                for (auto& e : u) {
+                    cd v(e.re, e.im);
+                    v *= f;
+                    e = cdbl{v.real(), v.imag()};
+                }
+                for (int r = 0; r < dim; ++r) {
+                    cd v(u[r * dim + r].re, u[r * dim + r].im);
+                    v += c;  // as realise(): complex += double leaves the imaginary part alone
+                    u[r * dim + r] = cdbl{v.real(), v.imag()};
+                }
+            }
+        } else if (op.gen == QBG_GEN_SHIFT) {
+            const cd e = std::polar(1.0, th);
+            u[0] = cdbl{1.0, 0.0};
+            u[1] = cdbl{e.real(), e.imag()};
+        } else {
+            const cd e = std::polar(1.0, th);
+            for (auto& v : u) v = cdbl{e.real(), e.imag()};
+        }
+        // udag = adjoint(u) (kernels.cu), in place
+        std::vector<cdbl>& a = ro.udag.m;
+        if (ro.u.kind == QBG_MAT_DENSE) {
+            for (int cc = 0; cc < dim; ++cc)
+                for (int r = 0; r < dim; ++r) a[r * dim + cc] = cdbl{u[cc * dim + r].re, -u[cc * dim + r].im};
+        } else {
+            for (size_t r = 0; r < u.size(); ++r) a[r] = cdbl{u[r].re, -u[r].im};
+        }
+    }
+}
+
 namespace {
 
 // NVTX ranges around the engine's phases (visible to ncu --nvtx / nsys; no cost without a tool)
@@ -1038,7 +1103,14 @@ int qbg_prog_set_params(qbg_prog* p, const double* theta, int64_t n) {
     return guarded([&] {
         if (n != p->p.nparams) raise(QBG_ERR_VALIDATION, "dispatch: parameter count mismatch");
         p->p.theta.assign(theta, theta + n);
-        realise(p->p);
+        static const bool fast = [] {
+            const char* e = std::getenv("QBG_REALISE_FULL");  // diagnostics: always rebuild every op
+            return !(e && e[0] == '1');
+        }();
+        if (fast && p->p.realised && p->p.real.size() == p->p.ops.size())
+            realise_params(p->p);
+        else
+            realise(p->p);
         p->p.version++;
     });
 }
