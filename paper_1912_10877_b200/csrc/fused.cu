@@ -278,6 +278,62 @@ std::vector<PG> fuse_runs(std::vector<PG> in, bool backward) {
     return out;
 }
 
+// Whether every cross matrix A_k of a run is Hermitian (4 statistics suffice, G_CROSSH).
+bool run_hermitian(const PG& pg) {
+    for (const RunGrad& rg : pg.run) {
+        double sc = 0.0;
+        for (int k = 0; k < 4; ++k) sc = std::max(sc, std::hypot(rg.A[k].re, rg.A[k].im));
+        const double tol = 1e-12 * std::max(sc, 1e-300);
+        if (std::fabs(rg.A[0].im) > tol || std::fabs(rg.A[3].im) > tol || std::fabs(rg.A[2].re - rg.A[1].re) > tol ||
+            std::fabs(rg.A[2].im + rg.A[1].im) > tol)
+            return false;
+    }
+    return true;
+}
+
+// Where a plan matrix came from (plan_passes' emit_mat), so a new θ can rewrite the values only.
+enum { MS_G = 0, MS_GDENSE = 1, MS_KDIAG = 2, MS_KDENSE = 3 };
+struct MatSrc {
+    int gi;    // index into FusedPlan::gates
+    int what;  // MS_*
+};
+
+// Everything plan_passes reads from a fused gate apart from its matrix values: kinds, qubits,
+// controls, permutations, parameters, and the value-dependent predicates the emission branches
+// on (identity, X, Hermitian cross matrices).  Equal signatures => identical passes and ops.
+uint64_t pg_sig(const PG& pg) {
+    uint64_t h = 1469598103934665603ULL;
+    auto mix = [&](uint64_t v) {
+        h ^= v;
+        h *= 1099511628211ULL;
+        h ^= h >> 29;
+    };
+    auto mixg = [&](const Gate& g) {
+        mix(static_cast<uint64_t>(g.kind));
+        mix(static_cast<uint64_t>(g.t));
+        mix(static_cast<uint64_t>(g.dim));
+        for (int q = 0; q < g.t; ++q) mix(g.tbit[q]);
+        mix(g.tmask);
+        mix(g.cmask);
+        mix(g.cval);
+        mix(g.m.size());
+        mix(g.perm.size());
+        for (int v : g.perm) mix(static_cast<uint64_t>(v));
+    };
+    const Gate& g = pg.gate();
+    mixg(g);
+    mix(static_cast<uint64_t>(pg.param + 1));
+    mix(pg.k != nullptr);
+    if (pg.k) mixg(*pg.k);
+    mix(pg.run.size());
+    for (const RunGrad& rg : pg.run) mix(static_cast<uint64_t>(rg.param + 1));
+    mix(run_hermitian(pg));
+    const bool x1 = g.kind == QBG_MAT_PERMUTATION && g.t == 1 && g.perm[0] == 1 && g.m[0].re == 1 &&
+                    g.m[0].im == 0 && g.m[1].re == 1 && g.m[1].im == 0;
+    mix(x1);
+    return h;
+}
+
 struct Step {
     bool tile = false;
     DPass pass;
@@ -300,6 +356,11 @@ struct FusedPlan {
     std::vector<DOp> ops;
     std::vector<cdbl> mats;
     std::vector<GradEntry> epi;
+    // values-only refresh (new θ, same structure, refresh_values): where each matrix entry and
+    // each cross-gradient entry came from, and the structural signature of the fused gate list
+    std::vector<MatSrc> msrc;
+    std::vector<std::pair<int, int>> esrc;  // (gate, run index), (-1, -1): no value
+    std::vector<uint64_t> sig;
     int64_t ncomps = 0;
     std::vector<jit::Kernel> jk;
     DOp* d_ops = nullptr;
@@ -609,9 +670,10 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
                     if (slot_of[L] >= 0) return static_cast<uint8_t>((LOC_REG << 6) | slot_of[L]);
                     return static_cast<uint8_t>((LOC_THR << 6) | pos_of[L]);
                 };
-                auto emit_mat = [&](const std::vector<cdbl>& m) {
+                auto emit_mat = [&](const std::vector<cdbl>& m, int what) {
                     int off = static_cast<int>(pl.mats.size()) - P.mat_base;
                     pl.mats.insert(pl.mats.end(), m.begin(), m.end());
+                    pl.msrc.push_back({gi, what});
                     return off;
                 };
                 // gradient ops first (reverse pass: before the uncompute)
@@ -621,15 +683,7 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
                     const bool diag_run = is_diagonal(g);
                     if ((rl >> 6) != LOC_REG && !diag_run)
                         raise(QBG_ERR_INTERNAL, "fused plan: a non-diagonal run off the register slots");
-                    bool herm = jit::enabled();
-                    for (const RunGrad& rg : pg.run) {
-                        double sc = 0.0;
-                        for (int k = 0; k < 4; ++k) sc = std::max(sc, std::hypot(rg.A[k].re, rg.A[k].im));
-                        const double tol = 1e-12 * std::max(sc, 1e-300);
-                        if (std::fabs(rg.A[0].im) > tol || std::fabs(rg.A[3].im) > tol ||
-                            std::fabs(rg.A[2].re - rg.A[1].re) > tol || std::fabs(rg.A[2].im + rg.A[1].im) > tol)
-                            herm = false;
-                    }
+                    bool herm = jit::enabled() && run_hermitian(pg);
                     // a diagonal run only needs Im C00 / Im C11, wherever its qubit lives (its
                     // A_k = K_k are diagonal); it may sit on a thread or tile bit
                     if (diag_run) herm = true;
@@ -638,13 +692,15 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
                     o.a = static_cast<uint8_t>(rl & 63);
                     o.b = static_cast<uint8_t>(rl >> 6);
                     o.gslot = ncomp;
-                    for (const RunGrad& rg : pg.run) {
+                    for (size_t r = 0; r < pg.run.size(); ++r) {
+                        const RunGrad& rg = pg.run[r];
                         GradEntry e{};
                         e.type = herm ? 2 : 1;
                         e.comp = static_cast<int>(P.grad_base) + ncomp;
                         e.param = rg.param;
                         std::memcpy(e.A, rg.A, sizeof(e.A));
                         pl.epi.push_back(e);
+                        pl.esrc.push_back({gi, static_cast<int>(r)});
                     }
                     ncomp += herm ? 4 : 8;
                     pl.ops.push_back(o);
@@ -658,6 +714,7 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
                     e.comp = static_cast<int>(P.grad_base) + ncomp;
                     e.param = pg.param;
                     pl.epi.push_back(e);
+                    pl.esrc.push_back({-1, -1});
                     ncomp += 1;
                     if (is_diagonal(K)) {
                         std::vector<cdbl> d(K.dim);
@@ -677,16 +734,16 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
                             o.t = static_cast<uint8_t>(K.t);
                             for (int q = 0; q < K.t; ++q) o.aux |= static_cast<uint64_t>(loc_code(K.tbit[q])) << (8 * q);
                         }
-                        o.mat = emit_mat(d);
+                        o.mat = emit_mat(d, MS_KDIAG);
                     } else if (K.t == 1) {
                         o.code = G_DENSE1;
                         o.a = static_cast<uint8_t>(slot_of[tg.local[K.tbit[0]]]);
-                        o.mat = emit_mat(dense_of(K));
+                        o.mat = emit_mat(dense_of(K), MS_KDENSE);
                     } else {
                         o.code = G_DENSE2;
                         o.a = static_cast<uint8_t>(slot_of[tg.local[K.tbit[0]]]);
                         o.b = static_cast<uint8_t>(slot_of[tg.local[K.tbit[1]]]);
-                        o.mat = emit_mat(dense_of(K));
+                        o.mat = emit_mat(dense_of(K), MS_KDENSE);
                     }
                     pl.ops.push_back(o);
                 }
@@ -702,7 +759,7 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
                         o.t = static_cast<uint8_t>(g.t);
                         for (int q = 0; q < g.t; ++q) o.aux |= static_cast<uint64_t>(loc_code(g.tbit[q])) << (8 * q);
                     }
-                    o.mat = emit_mat(g.m);
+                    o.mat = emit_mat(g.m, MS_G);
                 } else if (g.t == 1) {
                     o.a = static_cast<uint8_t>(slot_of[tg.local[g.tbit[0]]]);
                     if (g.kind == QBG_MAT_PERMUTATION) {
@@ -713,17 +770,17 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
                         } else {
                             o.code = OP_PERM1;
                             o.b = swapped ? 1 : 0;
-                            o.mat = emit_mat(g.m);
+                            o.mat = emit_mat(g.m, MS_G);
                         }
                     } else {
                         o.code = OP_DENSE1;
-                        o.mat = emit_mat(g.m);
+                        o.mat = emit_mat(g.m, MS_G);
                     }
                 } else {
                     o.code = OP_DENSE2;
                     o.a = static_cast<uint8_t>(slot_of[tg.local[g.tbit[0]]]);
                     o.b = static_cast<uint8_t>(slot_of[tg.local[g.tbit[1]]]);
-                    o.mat = emit_mat(dense_of(g));
+                    o.mat = emit_mat(dense_of(g), MS_GDENSE);
                 }
                 pl.ops.push_back(o);
             }
@@ -1403,26 +1460,32 @@ uint64_t pass_key(const DPass& P, const DOp* ops, int M, int RB, bool back, bool
 std::mutex g_pass_mu;
 std::unordered_map<uint64_t, jit::Kernel> g_pass_kernels;  // pass_key -> loaded kernel
 
+// The specialised kernel's matrix parameter (PM<T, 2*nmats>): the pass's matrices by value.
+void fill_blob(Step& st, const std::vector<cdbl>& mats, bool c128) {
+    const DPass& P = st.pass;
+    const int nm2 = std::max(2, 2 * P.nmats);
+    st.blob.assign(static_cast<size_t>(nm2) * (c128 ? 8 : 4), 0);
+    for (int k = 0; k < P.nmats; ++k) {
+        const cdbl& v = mats[P.mat_base + k];
+        if (c128) {
+            double* d = reinterpret_cast<double*>(st.blob.data());
+            d[2 * k] = v.re;
+            d[2 * k + 1] = v.im;
+        } else {
+            float* f = reinterpret_cast<float*>(st.blob.data());
+            f[2 * k] = static_cast<float>(v.re);
+            f[2 * k + 1] = static_cast<float>(v.im);
+        }
+    }
+}
+
 void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128, bool check_only = false) {
     const int NW = (1 << (M - RB)) / 32;
     const size_t elem = c128 ? 16 : 8;
     auto fill = [&](Step& st) {  // matrix parameter blob + shared memory of one step
         const DPass& P = st.pass;
         st.flops = pass_flops(P, pl.ops.data() + P.op_base, M, back);
-        const int nm2 = std::max(2, 2 * P.nmats);
-        st.blob.assign(static_cast<size_t>(nm2) * (c128 ? 8 : 4), 0);
-        for (int k = 0; k < P.nmats; ++k) {
-            const cdbl& v = pl.mats[P.mat_base + k];
-            if (c128) {
-                double* d = reinterpret_cast<double*>(st.blob.data());
-                d[2 * k] = v.re;
-                d[2 * k + 1] = v.im;
-            } else {
-                float* f = reinterpret_cast<float*>(st.blob.data());
-                f[2 * k] = static_cast<float>(v.re);
-                f[2 * k + 1] = static_cast<float>(v.im);
-            }
-        }
+        fill_blob(st, pl.mats, c128);
         const size_t tile_bytes = (back ? 2 : 1) * (elem << M);
         const int nwt = (pipeline_enabled() ? consumer_groups(back) : 1) * NW;
         const size_t cells = back ? static_cast<size_t>(P.ngrad) * (nwt + 1) * 8 : 0;
@@ -1547,11 +1610,18 @@ int batch_bits(int64_t B) {
 }
 
 std::shared_ptr<FusedPlan> build_host_plan(const Program& p, const DevState& s, int dir);
+bool refresh_values(FusedPlan& pl, const Program& p);
 
 std::shared_ptr<FusedPlan> get_plan(std::vector<std::shared_ptr<FusedPlan>>& cache, const Program& p,
                                     const DevState& s, int dir) {
     for (auto& c : cache)
         if (c->dir == dir && c->B == s.B && c->dtype == s.dtype && c->n == s.n && c->version == p.version) return c;
+    static const bool refresh = env_int("QBG_PLAN_REFRESH", 1) != 0;  // 0: rebuild the plan on every new θ
+    if (refresh)
+        for (auto& c : cache)
+            if (c->dir == dir && c->B == s.B && c->dtype == s.dtype && c->n == s.n && !c->msrc.empty() &&
+                refresh_values(*c, p))
+                return c;
     cache.erase(std::remove_if(cache.begin(), cache.end(),
                                [&](const std::shared_ptr<FusedPlan>& c) { return c->dir == dir && c->B == s.B; }),
                 cache.end());
@@ -1590,14 +1660,8 @@ std::shared_ptr<FusedPlan> get_plan(std::vector<std::shared_ptr<FusedPlan>>& cac
     return pl;
 }
 
-// The planner alone (no device, no JIT): used by get_plan and by the host-only preview.
-std::shared_ptr<FusedPlan> build_host_plan(const Program& p, const DevState& s, int dir) {
-    auto pl = std::make_shared<FusedPlan>();
-    pl->version = p.version;
-    pl->B = s.B;
-    pl->dtype = s.dtype;
-    pl->n = s.n;
-    pl->dir = dir;
+// The realised program as the planner's fused gate list (dir 0 forward, 1 adjoint, 2 reverse).
+std::vector<PG> plan_gates(const Program& p, int dir) {
     const size_t N = p.real.size();
     std::vector<PG> gs;
     gs.reserve(N);
@@ -1615,7 +1679,74 @@ std::shared_ptr<FusedPlan> build_host_plan(const Program& p, const DevState& s, 
         }
         gs.push_back(std::move(g));
     }
-    pl->gates = fuse_runs(std::move(gs), dir == 2);
+    return fuse_runs(std::move(gs), dir == 2);
+}
+
+// New θ on a program whose plan exists: when the fused gate list keeps its structure (pg_sig),
+// the passes, ops and specialised kernels stay; only the matrix values, the cross-gradient
+// matrices and the kernels' matrix parameters are rewritten (no plan_passes, no JIT lookup).
+// Returns false when the structure changed (the caller rebuilds).
+bool refresh_values(FusedPlan& pl, const Program& p) {
+    std::vector<PG> gates = plan_gates(p, pl.dir);
+    if (gates.size() != pl.sig.size()) return false;
+    for (size_t i = 0; i < gates.size(); ++i)
+        if (pg_sig(gates[i]) != pl.sig[i]) return false;
+    std::vector<cdbl> mats;
+    mats.reserve(pl.mats.size());
+    for (const MatSrc& ms : pl.msrc) {
+        const Gate& g = gates[ms.gi].gate();
+        switch (ms.what) {
+            case MS_G:
+                mats.insert(mats.end(), g.m.begin(), g.m.end());
+                break;
+            case MS_GDENSE: {
+                std::vector<cdbl> d = dense_of(g);
+                mats.insert(mats.end(), d.begin(), d.end());
+                break;
+            }
+            case MS_KDIAG: {
+                const Gate& K = *gates[ms.gi].k;
+                for (int r = 0; r < K.dim; ++r) mats.push_back(K.kind == QBG_MAT_IDENTITY ? cdbl{1, 0} : K.m[r]);
+                break;
+            }
+            default: {
+                std::vector<cdbl> d = dense_of(*gates[ms.gi].k);
+                mats.insert(mats.end(), d.begin(), d.end());
+            }
+        }
+    }
+    if (mats.size() != pl.mats.size() || pl.esrc.size() != pl.epi.size())
+        raise(QBG_ERR_INTERNAL, "fused plan: value refresh does not match the plan layout");
+    for (size_t e = 0; e < pl.epi.size(); ++e)
+        if (pl.esrc[e].first >= 0)
+            std::memcpy(pl.epi[e].A, gates[pl.esrc[e].first].run[pl.esrc[e].second].A, sizeof(pl.epi[e].A));
+    pl.mats.swap(mats);
+    pl.gates = std::move(gates);
+    const bool c128 = pl.dtype == QBG_C128;
+    for (auto& st : pl.steps)
+        if (st.tile) fill_blob(st, pl.mats, c128);
+    // stream-ordered: passes of the previous θ still queued read the old values first
+    if (!pl.mats.empty())
+        QBG_CUDA(cudaMemcpyAsync(pl.d_mats, pl.mats.data(), pl.mats.size() * sizeof(cdbl), cudaMemcpyHostToDevice,
+                                 stream()));
+    if (!pl.epi.empty())
+        QBG_CUDA(cudaMemcpyAsync(pl.d_epi, pl.epi.data(), pl.epi.size() * sizeof(GradEntry), cudaMemcpyHostToDevice,
+                                 stream()));
+    pl.version = p.version;
+    return true;
+}
+
+// The planner alone (no device, no JIT): used by get_plan and by the host-only preview.
+std::shared_ptr<FusedPlan> build_host_plan(const Program& p, const DevState& s, int dir) {
+    auto pl = std::make_shared<FusedPlan>();
+    pl->version = p.version;
+    pl->B = s.B;
+    pl->dtype = s.dtype;
+    pl->n = s.n;
+    pl->dir = dir;
+    pl->gates = plan_gates(p, dir);
+    pl->sig.reserve(pl->gates.size());
+    for (const PG& g : pl->gates) pl->sig.push_back(pg_sig(g));
     const int nb = batch_bits(s.B);
     const Geo g = geo_for(dir);
     pl->M = g.M;
@@ -1630,6 +1761,7 @@ std::shared_ptr<FusedPlan> build_host_plan(const Program& p, const DevState& s, 
             e.comp = st.single_comp;
             e.param = pl->gates[st.single].param;
             pl->epi.push_back(e);
+            pl->esrc.push_back({-1, -1});
         } else if (!st.tile && !pl->gates[st.single].run.empty()) {
             raise(QBG_ERR_INTERNAL, "fused plan: untiled rotation run");
         }

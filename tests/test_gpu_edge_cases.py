@@ -144,3 +144,30 @@ def test_redispatch_matches_fresh_program():
         assert np.array_equal(a.param_grads, b.param_grads)
         assert np.array_equal(a.state_grad.state(), b.state_grad.state())
         assert np.array_equal(r1.state(), r2.state())
+
+
+@pytest.mark.parametrize("dtype,nbatch", [("c128", 1), ("c128", 4), ("c64", 2)])
+def test_plan_value_refresh_over_many_thetas(dtype, nbatch):
+    """A new θ on a program whose fused plans exist rewrites only the plans' matrix values
+    (fused.cu refresh_values: same passes, ops and kernels).  Over successive θ — an optimiser
+    loop — the reused program must match a freshly compiled one bit for bit, forward and reverse."""
+    n, d = 13, 3
+    h = C.heisenberg(n)
+    reused = C.variational_circuit(n, d)
+    rng = np.random.default_rng(5)
+    P = B.nparameters(reused)
+    for it in range(4):
+        th = rng.uniform(0, 2 * np.pi, P)
+        if it == 2:
+            th[::7] = 0.0  # rotations at the identity keep their structure
+        B.dispatch(reused, th)
+        fresh = C.variational_circuit(n, d)
+        B.dispatch(fresh, th)
+        a = qb.expect_grad(h, (qb.zero_state(n, nbatch=nbatch, dtype=dtype), reused))
+        b = qb.expect_grad(h, (qb.zero_state(n, nbatch=nbatch, dtype=dtype), fresh))
+        assert np.array_equal(a.energies, b.energies)
+        assert np.array_equal(a.param_grads, b.param_grads)
+        r1, r2 = qb.zero_state(n, nbatch=nbatch, dtype=dtype), qb.zero_state(n, nbatch=nbatch, dtype=dtype)
+        qb.apply(r1, reused)
+        qb.apply(r2, fresh)
+        assert np.array_equal(r1.state(), r2.state())
