@@ -360,6 +360,11 @@ def main():
                     "per_gate_convention": per_gate_roofline(top, per_launch_ms, G, S, peak),
                     "kernels": [{k2: (round(v, 6) if isinstance(v, float) else v) for k2, v in kk.items()}
                                 for kk in kernels[:8]]}
+        # whole-step HBM throughput: every kernel's algorithmic bytes of one step over the step time
+        step_bytes = sum(k["bytes"] for k in kernels) / 2
+        roofline["step"] = {"hbm_gbs": step_bytes / (ms / 1e3) / 1e9, "frac": step_bytes / (ms / 1e3) / 1e9 / peak,
+                            "bytes_per_step": step_bytes,
+                            "note": "algorithmic bytes of all passes of one step / device step time"}
 
     # ---- CPU baseline: the reference on this host's cores, bounded sample (rank 0, N=1) ----
     cpu = None
@@ -383,6 +388,9 @@ def main():
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (zero_state, θ ~ U(0,2π) from Rng(42+rank))",
             "config": workload_config(args),
             "hbm_gbs_algorithmic": hbm_alg, "hbm_frac_algorithmic": hbm_alg / peak,
+            "hbm_note": "hbm_*_algorithmic use the per-gate convention (2S per gate per state pass, SURVEY 8(d)): "
+                        "> 1 because fusion applies ~34 gates per HBM pass; the real HBM rates are "
+                        "roofline.achieved (dominant kernel) and roofline.step (whole step)",
             "energy": float(res.energies[0]),
             "fusion": not args.no_fusion, "prog_stats": prog.stats(),
             "e2e": e2e, "gpu_launches": launches, "clocks": ck, "roofline": roofline, "cpu_baseline": cpu,
