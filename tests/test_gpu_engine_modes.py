@@ -37,3 +37,23 @@ def test_fast_consumers_slot_protocol(tma):
     e = dict(os.environ, QBG_EXP="2", QBG_TMA=tma)
     r = subprocess.run([sys.executable, "-c", code], env=e, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_plan_refresh_equals_rebuild():
+    """An optimiser loop (new θ every step) with the values-only plan refresh (default) and with a
+    full replan per θ (QBG_PLAN_REFRESH=0) gives bitwise-identical energies and gradients."""
+    code = ("import sys, hashlib; sys.path.insert(0, '.'); import numpy as np; import paper_1912_10877_b200 as qb; "
+            "c = qb.variational_circuit(14, 4); h = qb.heisenberg(14); rng = np.random.default_rng(3); "
+            "P = len(qb.parameters(c)); m = hashlib.sha256()\n"
+            "for it in range(5):\n"
+            "    qb.dispatch(c, rng.uniform(0, 2 * np.pi, P))\n"
+            "    r = qb.expect_grad(h, (qb.zero_state(14, nbatch=2), c))\n"
+            "    m.update(np.ascontiguousarray(r.energies).tobytes()); m.update(np.ascontiguousarray(r.param_grads).tobytes())\n"
+            "print('H', m.hexdigest())")
+    outs = []
+    for v in ("1", "0"):
+        e = dict(os.environ, QBG_PLAN_REFRESH=v)
+        r = subprocess.run([sys.executable, "-c", code], env=e, cwd=ROOT, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+        outs.append([ln for ln in r.stdout.splitlines() if ln.startswith("H ")][-1])
+    assert outs[0] == outs[1]
