@@ -863,7 +863,6 @@ bool tma_layout(const DPass& P, int M, bool c128, std::vector<TmaDim>& dims) {
         runs.push_back({static_cast<uint64_t>(P.B) << q, e - q, in, in ? 0 : 2, q});
         q = e;
     }
-    bool folded = false;
     for (size_t i = 0; i < runs.size(); ++i) {
         const Run& r = runs[i];
         const uint64_t size = r.len < 0 ? static_cast<uint64_t>(-r.len) : (uint64_t{1} << r.len);
@@ -877,7 +876,6 @@ bool tma_layout(const DPass& P, int M, bool c128, std::vector<TmaDim>& dims) {
                 d.stride = (r.elems_w << done) * 16;
                 d.box = static_cast<uint32_t>(d.size);
                 d.coord = 0;
-                if (first) folded = true;
                 dims.push_back(d);
                 done += piece;
             }
@@ -893,7 +891,6 @@ bool tma_layout(const DPass& P, int M, bool c128, std::vector<TmaDim>& dims) {
             dims.push_back(d);
         }
     }
-    (void)folded;
     return dims.size() <= 5;
 }
 

@@ -18,6 +18,8 @@ def main():
     h = qb.heisenberg(n)
     reg = qb.rand_state(n, 2, seed=1)
     r = qb.expect_grad(h, (reg, circ))
+    qb.dispatch(circ, qb.parameters(circ) + 0.1)  # new θ: values-only plan refresh
+    r = qb.expect_grad(h, (reg, circ))
     qb.set_fusion(False)
     r2 = qb.expect_grad(h, (reg, circ))
     qb.set_fusion(True)
