@@ -57,3 +57,7 @@ def test_plan_refresh_equals_rebuild():
         assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
         outs.append([ln for ln in r.stdout.splitlines() if ln.startswith("H ")][-1])
     assert outs[0] == outs[1]
+    # the refreshed plans' kernels with every generated index bounds-checked (trap on violation)
+    e = dict(os.environ, QBG_JIT_CHECK="1")
+    r = subprocess.run([sys.executable, "-c", code], env=e, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
