@@ -453,10 +453,12 @@ struct Nvtx {
     ~Nvtx() { nvtxRangePop(); }
 };
 
-void run_program(const DevState& s, Program& p, bool adjoint) {
+// src (optional): the input when it is not s — s receives U·src (out-of-place apply).
+void run_program(const DevState& s, Program& p, bool adjoint, const void* src = nullptr) {
     Nvtx r(adjoint ? "qbg.apply_adjoint" : "qbg.apply");
     if (!p.realised) realise(p);
-    if (g_fusion && fused_forward(s, p, adjoint)) return;
+    if (g_fusion && fused_forward(s, p, adjoint, src)) return;
+    if (src) QBG_CUDA(cudaMemcpyAsync(s.ptr, src, s.bytes(), cudaMemcpyDeviceToDevice, g_stream));
     size_t N = p.real.size();
     for (size_t q = 0; q < N; ++q) {
         size_t k = adjoint ? N - 1 - q : q;
@@ -1252,7 +1254,6 @@ void grad_driver(qbg_reg* r, Program& p, int32_t inplace, qbg_reg* state_grad, d
     if (!inplace) {
         ensure(work);
         psi.ptr = work.ptr;
-        QBG_CUDA(cudaMemcpyAsync(psi.ptr, r->s.ptr, r->s.bytes(), cudaMemcpyDeviceToDevice, g_stream));
     }
     DevState adj = r->s;
     if (state_grad) {
@@ -1261,7 +1262,8 @@ void grad_driver(qbg_reg* r, Program& p, int32_t inplace, qbg_reg* state_grad, d
         ensure(adjbuf);
         adj.ptr = adjbuf.ptr;
     }
-    run_program(psi, p, false);
+    // out-of-place: the first forward pass reads the caller's register (no separate copy)
+    run_program(psi, p, false, inplace ? nullptr : r->s.ptr);
     double* e = static_cast<double*>(scratch(r->s.B * sizeof(double), 10));
     seed(psi, adj, e);
     double* dg = static_cast<double*>(scratch(std::max<int64_t>(1, p.nparams) * sizeof(double), 11));

@@ -934,6 +934,9 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
       << (c128 ? "double" : "float") << ", " << std::max(2, 2 * nmats)
       << "> pm, const __grid_constant__ TMap tmp, const __grid_constant__ TMap tma) {\n";
     s << "typedef " << (c128 ? "c128" : "c64") << " V;\nconstexpr int R = " << R << ";\n";
+    // forward: the tile is stored to adj when given (out-of-place pass: load psi, store adj; the
+    // first pass of an out-of-place expect' reads the caller's register directly), else in place
+    if (!back) s << "V* const outp = adj ? adj : psi;\nconst TMap* const outm = adj ? &tma : &tmp;\n";
     s << (pipe ? "const int tid_all = threadIdx.x;\n" : "const int tid = threadIdx.x;\n");
     s << "#define MV(i) mk<V>(pm.m[2 * (i)], pm.m[2 * (i) + 1])\n";
     // index checks (QBG_JIT_CHECK=1: every global / shared tile index is bounds-checked and traps;
@@ -1004,7 +1007,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             // one elected thread: the computed tile (linear layout) back as one TMA tensor store, and
             // its shared-memory reads retired before the slot is refilled
             s << "if (lane == 0) {\nconst u64 ptile = blockIdx.x + (it - " << nbuf << ") * gridDim.x;\n";
-            s << "tma_store" << td.size() << "(&tmp, buf, " << tma_coords("outer", "ptile") << ");\n";
+            s << "tma_store" << td.size() << (back ? "(&tmp" : "(outm") << ", buf, " << tma_coords("outer", "ptile") << ");\n";
             if (back) s << "tma_store" << td.size() << "(&tma, buf + " << (1 << M) << ", " << tma_coords("outer", "ptile") << ");\n";
             s << "tma_commit();\ntma_wait_read0();\n}\n";
         } else if (pstore) {
@@ -1020,7 +1023,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                     s << "\n";
                 }
                 for (int k = k0; k < k1; ++k) {
-                    s << "psi[GI(tb + gp + " << kgo(k) << "ll)] = d" << k << ";";
+                    s << (back ? "psi" : "outp") << "[GI(tb + gp + " << kgo(k) << "ll)] = d" << k << ";";
                     if (back) s << " adj[GI(tb + gp + " << kgo(k) << "ll)] = e" << k << ";";
                     s << "\n";
                 }
@@ -1363,7 +1366,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
     } else {
         if (exp_mode == 1 || exp_mode == 5 || exp_mode == 6) s << "if (outer == ~0ull) {\n";
         for (int j = 0; j < R; ++j) {
-            s << "psi[GI(tb + gL + " << goff(SL, j) << "ll)] = x[" << j << "];";
+            s << (back ? "psi" : "outp") << "[GI(tb + gL + " << goff(SL, j) << "ll)] = x[" << j << "];";
             if (back) s << " adj[GI(tb + gL + " << goff(SL, j) << "ll)] = y[" << j << "];";
             s << "\n";
         }
@@ -1574,7 +1577,7 @@ void launch_jit(V* psi, V* adj, Step& st, FusedPlan& pl, double* gpart, int64_t 
                 bx[d] = td[d].box;
             }
             jit::encode_tensor_map(tmp, psi, static_cast<int>(td.size()), sz, st, bx);
-            if (BACK) jit::encode_tensor_map(tma, adj, static_cast<int>(td.size()), sz, st, bx);
+            if (adj) jit::encode_tensor_map(tma, adj, static_cast<int>(td.size()), sz, st, bx);
         }
     }
     void* args[] = {&psi, &adj, &gpart, &gcols, &gbase, st.blob.data(), tmp, tma};
@@ -1770,10 +1773,27 @@ bool fusable(const DevState& s, int M) {
     return s.n >= M - nb && s.n <= 62;
 }
 
+// src (optional): the input state when it is not s itself — the first pass then loads from src
+// and stores to s (specialised tile kernels), else src is copied into s first.
 template <typename V>
-void run_forward(const DevState& s, FusedPlan& pl) {
+void run_forward(const DevState& s, FusedPlan& pl, const void* src) {
     V* psi = static_cast<V*>(s.ptr);
+    static const bool oop = env_int("QBG_FWD_OOP", 1) != 0;  // 0: always copy, then in place
+    if (src) {
+        const Step* f = pl.steps.empty() ? nullptr : &pl.steps.front();
+        if (oop && f && f->tile && f->jk >= 0) {
+            launch_jit<V, false>(static_cast<V*>(const_cast<void*>(src)), psi, pl.steps.front(), pl, nullptr, 0);
+        } else {
+            QBG_CUDA(cudaMemcpyAsync(psi, src, s.bytes(), cudaMemcpyDeviceToDevice, stream()));
+            src = nullptr;
+        }
+    }
+    bool skip = src != nullptr;
     for (auto& st : pl.steps) {
+        if (skip) {
+            skip = false;
+            continue;
+        }
         if (st.tile)
             if (st.jk >= 0)
                 launch_jit<V, false>(psi, nullptr, st, pl, nullptr, 0);
@@ -1812,13 +1832,13 @@ void run_backward(const DevState& psi, const DevState& adj, FusedPlan& pl, doubl
 
 }  // namespace
 
-bool fused_forward(const DevState& s, Program& p, bool adjoint) {
+bool fused_forward(const DevState& s, Program& p, bool adjoint, const void* src) {
     if (!fusable(s, geo_for(0).M)) return false;
     auto pl = get_plan(p.plans, p, s, adjoint ? 1 : 0);
     if (s.dtype == QBG_C128)
-        run_forward<double2>(s, *pl);
+        run_forward<double2>(s, *pl, src);
     else
-        run_forward<float2>(s, *pl);
+        run_forward<float2>(s, *pl, src);
     return true;
 }
 

@@ -42,7 +42,8 @@ Gate place_gate(const qbg_op& op, int kind, int dim, const std::vector<cdbl>& m,
 void realise(Program& p);
 
 // fused engine (fused.cu); return false when the plan does not apply (caller falls back)
-bool fused_forward(const DevState& s, Program& p, bool adjoint);
+// src: optional input state (not s): the first pass reads it and writes s (out-of-place start)
+bool fused_forward(const DevState& s, Program& p, bool adjoint, const void* src = nullptr);
 bool fused_backward(const DevState& psi, const DevState& adj, Program& p, double* d_grads /* nparams, += */);
 bool fused_obs_apply(const DevState& psi, const DevState& phi, Observable& o, double* d_energy /* B or null */);
 // passes of the most recently built forward / backward plans (0 when unfused)

@@ -171,3 +171,21 @@ def test_plan_value_refresh_over_many_thetas(dtype, nbatch):
         qb.apply(r1, reused)
         qb.apply(r2, fresh)
         assert np.array_equal(r1.state(), r2.state())
+
+
+@pytest.mark.parametrize("dtype,nbatch", [("c128", 1), ("c128", 2), ("c64", 4)])
+def test_out_of_place_expect_grad_reads_input_directly(dtype, nbatch):
+    """The out-of-place expect' starts with a forward pass that loads the caller's register and
+    stores the work state (no device copy first).  The input must be left untouched, and the
+    results must equal the in-place run's bit for bit (the same passes on the same values)."""
+    n = 13
+    circ = C.variational_circuit(n, 3)
+    B.dispatch(circ, np.random.default_rng(8).uniform(0, 2 * np.pi, B.nparameters(circ)))
+    h = C.heisenberg(n)
+    reg = qb.rand_state(n, nbatch, seed=4, dtype=dtype)
+    before = reg.state().copy()
+    a = qb.expect_grad(h, (reg, circ))
+    assert np.array_equal(reg.state(), before)
+    b = qb.expect_grad(h, (reg.copy(), circ), inplace=True)
+    assert np.array_equal(a.energies, b.energies)
+    assert np.array_equal(a.param_grads, b.param_grads)
