@@ -628,12 +628,17 @@ __global__ void k_grad_csr(const double* __restrict__ vals, const int* __restric
     if (ptr[p + 1] > ptr[p]) grads[p] += s;
 }
 
+// One warp per row: lane l sums columns l, l+32, … in order (coalesced across the warp), then a
+// fixed xor-butterfly — the same order on every run (deterministic gradients).
 __global__ void k_rows(const double* __restrict__ part, int64_t nrows, int64_t cols, double* __restrict__ out) {
-    int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t r = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (r >= nrows) return;
+    const double* row = part + r * cols;
     double s = 0.0;
-    for (int64_t b = 0; b < cols; ++b) s += part[r * cols + b];
-    out[r] = s;
+    for (int64_t b = lane; b < cols; b += 32) s += row[b];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[r] = s;
 }
 
 // ---- observable seed: phi (+)= Σ_groups Σ_terms c (-1)^{|src & z|} psi[src], src = l ^ xloc ----
@@ -759,7 +764,7 @@ void launch_interp(int dtype, bool back, void* psi, void* adj, const DPass& P, c
 
 void launch_grad_rows(const double* part, int64_t nrows, int64_t cols, double* sums) {
     LaunchScope ls("grad_rows", 8.0 * nrows * cols);
-    k_rows<<<static_cast<unsigned>((nrows + 127) / 128), 128, 0, stream()>>>(part, nrows, cols, sums);
+    k_rows<<<static_cast<unsigned>((nrows + 7) / 8), 256, 0, stream()>>>(part, nrows, cols, sums);
     QBG_CUDA(cudaGetLastError());
 }
 
