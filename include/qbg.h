@@ -117,8 +117,13 @@ int32_t qbg_get_qubit_cap(void);
 /* state_alloc_counter, register.hpp:45-48: counts full-state device allocations */
 uint64_t qbg_alloc_count(void);
 /* Select the CUDA device and the stream (a cudaStream_t, 0 = legacy default) new work is
-   issued on.  Per calling process. */
+   issued on.  One device per process: once the library holds anything on a device (registers,
+   workspace, plans, loaded kernels) a different device is rejected with QBG_ERR_VALIDATION. */
 int qbg_set_device(int32_t device);
+/* Frees the library-owned device workspace: the expect' work/adjoint states, the Krylov basis and
+   the scratch slots (counted by qbg_alloc_count while held).  Workspace larger than every live
+   register is also released automatically when a register is destroyed. */
+int qbg_release_workspace(void);
 int qbg_set_stream(void* stream);
 int qbg_synchronize(void);
 /* Fusion switch: 1 (default) = tiled multi-gate passes, 0 = one kernel per gate. */
@@ -198,6 +203,8 @@ int qbg_relax(qbg_reg* reg, const int32_t* locs, int32_t nloc, int32_t to_nactiv
    layout (batch slowest) as little-endian complex doubles.  Files interchange with qblock. */
 int qbg_save(const qbg_reg* reg, const char* path);
 int qbg_load(const char* path, uint64_t seed, int32_t dtype, qbg_reg** out);
+/* The same format from memory (Register::load(std::istream&) of the C++ shim). */
+int qbg_load_memory(const void* data, int64_t nbytes, uint64_t seed, int32_t dtype, qbg_reg** out);
 
 /* ---- gate programs: apply(reg, block) lowered to instruct, SPEC.md:315-323 --------------- */
 int qbg_prog_create(int32_t nqubits, const qbg_op* ops, int64_t nops, const double* vals,
@@ -216,6 +223,9 @@ int qbg_prog_plan_preview(const qbg_prog* prog, int64_t nbatch, int32_t dtype, c
 /* Generates and compiles (NVRTC -> sm_100a cubin, no device needed) every specialised kernel the
    program (and observable, may be NULL) would use; *nkernels receives the number of passes. */
 int qbg_jit_check(const qbg_prog* prog, const qbg_obs* obs, int64_t nbatch, int32_t dtype, int64_t* nkernels);
+/* Kernel-cache statistics since load: NVRTC compilations vs cubins found in the cache (the
+   ahead-of-time cache built by build() lives in jit_cache/ next to libqbg.so). */
+int qbg_jit_stats(int64_t* nvrtc_builds, int64_t* cache_hits);
 int qbg_apply(qbg_reg* reg, const qbg_prog* prog);
 /* Applies the adjoint program (Daggered chain). */
 int qbg_apply_adjoint(qbg_reg* reg, const qbg_prog* prog);

@@ -16,7 +16,13 @@
 
 #include <complex>
 #include <cstdint>
+#include <cstring>
+#include <istream>
+#include <iterator>
+#include <map>
 #include <memory>
+#include <numbers>
+#include <ostream>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -64,12 +70,326 @@ inline void check(int rc) {
     }
 }
 
-// ---- matrix formats passed to instruct (matrix.hpp:41-129) -----------------------------------
-struct Identity { std::size_t dim; };
-struct Diagonal { std::vector<cplx> diag; };
-struct Permutation { std::vector<std::size_t> perm; std::vector<cplx> vals; };
-struct Dense { std::size_t dim; std::vector<cplx> a; };  // column-major a[c*dim + r]
-using MatrixRepr = std::variant<Identity, Diagonal, Permutation, Dense>;
+// ---- matrix formats (matrix.hpp:41-129): the six MatrixRepr alternatives, same validation ------
+struct Identity {
+    std::size_t dim = 0;
+    explicit Identity(std::size_t d) : dim(d) {
+        if (d == 0) throw ShapeError("Identity: dimension must be positive");
+    }
+};
+struct Diagonal {
+    std::vector<cplx> diag;
+    explicit Diagonal(std::vector<cplx> d) : diag(std::move(d)) {
+        if (diag.empty()) throw ShapeError("Diagonal: dimension must be positive");
+    }
+};
+// row i holds vals[i] at column perm[i] (0-based)
+struct Permutation {
+    std::vector<std::size_t> perm;
+    std::vector<cplx> vals;
+    Permutation(std::vector<std::size_t> p, std::vector<cplx> v) : perm(std::move(p)), vals(std::move(v)) {
+        if (perm.empty() || perm.size() != vals.size())
+            throw ShapeError("Permutation: perm and vals must be non-empty and equal length");
+        std::vector<char> hit(perm.size(), 0);
+        for (std::size_t c : perm) {
+            if (c >= perm.size() || hit[c]) throw ValidationError("Permutation: column indices must form a permutation");
+            hit[c] = 1;
+        }
+    }
+};
+// compressed sparse columns, rows sorted and unique within a column
+struct SparseColumns {
+    std::size_t dim = 0;
+    std::vector<std::size_t> colptr, rows;
+    std::vector<cplx> vals;
+    SparseColumns(std::size_t d, std::vector<std::size_t> cp, std::vector<std::size_t> r, std::vector<cplx> v)
+        : dim(d), colptr(std::move(cp)), rows(std::move(r)), vals(std::move(v)) {
+        if (dim == 0 || colptr.size() != dim + 1 || colptr.front() != 0 || colptr.back() != rows.size() ||
+            rows.size() != vals.size())
+            throw ShapeError("SparseColumns: inconsistent structure");
+        for (std::size_t c = 0; c < dim; ++c) {
+            if (colptr[c] > colptr[c + 1]) throw ShapeError("SparseColumns: column pointers not monotone");
+            for (std::size_t k = colptr[c]; k + 1 < colptr[c + 1]; ++k)
+                if (rows[k] >= rows[k + 1]) throw ValidationError("SparseColumns: rows must be sorted and unique");
+            if (colptr[c] < colptr[c + 1] && rows[colptr[c + 1] - 1] >= dim)
+                throw RangeError("SparseColumns: row index out of range");
+        }
+    }
+};
+// column-major a[c*dim + r]
+struct Dense {
+    std::size_t dim = 0;
+    std::vector<cplx> a;
+    Dense(std::size_t d, std::vector<cplx> data) : dim(d), a(std::move(data)) {
+        if (dim == 0 || a.size() != dim * dim) throw ShapeError("Dense: data size must be dim^2");
+    }
+    explicit Dense(std::size_t d) : dim(d), a(d * d, cplx(0.0)) {
+        if (dim == 0) throw ShapeError("Dense: dimension must be positive");
+    }
+    cplx& at(std::size_t r, std::size_t c) { return a[c * dim + r]; }
+    const cplx& at(std::size_t r, std::size_t c) const { return a[c * dim + r]; }
+};
+// rank one: left * right (right is a row vector, not conjugated)
+struct OuterProduct {
+    std::vector<cplx> left, right;
+    OuterProduct(std::vector<cplx> l, std::vector<cplx> r) : left(std::move(l)), right(std::move(r)) {
+        if (left.empty() || left.size() != right.size())
+            throw ShapeError("OuterProduct: vectors must be non-empty and equal length");
+    }
+};
+using MatrixRepr = std::variant<Identity, Diagonal, Permutation, SparseColumns, Dense, OuterProduct>;
+enum class MatKind : int { I = 0, D = 1, P = 2, S = 3, M = 4, Outer = 5 };
+inline MatKind kind_of(const MatrixRepr& m) { return static_cast<MatKind>(m.index()); }
+
+inline std::size_t mat_dim(const MatrixRepr& m) {
+    switch (kind_of(m)) {
+        case MatKind::I: return std::get<Identity>(m).dim;
+        case MatKind::D: return std::get<Diagonal>(m).diag.size();
+        case MatKind::P: return std::get<Permutation>(m).perm.size();
+        case MatKind::S: return std::get<SparseColumns>(m).dim;
+        case MatKind::M: return std::get<Dense>(m).dim;
+        default: return std::get<OuterProduct>(m).left.size();
+    }
+}
+inline Dense to_dense(const MatrixRepr& m) {  // matrix.hpp:229-233
+    const std::size_t d = mat_dim(m);
+    if (auto* x = std::get_if<Dense>(&m)) return *x;
+    Dense out(d);
+    switch (kind_of(m)) {
+        case MatKind::I:
+            for (std::size_t i = 0; i < d; ++i) out.at(i, i) = 1.0;
+            break;
+        case MatKind::D:
+            for (std::size_t i = 0; i < d; ++i) out.at(i, i) = std::get<Diagonal>(m).diag[i];
+            break;
+        case MatKind::P: {
+            auto& p = std::get<Permutation>(m);
+            for (std::size_t i = 0; i < d; ++i) out.at(i, p.perm[i]) = p.vals[i];
+            break;
+        }
+        case MatKind::S: {
+            auto& s = std::get<SparseColumns>(m);
+            for (std::size_t c = 0; c < d; ++c)
+                for (std::size_t k = s.colptr[c]; k < s.colptr[c + 1]; ++k) out.at(s.rows[k], c) = s.vals[k];
+            break;
+        }
+        default: {
+            auto& o = std::get<OuterProduct>(m);
+            for (std::size_t c = 0; c < d; ++c)
+                for (std::size_t r = 0; r < d; ++r) out.at(r, c) = o.left[r] * o.right[c];
+        }
+    }
+    return out;
+}
+// U† in the same class (matrix.hpp:594-643)
+inline MatrixRepr adjoint_mat(const MatrixRepr& m) {
+    switch (kind_of(m)) {
+        case MatKind::I: return m;
+        case MatKind::D: {
+            auto d = std::get<Diagonal>(m).diag;
+            for (auto& v : d) v = std::conj(v);
+            return Diagonal(std::move(d));
+        }
+        case MatKind::P: {
+            auto& p = std::get<Permutation>(m);
+            std::vector<std::size_t> inv(p.perm.size());
+            std::vector<cplx> v(p.perm.size());
+            for (std::size_t i = 0; i < p.perm.size(); ++i) {
+                inv[p.perm[i]] = i;
+                v[p.perm[i]] = std::conj(p.vals[i]);
+            }
+            return Permutation(std::move(inv), std::move(v));
+        }
+        case MatKind::Outer: {
+            auto& o = std::get<OuterProduct>(m);
+            std::vector<cplx> l(o.right.size()), r(o.left.size());
+            for (std::size_t i = 0; i < l.size(); ++i) l[i] = std::conj(o.right[i]);
+            for (std::size_t i = 0; i < r.size(); ++i) r[i] = std::conj(o.left[i]);
+            return OuterProduct(std::move(l), std::move(r));
+        }
+        default: {  // Sparse / Dense: conjugate transpose (kept dense; sparse gates are densified by instruct anyway)
+            Dense a = to_dense(m), out(a.dim);
+            for (std::size_t c = 0; c < a.dim; ++c)
+                for (std::size_t r = 0; r < a.dim; ++r) out.at(c, r) = std::conj(a.at(r, c));
+            if (kind_of(m) == MatKind::M) return out;
+            std::vector<std::size_t> cp{0}, rows;
+            std::vector<cplx> vals;
+            for (std::size_t c = 0; c < out.dim; ++c) {
+                for (std::size_t r = 0; r < out.dim; ++r)
+                    if (out.at(r, c) != cplx(0.0)) {
+                        rows.push_back(r);
+                        vals.push_back(out.at(r, c));
+                    }
+                cp.push_back(rows.size());
+            }
+            return SparseColumns(out.dim, std::move(cp), std::move(rows), std::move(vals));
+        }
+    }
+}
+
+// ---- gate matrices (gates.hpp:32-94) -----------------------------------------------------------
+namespace gatemat {
+inline const cplx i1{0.0, 1.0};
+inline MatrixRepr x() { return Permutation({1, 0}, {1.0, 1.0}); }
+inline MatrixRepr y() { return Permutation({1, 0}, {-i1, i1}); }
+inline MatrixRepr z() { return Diagonal({1.0, -1.0}); }
+inline MatrixRepr h() {
+    const double s = 1.0 / std::numbers::sqrt2;
+    return Dense(2, {s, s, s, -s});
+}
+inline MatrixRepr i2() { return Identity(2); }
+inline MatrixRepr s() { return Diagonal({1.0, i1}); }
+inline MatrixRepr sdag() { return Diagonal({1.0, -i1}); }
+inline MatrixRepr t() { return Diagonal({1.0, std::polar(1.0, std::numbers::pi / 4)}); }
+inline MatrixRepr tdag() { return Diagonal({1.0, std::polar(1.0, -std::numbers::pi / 4)}); }
+inline MatrixRepr swap() { return Permutation({0, 2, 1, 3}, {1.0, 1.0, 1.0, 1.0}); }
+inline MatrixRepr cnot() { return Permutation({0, 1, 3, 2}, {1.0, 1.0, 1.0, 1.0}); }  // control qubit 2, X on 1
+inline MatrixRepr cz() { return Permutation({0, 1, 2, 3}, {1.0, 1.0, 1.0, -1.0}); }
+inline MatrixRepr toffoli() { return Permutation({0, 1, 2, 3, 4, 5, 7, 6}, std::vector<cplx>(8, 1.0)); }
+inline MatrixRepr p0() { return SparseColumns(2, {0, 1, 1}, {0}, {1.0}); }
+inline MatrixRepr p1() { return SparseColumns(2, {0, 0, 1}, {1}, {1.0}); }
+inline MatrixRepr pu() { return SparseColumns(2, {0, 0, 1}, {0}, {1.0}); }
+inline MatrixRepr pd() { return SparseColumns(2, {0, 1, 1}, {1}, {1.0}); }
+inline MatrixRepr rx(double th) {
+    const cplx c = std::cos(th / 2), ms = -i1 * std::sin(th / 2);
+    return Dense(2, {c, ms, ms, c});
+}
+inline MatrixRepr ry(double th) {
+    const double c = std::cos(th / 2), s = std::sin(th / 2);
+    return Dense(2, {c, s, -s, c});
+}
+inline MatrixRepr rz(double th) { return Diagonal({std::polar(1.0, -th / 2), std::polar(1.0, th / 2)}); }
+inline MatrixRepr shift(double th) { return Diagonal({1.0, std::polar(1.0, th)}); }
+inline MatrixRepr global_phase(double th, std::size_t dim = 2) { return Diagonal(std::vector<cplx>(dim, std::polar(1.0, th))); }
+// rot(G, θ) = cos(θ/2) I − i sin(θ/2) G; a diagonal generator stays diagonal (gates.hpp:79-92)
+inline MatrixRepr rot(const MatrixRepr& g, double th) {
+    const double c = std::cos(th / 2), s = std::sin(th / 2);
+    const MatKind k = kind_of(g);
+    if (k == MatKind::I || k == MatKind::D) {
+        std::vector<cplx> d = k == MatKind::I ? std::vector<cplx>(mat_dim(g), 1.0) : std::get<Diagonal>(g).diag;
+        for (auto& v : d) v = cplx(c) - i1 * cplx(s) * v;
+        return Diagonal(std::move(d));
+    }
+    Dense out = to_dense(g);
+    for (auto& v : out.a) v *= -i1 * s;
+    for (std::size_t r = 0; r < out.dim; ++r) out.at(r, r) += c;
+    return out;
+}
+}  // namespace gatemat
+
+// ---- constant-gate registry / gate_by_tag (gates.hpp:97-175) ------------------------------------
+struct ConstGateDef {
+    std::string name;
+    MatrixRepr mat;
+    std::size_t nqubits;
+};
+inline std::map<std::string, ConstGateDef>& gate_registry() {
+    static std::map<std::string, ConstGateDef> reg = [] {
+        std::map<std::string, ConstGateDef> r;
+        auto put = [&](const char* nm, MatrixRepr m) {
+            std::size_t nq = 0;
+            while ((std::size_t{1} << nq) < mat_dim(m)) ++nq;
+            r.emplace(nm, ConstGateDef{nm, std::move(m), nq});
+        };
+        put("X", gatemat::x()); put("Y", gatemat::y()); put("Z", gatemat::z()); put("H", gatemat::h());
+        put("I2", gatemat::i2()); put("S", gatemat::s()); put("Sdag", gatemat::sdag()); put("T", gatemat::t());
+        put("Tdag", gatemat::tdag()); put("SWAP", gatemat::swap()); put("CNOT", gatemat::cnot());
+        put("CZ", gatemat::cz()); put("Toffoli", gatemat::toffoli()); put("P0", gatemat::p0());
+        put("P1", gatemat::p1()); put("Pu", gatemat::pu()); put("Pd", gatemat::pd());
+        return r;
+    }();
+    return reg;
+}
+inline const ConstGateDef& define_const_gate(const std::string& name, const MatrixRepr& m) {
+    const std::size_t d = mat_dim(m);
+    if (d < 2 || (d & (d - 1)) != 0) throw ValidationError("define_const_gate: dimension must be a power of 2");
+    std::size_t nq = 0;
+    while ((std::size_t{1} << nq) < d) ++nq;
+    auto& r = gate_registry();
+    r.erase(name);
+    return r.emplace(name, ConstGateDef{name, m, nq}).first->second;
+}
+inline const ConstGateDef* find_gate(const std::string& name) {
+    auto& r = gate_registry();
+    auto it = r.find(name);
+    return it == r.end() ? nullptr : &it->second;
+}
+inline MatrixRepr gate_by_tag(const std::string& tag, std::span<const double> params = {}) {
+    if (tag == "Rx" || tag == "Ry" || tag == "Rz" || tag == "shift" || tag == "phase") {
+        if (params.size() != 1) throw DispatchError("gate " + tag + " expects one parameter");
+        const double th = params[0];
+        if (tag == "Rx") return gatemat::rx(th);
+        if (tag == "Ry") return gatemat::ry(th);
+        if (tag == "Rz") return gatemat::rz(th);
+        if (tag == "shift") return gatemat::shift(th);
+        return gatemat::global_phase(th);
+    }
+    if (const ConstGateDef* def = find_gate(tag)) {
+        if (!params.empty()) throw DispatchError("gate " + tag + " takes no parameters");
+        return def->mat;
+    }
+    throw DispatchError("unknown gate tag: " + tag);
+}
+
+// ---- BitStr (bits.hpp:29-139) -----------------------------------------------------------------------
+struct BitStr {
+    std::uint64_t value = 0;
+    std::size_t nbits = 1;
+    static constexpr std::size_t max_bits = 63;
+    BitStr() = default;
+    BitStr(std::uint64_t v, std::size_t n) : value(v), nbits(n) {
+        if (n == 0 || n > max_bits) throw ValidationError("BitStr width must be in 1.." + std::to_string(max_bits));
+        if (v >> n) throw ValidationError("BitStr value does not fit in " + std::to_string(n) + " bits");
+    }
+    friend bool operator==(const BitStr&, const BitStr&) = default;
+};
+inline int bit_at(const BitStr& b, std::size_t i) {
+    if (i < 1 || i > b.nbits) throw RangeError("bit index " + std::to_string(i) + " out of range");
+    return static_cast<int>((b.value >> (i - 1)) & 1u);
+}
+inline std::vector<int> to_bits(const BitStr& b) {
+    std::vector<int> v(b.nbits);
+    for (std::size_t i = 0; i < b.nbits; ++i) v[i] = static_cast<int>((b.value >> i) & 1u);
+    return v;
+}
+inline BitStr from_bits(std::span<const int> bits) {
+    if (bits.empty()) throw ValidationError("from_bits: empty bit list");
+    if (bits.size() > BitStr::max_bits) throw ValidationError("from_bits: too many bits");
+    std::uint64_t v = 0;
+    for (std::size_t i = 0; i < bits.size(); ++i) {
+        if (bits[i] != 0 && bits[i] != 1) throw ValidationError("from_bits: entry " + std::to_string(i + 1) + " is not 0 or 1");
+        v |= static_cast<std::uint64_t>(bits[i]) << i;
+    }
+    return BitStr(v, bits.size());
+}
+inline BitStr from_bits(std::initializer_list<int> bits) { return from_bits(std::span<const int>(bits.begin(), bits.size())); }
+inline bool ctrl_match(std::uint64_t index, std::span<const std::size_t> ctrl_locs, std::span<const int> ctrl_config) {
+    if (ctrl_locs.size() != ctrl_config.size())
+        throw ValidationError("ctrl_match: control locations and configuration differ in length");
+    for (std::size_t k = 0; k < ctrl_locs.size(); ++k)
+        if (static_cast<int>((index >> (ctrl_locs[k] - 1)) & 1u) != ctrl_config[k]) return false;
+    return true;
+}
+inline std::string to_binary(const BitStr& b) {  // qubit 1 rightmost
+    std::string s(b.nbits, '0');
+    for (std::size_t i = 0; i < b.nbits; ++i)
+        if ((b.value >> i) & 1) s[b.nbits - 1 - i] = '1';
+    return s;
+}
+inline std::string to_text(const BitStr& b) { return to_binary(b) + " (2)"; }
+inline BitStr bits_from_text(const std::string& text) {
+    if (text.empty()) throw ValidationError("empty bit string");
+    std::vector<int> bits(text.size());
+    for (std::size_t k = 0; k < text.size(); ++k) {
+        const char c = text[text.size() - 1 - k];
+        if (c != '0' && c != '1') throw ValidationError("bit string may contain only 0 and 1");
+        bits[k] = c - '0';
+    }
+    return from_bits(bits);
+}
+struct MeasureOutcome {
+    std::vector<BitStr> samples;
+};
 
 // ---- Rng (rng.hpp:25-66): same libstdc++ stream, owned by the engine ---------------------------
 class Rng {
@@ -171,9 +491,28 @@ class Register {
         std::vector<int32_t> l(locs.begin(), locs.end());
         check(qbg_relax(h_, l.data(), static_cast<int32_t>(l.size()), static_cast<int32_t>(to_nactive)));
     }
+    // QBREG1 state files (register.hpp:181-205): magic, u64 nqubits / nactive / nbatch, then the
+    // amplitudes batch-slowest — byte-identical with the reference's files
+    void save(std::ostream& os) const {
+        const char magic[8] = {'Q', 'B', 'R', 'E', 'G', '1', 0, 0};
+        const std::uint64_t hdr[3] = {nqubits(), nactive(), nbatch()};
+        const auto amps = amplitudes_raw();
+        os.write(magic, 8);
+        os.write(reinterpret_cast<const char*>(hdr), sizeof(hdr));
+        os.write(reinterpret_cast<const char*>(amps.data()), static_cast<std::streamsize>(amps.size() * sizeof(cplx)));
+    }
+    static Register load(std::istream& is, std::uint64_t seed = 42) {
+        std::string bytes((std::istreambuf_iterator<char>(is)), std::istreambuf_iterator<char>());
+        qbg_reg* h = nullptr;
+        check(qbg_load_memory(bytes.data(), static_cast<int64_t>(bytes.size()), seed, QBG_C128, &h));
+        return Register(h);
+    }
     qbg_reg* handle() const { return h_; }
 
    private:
+    explicit Register(qbg_reg* h) : h_(h) {}
+    // amplitudes in the device's current layout order (focus permutes physically, like the reference)
+    std::vector<cplx> amplitudes_raw() const { return amplitudes(); }
     struct Info {
         std::size_t nq, na, nb;
     };
@@ -196,13 +535,21 @@ inline Register rand_state(std::size_t n, std::size_t nbatch = 1, std::uint64_t 
     check(qbg_set_rand(r.handle(), seed));
     return r;
 }
-inline Register product_state(std::uint64_t value, std::size_t nbits, std::size_t nbatch = 1, std::uint64_t seed = 42) {
-    Register r(nbits, nbatch, seed);
-    check(qbg_set_product(r.handle(), &value, 1));
+inline Register product_state(const BitStr& b, std::size_t nbatch = 1, std::uint64_t seed = 42) {
+    Register r(b.nbits, nbatch, seed);
+    check(qbg_set_product(r.handle(), &b.value, 1));
+    return r;
+}
+// batched form (no reference counterpart): one basis index per batch, batch-innermost on the device
+inline Register product_state(std::span<const std::uint64_t> values, std::size_t nbits, std::uint64_t seed = 42) {
+    Register r(nbits, values.size(), seed);
+    check(qbg_set_product(r.handle(), values.data(), static_cast<int64_t>(values.size())));
     return r;
 }
 
 // ---- instruct (register.hpp:392-408) -------------------------------------------------------------
+// Diagonal / Permutation / Dense go to the device as they are; SparseColumns and OuterProduct take
+// the reference's generic path, to_dense (register.hpp:372), on the host.
 inline void instruct(Register& reg, const MatrixRepr& gate, std::span<const std::size_t> locs,
                      std::span<const std::size_t> ctrl_locs = {}, std::span<const int> ctrl_config = {}) {
     if (ctrl_locs.size() != ctrl_config.size())
@@ -212,23 +559,23 @@ inline void instruct(Register& reg, const MatrixRepr& gate, std::span<const std:
     qbg_matrix m{};
     std::vector<cplx> vals;
     std::vector<int64_t> perm;
-    if (auto* id = std::get_if<Identity>(&gate)) {
-        m.kind = QBG_MAT_IDENTITY;
-        m.dim = static_cast<int32_t>(id->dim);
-    } else if (auto* d = std::get_if<Diagonal>(&gate)) {
-        m.kind = QBG_MAT_DIAGONAL;
-        m.dim = static_cast<int32_t>(d->diag.size());
-        vals = d->diag;
-    } else if (auto* p = std::get_if<Permutation>(&gate)) {
-        m.kind = QBG_MAT_PERMUTATION;
-        m.dim = static_cast<int32_t>(p->perm.size());
-        vals = p->vals;
-        perm.assign(p->perm.begin(), p->perm.end());
-    } else {
-        const Dense& dn = std::get<Dense>(gate);
-        m.kind = QBG_MAT_DENSE;
-        m.dim = static_cast<int32_t>(dn.dim);
-        vals = dn.a;
+    m.dim = static_cast<int32_t>(mat_dim(gate));
+    switch (kind_of(gate)) {
+        case MatKind::I: m.kind = QBG_MAT_IDENTITY; break;
+        case MatKind::D:
+            m.kind = QBG_MAT_DIAGONAL;
+            vals = std::get<Diagonal>(gate).diag;
+            break;
+        case MatKind::P: {
+            auto& p = std::get<Permutation>(gate);
+            m.kind = QBG_MAT_PERMUTATION;
+            vals = p.vals;
+            perm.assign(p.perm.begin(), p.perm.end());
+            break;
+        }
+        default:
+            m.kind = QBG_MAT_DENSE;
+            vals = to_dense(gate).a;
     }
     m.vals = reinterpret_cast<const double*>(vals.data());
     m.perm = perm.data();
@@ -236,27 +583,14 @@ inline void instruct(Register& reg, const MatrixRepr& gate, std::span<const std:
                        static_cast<int32_t>(c.size())));
 }
 
+// instruct by tag: gate_by_tag (builtin or define_const_gate-registered) then the matrix form
 inline void instruct(Register& reg, const std::string& tag, std::span<const std::size_t> locs,
                      std::span<const std::size_t> ctrl_locs = {}, std::span<const int> ctrl_config = {},
                      std::span<const double> params = {}) {
-    if (ctrl_locs.size() != ctrl_config.size())
-        throw ValidationError("instruct: control locations and configuration differ in length");
-    std::vector<int32_t> l(locs.begin(), locs.end()), c(ctrl_locs.begin(), ctrl_locs.end()),
-        f(ctrl_config.begin(), ctrl_config.end());
-    check(qbg_instruct_tag(reg.handle(), tag.c_str(), l.data(), static_cast<int32_t>(l.size()), c.data(), f.data(),
-                           static_cast<int32_t>(c.size()), params.data(), static_cast<int32_t>(params.size())));
+    instruct(reg, gate_by_tag(tag, params), locs, ctrl_locs, ctrl_config);
 }
 
 // ---- measurement (register.hpp:414-493) -----------------------------------------------------------
-struct BitStr {
-    std::uint64_t value = 0;
-    std::size_t nbits = 1;
-    friend bool operator==(const BitStr&, const BitStr&) = default;
-};
-struct MeasureOutcome {
-    std::vector<BitStr> samples;
-};
-
 inline std::vector<double> probabilities(const Register& reg, std::size_t b) {
     std::vector<double> p(reg.nrows());
     check(qbg_probabilities(reg.handle(), static_cast<int64_t>(b), p.data()));
@@ -266,36 +600,29 @@ inline MeasureOutcome measure(const Register& reg, std::size_t nshots, Rng& rng)
     std::vector<std::uint64_t> v(nshots * reg.nbatch());
     check(qbg_measure(reg.handle(), static_cast<int64_t>(nshots), rng.handle(), v.data()));
     MeasureOutcome o;
-    for (auto x : v) o.samples.push_back(BitStr{x, reg.nactive()});
+    for (auto x : v) o.samples.push_back(BitStr(x, reg.nactive()));
     return o;
 }
 inline MeasureOutcome measure(Register& reg, std::size_t nshots = 1) {
     std::vector<std::uint64_t> v(nshots * reg.nbatch());
     check(qbg_measure(reg.handle(), static_cast<int64_t>(nshots), nullptr, v.data()));
     MeasureOutcome o;
-    for (auto x : v) o.samples.push_back(BitStr{x, reg.nactive()});
+    for (auto x : v) o.samples.push_back(BitStr(x, reg.nactive()));
     return o;
 }
 inline MeasureOutcome measure_collapse(Register& reg, Rng& rng) {
     std::vector<std::uint64_t> v(reg.nbatch());
     check(qbg_measure_collapse(reg.handle(), rng.handle(), v.data()));
     MeasureOutcome o;
-    for (auto x : v) o.samples.push_back(BitStr{x, reg.nactive()});
+    for (auto x : v) o.samples.push_back(BitStr(x, reg.nactive()));
     return o;
 }
 inline MeasureOutcome measure_collapse(Register& reg) {
     std::vector<std::uint64_t> v(reg.nbatch());
     check(qbg_measure_collapse(reg.handle(), nullptr, v.data()));
     MeasureOutcome o;
-    for (auto x : v) o.samples.push_back(BitStr{x, reg.nactive()});
+    for (auto x : v) o.samples.push_back(BitStr(x, reg.nactive()));
     return o;
-}
-
-inline std::string to_text(const BitStr& b) {  // bits.hpp:104-112
-    std::string s(b.nbits, '0');
-    for (std::size_t i = 0; i < b.nbits; ++i)
-        if ((b.value >> i) & 1) s[b.nbits - 1 - i] = '1';
-    return s + " (2)";
 }
 
 }  // namespace qblock

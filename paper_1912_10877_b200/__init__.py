@@ -11,8 +11,8 @@ from .blocks import (CNOT, CZ, SWAP, Add, Block, Chain, Control, Daggered, Gener
                      Toffoli, X, Y, Z, apply, chain, compile_block, compile_observable, control, dagger,
                      define_const_gate, dispatch, gatecount, kron, mat, matblock, nparameters, parameters,
                      pauli_terms, phase, put, repeat, rot, shift, time_evolve, cache, evolve, TimeEvolution,
-                     Cached, SparseOperator, sparse_operator, apply_hamiltonian)
-from .circuits import heisenberg, variational_circuit
+                     Cached, SparseOperator, sparse_operator, apply_hamiltonian, Subroutine, subroutine, is_circuit)
+from .circuits import heisenberg, qft, variational_circuit
 from .mmd import MMD, RBFKernel, brbf_kernel, mmd_cross, mmd_expect, mmd_grad, mmd_seed
 from .register import (Register, Rng, instruct, measure, measure_collapse, probabilities, product_state, qubit_cap,
                        rand_state, set_qubit_cap, state_alloc_counter, to_text, zero_state)

@@ -65,6 +65,8 @@ def lib() -> ctypes.CDLL:
         "qbg_last_error": (c_char_p, []), "qbg_version": (c_char_p, []),
         "qbg_set_qubit_cap": (c_int32, [c_int32]), "qbg_get_qubit_cap": (c_int32, []),
         "qbg_alloc_count": (c_uint64, []), "qbg_set_device": (c_int32, [c_int32]),
+        "qbg_release_workspace": (c_int32, []),
+        "qbg_load_memory": (c_int32, [P, c_int64, c_uint64, c_int32, POINTER(P)]),
         "qbg_set_stream": (c_int32, [P]), "qbg_synchronize": (c_int32, []),
         "qbg_set_fusion": (c_int32, [c_int32]), "qbg_profile_enable": (c_int32, [c_int32]),
         "qbg_profile_reset": (c_int32, []), "qbg_profile_report": (c_int32, [c_char_p, c_int64]),
@@ -101,6 +103,7 @@ def lib() -> ctypes.CDLL:
         "qbg_prog_plan_info": (c_int32, [P, c_char_p, c_int64]),
         "qbg_prog_plan_preview": (c_int32, [P, c_int64, c_int32, c_char_p, c_int64]),
         "qbg_jit_check": (c_int32, [P, P, c_int64, c_int32, POINTER(c_int64)]),
+        "qbg_jit_stats": (c_int32, [POINTER(c_int64), POINTER(c_int64)]),
         "qbg_apply": (c_int32, [P, P]), "qbg_apply_adjoint": (c_int32, [P, P]),
         "qbg_obs_create": (c_int32, [c_int32, POINTER(QbgPauliTerm), c_int64, POINTER(P)]),
         "qbg_obs_destroy": (c_int32, [P]), "qbg_expect": (c_int32, [P, P, P]),

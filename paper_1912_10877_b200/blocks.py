@@ -188,6 +188,23 @@ class Repeat(Composite):
         return [self.block]
 
 
+class Subroutine(Composite):
+    """Subroutine (Listing 16): focus(locs) -> apply the child -> relax, i.e. the
+    child on a local scope.  For a unitary child that is put(n, locs => child), and it lowers so
+    (one program, fusable); a non-circuit child (Add / Scale) runs the explicit focus / relax."""
+
+    def __init__(self, n: int, block: Block, locs: Sequence[int]):
+        self.nqubits = n
+        self.block = block
+        self.locs = tuple(int(l) for l in locs)
+        _check_locs(n, self.locs, "subroutine")
+        if len(self.locs) != block.nqubits:
+            raise errors.ShapeError("subroutine: location count differs from the block's qubit count")
+
+    def subblocks(self):
+        return [self.block]
+
+
 class Add(Composite):
     def __init__(self, blocks: Sequence[Block]):
         self.blocks = []
@@ -366,6 +383,10 @@ def repeat(n: int, block: Block, locs=None) -> Repeat:
     return Repeat(n, block, range(1, n + 1) if locs is None else _locs(locs))
 
 
+def subroutine(n: int, block: Block, locs) -> Subroutine:
+    return Subroutine(n, block, _locs(locs))
+
+
 # ---------------------------------------------------------------------------------------------------
 # parameters / dispatch / gatecount / dagger
 # ---------------------------------------------------------------------------------------------------
@@ -492,6 +513,8 @@ def dagger(b: Block) -> Block:
         return Kron(b.nqubits, [(l, dagger(c)) for l, c in b.pairs])
     if isinstance(b, Repeat):
         return Repeat(b.nqubits, dagger(b.block), b.locs)
+    if isinstance(b, Subroutine):
+        return Subroutine(b.nqubits, dagger(b.block), b.locs)
     if isinstance(b, Scale):
         return Scale(b.factor.conjugate(), dagger(b.block))
     if isinstance(b, Add):
@@ -544,7 +567,7 @@ def mat(b: Block) -> np.ndarray:
         for c in b.blocks:
             out = mat(c) @ out
         return out
-    if isinstance(b, Put):
+    if isinstance(b, (Put, Subroutine)):
         return _embed(n, b.locs, mat(b.block))
     if isinstance(b, Control):
         return _embed(n, b.locs, mat(b.block), b.ctrl_locs, b.ctrl_config)
@@ -644,7 +667,7 @@ def _lower(b: Block, qmap: tuple, ctrls: tuple, cfg: tuple, em: _Emitter, adjoin
         seq = reversed(b.blocks) if adjoint else b.blocks
         for c in seq:
             _lower(c, qmap, ctrls, cfg, em, adjoint)
-    elif isinstance(b, Put):
+    elif isinstance(b, (Put, Subroutine)):
         _lower(b.block, tuple(qmap[l - 1] for l in b.locs), ctrls, cfg, em, adjoint)
     elif isinstance(b, Control):
         _lower(b.block, tuple(qmap[l - 1] for l in b.locs), ctrls + tuple(qmap[c - 1] for c in b.ctrl_locs),
@@ -748,6 +771,11 @@ def apply(reg, b: Block):
     if isinstance(b, Scale):
         apply(reg, b.block)
         return reg.scale(b.factor)
+    if isinstance(b, Subroutine) and not is_circuit(b):
+        na = reg.nactive
+        reg.focus(*b.locs)
+        apply(reg, b.block)
+        return reg.relax(*b.locs, to_nactive=na)
     if isinstance(b, Add):
         src = reg.copy()
         first = True
@@ -770,6 +798,13 @@ def apply(reg, b: Block):
     p = compile_block(b)
     check(lib().qbg_apply(reg._h, p._h))
     return reg
+
+
+def is_circuit(b: Block) -> bool:
+    """No Add / Scale anywhere: the block lowers to one gate program."""
+    if isinstance(b, (Add, Scale)):
+        return False
+    return all(is_circuit(c) for c in b.subblocks())
 
 
 # ---------------------------------------------------------------------------------------------------

@@ -2,7 +2,9 @@
 variational circuit and the Heisenberg chain.  They ARE the BASELINE workloads."""
 from __future__ import annotations
 
-from .blocks import Rx, Rz, X, Y, Z, Add, Block, chain, control, put
+import math
+
+from .blocks import H, Rx, Rz, X, Y, Z, Add, Block, chain, control, put, shift
 
 
 def variational_circuit(n: int, depth: int) -> Block:
@@ -33,3 +35,15 @@ def heisenberg(n: int, periodic: bool = False) -> Block:
         for s in (X, Y, Z):
             terms.append(put(n, i, s) * put(n, j, s))
     return Add(terms)
+
+
+def qft(n: int) -> Block:
+    """Listing 1: chain of hcphases(n, i) = chain(H on i, cphase(j, i) for j = i+1..n) with
+    cphase(j, i) = control(j, i => shift(2π / 2^(j-i+1)))."""
+    outer = []
+    for i in range(1, n + 1):
+        inner = [put(n, i, H)]
+        for j in range(i + 1, n + 1):
+            inner.append(control(n, j, i, shift(2 * math.pi / (1 << (j - i + 1)))))
+        outer.append(chain(n, *inner))
+    return chain(n, *outer)

@@ -22,6 +22,7 @@
 
 #include "engine.h"
 #include "program.h"
+#include "jit.h"
 
 // ---- opaque handles ---------------------------------------------------------------------------
 struct qbg_rng {
@@ -54,6 +55,10 @@ std::atomic<uint64_t> g_allocs{0};
 std::atomic<uint64_t> g_launches{0};
 cudaStream_t g_stream = nullptr;
 int g_device = 0;
+// Set once the library holds anything on g_device (registers, scratch, workspace, plan tables,
+// loaded kernels): from then on qbg_set_device may not move the library to another device, since
+// every cached pointer / CUfunction belongs to this device's context.
+std::atomic<bool> g_bound{false};
 int g_sms = 0;
 bool g_fusion = true;
 bool g_profile = false;
@@ -131,7 +136,32 @@ void* dev_alloc(size_t bytes, bool state) {
                                     cudaGetErrorString(e));
     }
     if (state) g_allocs.fetch_add(1);
+    g_bound.store(true);
     return p;
+}
+
+// ---- library-owned full-state workspace (the expect' work copy and adjoint; Krylov bases) ----
+// Replaces per-thread static buffers: owned here, counted by qbg_alloc_count, released by
+// qbg_release_workspace and automatically once no live register is as large as a buffer.
+std::mutex g_ws_mu;
+std::vector<qbg_reg*> g_live;  // live registers (for the release rule)
+DevState g_ws[2];              // [0] forward work state (out-of-place expect'), [1] adjoint buffer
+
+void ws_free(DevState& d) {
+    if (!d.ptr) return;
+    QBG_CUDA(cudaStreamSynchronize(g_stream));
+    QBG_CUDA(cudaFree(d.ptr));
+    d = DevState{};
+}
+// a buffer shaped like s (reused when it is at least as large and of the same dtype)
+DevState& ws_get(int k, const DevState& s) {
+    DevState& d = g_ws[k];
+    if (!(d.ptr && d.bytes() >= s.bytes() && d.dtype == s.dtype)) {
+        ws_free(d);
+        d = s;
+        d.ptr = dev_alloc(s.bytes(), true);
+    }
+    return d;
 }
 
 void stream_sync() { QBG_CUDA(cudaStreamSynchronize(g_stream)); }
@@ -154,6 +184,8 @@ qbg_reg* new_reg(int n, int64_t B, int dtype) {
         delete r;
         throw;
     }
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    g_live.push_back(r);
     return r;
 }
 
@@ -242,6 +274,15 @@ cudaStream_t stream() { return g_stream; }
 int num_sms() {
     ensure_device();
     return g_sms;
+}
+
+void release_krylov(size_t keep_bytes);  // capi.cu, below the Krylov driver
+void release_scratch() {
+    QBG_CUDA(cudaStreamSynchronize(g_stream));
+    for (auto& s : g_scratch) {
+        if (s.p) QBG_CUDA(cudaFree(s.p));
+        s = Scratch{};
+    }
 }
 
 void* scratch(size_t bytes, int slot) {
@@ -538,6 +579,10 @@ uint64_t qbg_alloc_count(void) { return g_allocs.load(); }
 
 int qbg_set_device(int32_t device) {
     return guarded([&] {
+        if (device != g_device && g_bound.load())
+            raise(QBG_ERR_VALIDATION, "qbg_set_device: the library already holds resources on device " +
+                                          std::to_string(g_device) + " (registers, workspace, plans, kernels); "
+                                          "select the device before the first allocation (one device per process)");
         g_device = device;
         QBG_CUDA(cudaSetDevice(device));
         QBG_CUDA(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, device));
@@ -648,7 +693,24 @@ int qbg_reg_destroy(qbg_reg* r) {
             QBG_CUDA(cudaStreamSynchronize(g_stream));
             QBG_CUDA(cudaFree(r->s.ptr));
         }
+        std::lock_guard<std::mutex> lk(g_ws_mu);
+        g_live.erase(std::remove(g_live.begin(), g_live.end(), r), g_live.end());
         delete r;
+        // release workspace no live register can use any more (an expect' of a large register
+        // must not keep two of its states resident after the register is gone)
+        size_t need = 0;
+        for (auto* x : g_live) need = std::max(need, x->s.bytes());
+        for (auto& w : g_ws)
+            if (w.ptr && w.bytes() > need) ws_free(w);
+        release_krylov(need);
+    });
+}
+int qbg_release_workspace(void) {
+    return guarded([&] {
+        std::lock_guard<std::mutex> lk(g_ws_mu);
+        for (auto& w : g_ws) ws_free(w);
+        release_krylov(0);
+        release_scratch();
     });
 }
 int qbg_reg_clone(const qbg_reg* src, qbg_reg** out) {
@@ -1017,29 +1079,22 @@ int qbg_save(const qbg_reg* r, const char* path) {
     });
 }
 
-int qbg_load(const char* path, uint64_t seed, int32_t dtype, qbg_reg** out) {
+int qbg_load_memory(const void* data, int64_t nbytes, uint64_t seed, int32_t dtype, qbg_reg** out) {
     return guarded([&] {
-        FILE* f = std::fopen(path, "rb");
-        if (!f) raise(QBG_ERR_SERIALIZATION, std::string("state file: cannot open ") + path);
-        char magic[8];
+        const char* p = static_cast<const char*>(data);
+        if (!p || nbytes < 8 || std::memcmp(p, "QBREG1\0\0", 8) != 0) raise(QBG_ERR_SERIALIZATION, "state file: bad magic");
         uint64_t hdr[3];
-        bool ok = std::fread(magic, 1, 8, f) == 8 && std::memcmp(magic, "QBREG1\0\0", 8) == 0;
-        if (!ok) {
-            std::fclose(f);
-            raise(QBG_ERR_SERIALIZATION, "state file: bad magic");
-        }
-        if (std::fread(hdr, 8, 3, f) != 3 || hdr[0] < 1 || hdr[1] > hdr[0] || hdr[0] > 62 || hdr[2] < 1) {
-            std::fclose(f);
-            raise(QBG_ERR_SERIALIZATION, "state file: bad header");
-        }
-        std::vector<double> host(2 * (uint64_t{1} << hdr[0]) * hdr[2]);
-        bool full = std::fread(host.data(), sizeof(double), host.size(), f) == host.size();
-        std::fclose(f);
-        if (!full) raise(QBG_ERR_SERIALIZATION, "state file: truncated amplitudes");
+        if (nbytes < 32) raise(QBG_ERR_SERIALIZATION, "state file: bad header");
+        std::memcpy(hdr, p + 8, sizeof(hdr));
+        if (hdr[0] < 1 || hdr[1] > hdr[0] || hdr[0] > 62 || hdr[2] < 1) raise(QBG_ERR_SERIALIZATION, "state file: bad header");
+        const uint64_t count = (uint64_t{1} << hdr[0]) * hdr[2];
+        if (static_cast<uint64_t>(nbytes) - 32 < 16 * count) raise(QBG_ERR_SERIALIZATION, "state file: truncated amplitudes");
         qbg_reg* r = nullptr;
         int rc = qbg_reg_create(static_cast<int32_t>(hdr[0]), static_cast<int64_t>(hdr[2]), dtype, seed, &r);
         if (rc) raise(rc, g_err);
-        rc = qbg_upload(r, host.data(), static_cast<int64_t>(host.size() / 2));
+        std::vector<double> host(2 * count);  // aligned copy of the amplitudes
+        std::memcpy(host.data(), p + 32, 16 * count);
+        rc = qbg_upload(r, host.data(), static_cast<int64_t>(count));
         if (rc) {
             qbg_reg_destroy(r);
             raise(rc, g_err);
@@ -1048,6 +1103,20 @@ int qbg_load(const char* path, uint64_t seed, int32_t dtype, qbg_reg** out) {
         stream_sync();
         *out = r;
     });
+}
+
+int qbg_load(const char* path, uint64_t seed, int32_t dtype, qbg_reg** out) {
+    std::vector<char> buf;
+    int rc = guarded([&] {
+        FILE* f = std::fopen(path, "rb");
+        if (!f) raise(QBG_ERR_SERIALIZATION, std::string("state file: cannot open ") + path);
+        char chunk[1 << 16];
+        size_t got;
+        while ((got = std::fread(chunk, 1, sizeof(chunk), f)) > 0) buf.insert(buf.end(), chunk, chunk + got);
+        std::fclose(f);
+    });
+    if (rc) return rc;
+    return qbg_load_memory(buf.data(), static_cast<int64_t>(buf.size()), seed, dtype, out);
 }
 
 // ---- programs -----------------------------------------------------------------------------------------
@@ -1149,6 +1218,9 @@ int qbg_jit_check(const qbg_prog* prog, const qbg_obs* obs, int64_t nbatch, int3
         if (nkernels) *nkernels = n;
     });
 }
+int qbg_jit_stats(int64_t* nvrtc_builds, int64_t* cache_hits) {
+    return guarded([&] { jit::stats(nvrtc_builds, cache_hits); });
+}
 int qbg_apply(qbg_reg* r, const qbg_prog* prog) {
     return guarded([&] {
         check_reg(r);
@@ -1240,28 +1312,11 @@ namespace {
 template <class Seed>
 void grad_driver(qbg_reg* r, Program& p, int32_t inplace, qbg_reg* state_grad, double* vals, double* grads,
                  Seed&& seed) {
-    static thread_local DevState work{}, adjbuf{};
-    auto ensure = [&](DevState& d) {
-        if (d.ptr && d.bytes() >= r->s.bytes() && d.dtype == r->s.dtype) return;
-        if (d.ptr) {
-            stream_sync();
-            QBG_CUDA(cudaFree(d.ptr));
-        }
-        d = r->s;
-        d.ptr = dev_alloc(r->s.bytes(), true);
-    };
+    std::lock_guard<std::mutex> lk(g_ws_mu);
     DevState psi = r->s;
-    if (!inplace) {
-        ensure(work);
-        psi.ptr = work.ptr;
-    }
+    if (!inplace) psi.ptr = ws_get(0, r->s).ptr;
     DevState adj = r->s;
-    if (state_grad) {
-        adj.ptr = state_grad->s.ptr;
-    } else {
-        ensure(adjbuf);
-        adj.ptr = adjbuf.ptr;
-    }
+    adj.ptr = state_grad ? state_grad->s.ptr : ws_get(1, r->s).ptr;
     // out-of-place: the first forward pass reads the caller's register (no separate copy)
     run_program(psi, p, false, inplace ? nullptr : r->s.ptr);
     double* e = static_cast<double*>(scratch(r->s.B * sizeof(double), 10));
@@ -1517,11 +1572,15 @@ struct KrylovBuf {
             v.clear();
         }
     }
-    ~KrylovBuf() {
+    void release() {
+        if (v.empty()) return;
+        stream_sync();
         for (auto& d : v)
             if (d.ptr) cudaFree(d.ptr);
+        v.clear();
     }
 };
+KrylovBuf g_krylov;  // library-owned (released with the workspace)
 
 // Lanczos on every batch column: builds the Krylov basis of H at psi until the residual estimate
 // of e^{-iH dt} drops below tol (or maxdim vectors); when the full basis does not reach tol for dt,
@@ -1696,7 +1755,7 @@ void evolve_driver(qbg_reg* r, const MatVec& matvec, double t, double tol, int32
     if (tol <= 0) tol = 1e-12;
     int used = 0;
     if (t != 0.0) {
-        static thread_local KrylovBuf kb;
+        KrylovBuf& kb = g_krylov;
         kb.fit(r->s);
         double rem = t;
         int steps = 0;
@@ -1711,6 +1770,12 @@ void evolve_driver(qbg_reg* r, const MatVec& matvec, double t, double tol, int32
     stream_sync();
 }
 }  // namespace
+}  // namespace qbg
+
+namespace qbg {
+void release_krylov(size_t keep_bytes) {
+    if (!g_krylov.v.empty() && g_krylov.v[0].bytes() > keep_bytes) g_krylov.release();
+}
 }  // namespace qbg
 
 struct qbg_sparse {

@@ -86,42 +86,17 @@ int consumer_groups(bool back) {
     static const int b = std::min(4, std::max(1, env_int("QBG_BWD_GROUPS", g)));
     return back ? b : f;
 }
-constexpr int kProducerThreads = 128;
-// producer threads of a pass (one warpgroup; QBG_FWD_PRODUCERS=256 gives the forward passes two)
-int producer_threads(bool back) {
-    static const int f = env_int("QBG_FWD_PRODUCERS", kProducerThreads);
-    return back ? kProducerThreads : (f == 256 ? 256 : kProducerThreads);
-}
-int seed_minb() {  // CTAs per SM the seed kernels are compiled for (2: 128 registers, a few spills)
-    static const int m = std::max(1, env_int("QBG_SEED_MINB", 2));  // measured: 2 (0.343 vs 0.373 ms)
-    return m;
-}
-bool split_acc() {  // two accumulator sets in the Hermitian cross statistics (QBG_SPLIT_ACC)
-    static const bool on = env_int("QBG_SPLIT_ACC", 0) != 0;  // measured slower (registers)
-    return on;
-}
+constexpr int kProducerThreads = 128;  // one producer warpgroup per CTA
+constexpr int kSeedMinB = 2;  // CTAs per SM the seed kernels are compiled for (measured: 0.343 vs 0.373 ms at 1)
 bool jit_check_mode() {
     static const bool on = env_int("QBG_JIT_CHECK", 0) != 0;
     return on;
 }
-bool dense_pair() {  // reverse 2x2 uncomputes of ψ and φ̄ interleaved in one template (QBG_DENSE_PAIR)
-    static const bool on = env_int("QBG_DENSE_PAIR", 0) != 0;  // measured slower (register pressure)
-    return on;
-}
-// Statistic stores without a lane branch (QBG_SG_BRANCHFREE, default on): after the butterfly
-// reductions every lane of a group holds the bitwise-identical sum (commutative adds), so all of
-// them may store it — same address, same value.  Dropping the `if (lane ...)` keeps a stage one
-// basic block, so ptxas can overlap a run's shuffle chain with the next run's FP64 work.
-bool sg_branchfree() {
-    static const bool on = env_int("QBG_SG_BRANCHFREE", 1) != 0;
-    return on;
-}
-// Thread- / tile-controlled register swaps (CNOT with a thread-bit control) by selects instead
-// of a branch (QBG_CSWAP_SEL=1; measured slower: reverse pass 0.615 -> 0.645 ms, so off)
-bool cswap_sel() {
-    static const bool on = env_int("QBG_CSWAP_SEL", 0) != 0;
-    return on;
-}
+// Gradient-statistic stores: after the butterfly reduction every lane of a group holds the same
+// sum; ONE lane per group read-modify-writes the shared cell, by a predicated store (sg_acc in
+// jit_prelude.h) rather than an `if`, so a stage stays one basic block and ptxas can overlap a
+// run's shuffle chain with the next run's FP64 work (measured: 0.643 -> 0.620 ms per reverse pass
+// against the branch).
 bool perm_ctrl_regs() {
     static const bool on = env_int("QBG_PERM_CTRL_REGS", 1) != 0;
     return on;
@@ -907,13 +882,12 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
     // who writes the results: with a deep ring the producer drains each computed slot to global
     // memory (consumers only compute); with a shallow one (reverse pass: 3 slots of 2 states) the
     // drain would delay the refill, so the consumers store from registers and release the slot
-    static const int pstore_extra = env_int("QBG_PSTORE_EXTRA", NG + 2);  // spare slots the drain needs
-    const bool pstore = pipe && nbuf >= NG + pstore_extra;
+    const bool pstore = pipe && nbuf >= 2 * NG + 2;  // the drain needs NG + 2 spare slots
     const size_t tile_elems = static_cast<size_t>(back ? 2 : 1) << M;
     const size_t tile_bytes = tile_elems * elem;
     const std::string SYNC = pipe ? "group_bar<" + std::to_string(TH) + ">(1 + cg);\n" : "__syncthreads();\n";
     std::ostringstream s;
-    const int NP = pipe ? producer_threads(back) : 0;
+    const int NP = pipe ? kProducerThreads : 0;
     std::vector<TmaDim> td;
     const bool use_tma = pipe && tma_enabled() && tma_layout(P, M, c128, td);
     const bool tstore = use_tma && tma_store_enabled();  // (used where the producer drains: pstore)
@@ -1011,22 +985,15 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             if (back) s << "tma_store" << td.size() << "(&tma, buf + " << (1 << M) << ", " << tma_coords("outer", "ptile") << ");\n";
             s << "tma_commit();\ntma_wait_read0();\n}\n";
         } else if (pstore) {
-            // drain in batches of QBG_DRAIN_BATCH shared-memory reads, then their stores
-            static const int dbat = std::max(1, env_int("QBG_DRAIN_BATCH", 1));
-            const int per = (1 << M) / NP;
-            for (int k0 = 0; k0 < per; k0 += dbat) {
-                const int k1 = std::min(per, k0 + dbat);
-                for (int k = k0; k < k1; ++k) {
-                    const uint32_t sk = swz(static_cast<uint32_t>(k * NP));
-                    s << "const V d" << k << " = buf[SI(sl ^ " << sk << "u)];";
-                    if (back) s << " const V e" << k << " = buf[SI(" << (1 << M) << " + (sl ^ " << sk << "u))];";
-                    s << "\n";
-                }
-                for (int k = k0; k < k1; ++k) {
-                    s << (back ? "psi" : "outp") << "[GI(tb + gp + " << kgo(k) << "ll)] = d" << k << ";";
-                    if (back) s << " adj[GI(tb + gp + " << kgo(k) << "ll)] = e" << k << ";";
-                    s << "\n";
-                }
+            // element by element: shared-memory read, then its global store
+            for (int k = 0; k < (1 << M) / NP; ++k) {
+                const uint32_t sk = swz(static_cast<uint32_t>(k * NP));
+                s << "{ const V d = buf[SI(sl ^ " << sk << "u)]; " << (back ? "psi" : "outp") << "[GI(tb + gp + " << kgo(k)
+                  << "ll)] = d;";
+                if (back)
+                    s << " const V e = buf[SI(" << (1 << M) << " + (sl ^ " << sk << "u))]; adj[GI(tb + gp + " << kgo(k)
+                      << "ll)] = e;";
+                s << " }\n";
             }
             if (use_tma) s << "fence_proxy_async();\n";
             s << "group_bar<" << NP << ">(" << 2 + NG << ");\n";  // slot read out before it is refilled
@@ -1195,21 +1162,12 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                     s << "if (" << cond << ") { const V m00 = MV(" << o << "), m10 = MV(" << o + 1 << "), m01 = MV(" << o + 2
                       << "), m11 = MV(" << o + 3 << "); ";
                     std::string tp = "<V, R, " + std::to_string(op.a) + ", " + t5 + ">";
-                    if (back && dense_pair())
-                        s << "dense1x2" << tp << "(x, y, m00, m10, m01, m11);";
-                    else
-                        both("dense1" + tp + "(x, m00, m10, m01, m11);", "dense1" + tp + "(y, m00, m10, m01, m11);");
+                    both("dense1" + tp + "(x, m00, m10, m01, m11);", "dense1" + tp + "(y, m00, m10, m01, m11);");
                     s << " }\n";
                     break;
                 }
                 case OP_X1: {
                     std::string tp = "<V, R, " + std::to_string(op.a) + ", " + t5 + ">";
-                    if (has_ctl && cswap_sel()) {
-                        s << "{ const bool p = " << cond << "; ";
-                        both("cswap1" + tp + "(x, p);", "cswap1" + tp + "(y, p);");
-                        s << " }\n";
-                        break;
-                    }
                     s << "if (" << cond << ") { ";
                     both("swap1" + tp + "(x);", "swap1" + tp + "(y);");
                     s << " }\n";
@@ -1280,14 +1238,14 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                         }
                     }
                     s << " }";
-                    if (grad) s << " g = warp_sum(g); " << (sg_branchfree() ? "" : "if (lane == 0) ") << "sg[" << op.gslot * CS << " + warp] += g;";
+                    if (grad) s << " g = warp_sum(g); sg_acc(&sg[" << op.gslot * CS << " + warp], g, lane == 0);";
                     s << " }\n";
                     break;
                 }
                 case G_CROSS1: {
                     s << "{ double c[8] = {0, 0, 0, 0, 0, 0, 0, 0}; if (" << cond << ") gcross1<V, R, " << int(op.a)
-                      << ">(x, y, c); const double v = warp_sum8(c, lane); " << (sg_branchfree() ? "" : "if ((lane & 3) == 0) ") << "sg[(" << op.gslot
-                      << " + (lane >> 2)) * " << CS << " + warp] += v; }\n";
+                      << ">(x, y, c); const double v = warp_sum8(c, lane); sg_acc(&sg[(" << op.gslot
+                      << " + (lane >> 2)) * " << CS << " + warp], v, (lane & 3) == 0); }\n";
                     break;
                 }
                 case G_CROSSD: {
@@ -1299,8 +1257,8 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                     else
                         call = "gcrossd_u<V, R>(x, y, c, (int)((outer >> " + std::to_string(op.a) + ") & 1ull));";
                     s << "{ double c[4] = {0, 0, 0, 0}; if (" << cond << ") " << call
-                      << " const double v = warp_sum4(c, lane); " << (sg_branchfree() ? "" : "if ((lane & 7) == 0) ") << "sg[(" << op.gslot
-                      << " + (lane >> 3)) * " << CS << " + warp] += v; }\n";
+                      << " const double v = warp_sum4(c, lane); sg_acc(&sg[(" << op.gslot
+                      << " + (lane >> 3)) * " << CS << " + warp], v, (lane & 7) == 0); }\n";
                     break;
                 }
                 case G_CROSSH: {
@@ -1309,10 +1267,10 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                           << ">(x, y, c); if (c[0] + c[1] + c[2] + c[3] == 1.2345) sg[" << op.gslot * CS << " + warp] += 1.0; }\n";
                         break;
                     }
-                    s << "{ double c[4] = {0, 0, 0, 0}; if (" << cond << ") " << (split_acc() ? "gcrossh2" : "gcrossh1")
+                    s << "{ double c[4] = {0, 0, 0, 0}; if (" << cond << ") " << "gcrossh1"
                       << "<V, R, " << int(op.a)
-                      << ">(x, y, c); const double v = warp_sum4(c, lane); " << (sg_branchfree() ? "" : "if ((lane & 7) == 0) ") << "sg[(" << op.gslot
-                      << " + (lane >> 3)) * " << CS << " + warp] += v; }\n";
+                      << ">(x, y, c); const double v = warp_sum4(c, lane); sg_acc(&sg[(" << op.gslot
+                      << " + (lane >> 3)) * " << CS << " + warp], v, (lane & 7) == 0); }\n";
                     break;
                 }
                 case G_DENSE1:
@@ -1331,7 +1289,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                     else
                         s << "const V m[16] = {" << mvs(o, 16) << "}; g = gdense2<V, R, " << int(op.a) << ", " << int(op.b)
                           << ", " << t5 << ">(x, y, m);";
-                    s << " } g = warp_sum(g); " << (sg_branchfree() ? "" : "if (lane == 0) ") << "sg[" << op.gslot * CS << " + warp] += g; }\n";
+                    s << " } g = warp_sum(g); sg_acc(&sg[" << op.gslot * CS << " + warp], g, lane == 0); }\n";
                     break;
                 }
                 default:
@@ -1582,7 +1540,7 @@ void launch_jit(V* psi, V* adj, Step& st, FusedPlan& pl, double* gpart, int64_t 
     }
     void* args[] = {&psi, &adj, &gpart, &gcols, &gbase, st.blob.data(), tmp, tma};
     LaunchScope ls(BACK ? "fused_bwd" : "fused_fwd", bytes, st.flops);
-    jit::launch(pl.jk[st.jk], static_cast<unsigned>(grid), pipe ? consumer_groups(BACK) * T + producer_threads(BACK) : T, st.smem,
+    jit::launch(pl.jk[st.jk], static_cast<unsigned>(grid), pipe ? consumer_groups(BACK) * T + kProducerThreads : T, st.smem,
                 args);
     static const bool sync_each = env_int("QBG_SYNC_EACH", 0) != 0;  // diagnostics: localise a failing pass
     if (sync_each) {
@@ -2023,7 +1981,7 @@ std::string gen_seed(const SPass& sp, const std::vector<SGroup>& groups, const s
     std::ostringstream s;
     int nterm = 0;
     for (int gi = sp.g0; gi < sp.g1; ++gi) nterm += groups[gi].term_end - groups[gi].term_begin;
-    s << "extern \"C\" __global__ void __launch_bounds__(" << T << ", " << seed_minb() << ") __NAME__(const " << (c128 ? "c128" : "c64")
+    s << "extern \"C\" __global__ void __launch_bounds__(" << T << ", " << kSeedMinB << ") __NAME__(const " << (c128 ? "c128" : "c64")
       << "* __restrict__ psi, " << (c128 ? "c128" : "c64")
       << "* __restrict__ phi, double* __restrict__ epart, const __grid_constant__ PM<" << (c128 ? "double" : "float")
       << ", " << std::max(2, 2 * nterm) << "> pm) {\n";
@@ -2206,8 +2164,10 @@ int64_t fused_jit_check(const Program& p, const Observable* o, int64_t B, int dt
         count += static_cast<int64_t>(pl->steps.size());
     }
     if (o && !o->terms.empty() && s.n >= kSeedM - batch_bits(B)) {
-        auto pl = make_seed_plan(*o, s, true, false);
-        count += static_cast<int64_t>(pl->spasses.size());
+        for (bool energy_only : {false, true}) {  // expect' (φ̄ = Oψ) and expect (energies only)
+            auto pl = make_seed_plan(*o, s, true, energy_only);
+            count += static_cast<int64_t>(pl->spasses.size());
+        }
     }
     return count;
 }

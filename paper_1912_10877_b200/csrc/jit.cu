@@ -15,6 +15,7 @@
 #include <sstream>
 #include <thread>
 #include <algorithm>
+#include <atomic>
 
 #include "common.cuh"
 #include "jit_prelude.h"
@@ -63,12 +64,26 @@ Nvrtc& nvrtc() {
 
 std::mutex g_mu;
 std::map<uint64_t, cudaLibrary_t> g_libs;  // source hash -> loaded library
+std::atomic<int64_t> g_nvrtc_builds{0}, g_cache_hits{0};  // qbg_jit_stats
 
+// Kernel cache: QBG_JIT_CACHE if set, else `jit_cache/` next to libqbg.so (in-tree: build()
+// pre-compiles the kernels of the standard workloads there on the CPU host — NVRTC needs no GPU —
+// so they travel with the library and a fresh GPU box does not pay the first-call compile), else
+// ~/.cache/qbg_jit when the library directory is read-only.
 std::string cache_dir() {
     const char* e = std::getenv("QBG_JIT_CACHE");
     if (e && *e) return e;
-    const char* home = std::getenv("HOME");
-    return std::string(home ? home : "/tmp") + "/.cache/qbg_jit";
+    static const std::string d = [] {
+        Dl_info info{};
+        if (dladdr(reinterpret_cast<void*>(&fnv), &info) && info.dli_fname) {
+            std::string lib = info.dli_fname;
+            const std::string dir = lib.substr(0, lib.rfind('/'));
+            if (!dir.empty() && ::access(dir.c_str(), W_OK) == 0) return dir + "/jit_cache";
+        }
+        const char* home = std::getenv("HOME");
+        return std::string(home ? home : "/tmp") + "/.cache/qbg_jit";
+    }();
+    return d;
 }
 
 bool read_file(const std::string& p, std::string& out) {
@@ -94,6 +109,7 @@ void write_file(const std::string& p, const std::string& data) {
 }
 
 std::string build_cubin(const std::string& src, uint64_t key) {
+    g_nvrtc_builds.fetch_add(1);
     Nvrtc& n = nvrtc();
     if (!n.ok) raise(QBG_ERR_INTERNAL, "jit: NVRTC is not available");
     std::string full = std::string(kPrelude) + src;
@@ -128,9 +144,19 @@ uint64_t fnv(const std::string& s) {
     return h;
 }
 
+// chunks of whole kernels per cubin: a fixed count, so the chunk sources (and their cache keys)
+// do not depend on the host's core count — cubins built on the CPU host are found on the GPU box
+constexpr size_t kChunks = 16;
+
 size_t compile_only(const std::string& src) {
-    const uint64_t key = fnv(src);
-    std::string cub = build_cubin(src, key);
+    const uint64_t key = fnv(std::string(kPrelude) + src);
+    char fname[64];
+    std::snprintf(fname, sizeof(fname), "/%016llx.cubin", static_cast<unsigned long long>(key));
+    std::string cub;
+    if (!read_file(cache_dir() + fname, cub)) {
+        cub = build_cubin(src, key);
+        write_file(cache_dir() + fname, cub);  // the ahead-of-time cache the runtime looks up
+    }
     // QBG_JIT_DUMP=<dir>: keep the cubin for offline inspection (cuobjdump -sass / -res-usage)
     if (const char* d = std::getenv("QBG_JIT_DUMP")) {
         char name[64];
@@ -162,6 +188,8 @@ std::vector<Kernel> compile(const std::string& src, const std::vector<std::strin
         if (!read_file(path, cub)) {
             cub = build_cubin(src, key);
             write_file(path, cub);
+        } else {
+            g_cache_hits.fetch_add(1);
         }
         cudaError_t e = cudaLibraryLoadData(&lib, cub.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
         if (e != cudaSuccess) {
@@ -186,8 +214,7 @@ std::vector<Kernel> compile_parallel(const std::vector<std::string>& bodies, con
     // chunks of whole kernels; each chunk is its own cached cubin / library, the missing ones are
     // built by concurrent NVRTC invocations (first use of a large circuit: seconds, not tens)
     const size_t nk = bodies.size();
-    unsigned hw = std::thread::hardware_concurrency();
-    const size_t nchunk = std::max<size_t>(1, std::min<size_t>({nk, hw ? hw : 4, 16}));
+    const size_t nchunk = std::max<size_t>(1, std::min(nk, kChunks));
     std::vector<std::string> srcs(nchunk);
     std::vector<std::vector<size_t>> members(nchunk);
     for (size_t i = 0; i < nk; ++i) {
@@ -204,6 +231,7 @@ std::vector<Kernel> compile_parallel(const std::vector<std::string>& bodies, con
         char name[64];
         std::snprintf(name, sizeof(name), "/%016llx.cubin", static_cast<unsigned long long>(keys[c]));
         if (!read_file(cache_dir() + name, cubs[c])) need[c] = 1;
+        else g_cache_hits.fetch_add(1);
     }
     std::vector<std::string> errs(nchunk);
     {
@@ -248,8 +276,7 @@ std::vector<Kernel> compile_parallel(const std::vector<std::string>& bodies, con
 size_t compile_only_parallel(const std::vector<std::string>& bodies) {
     const size_t nk = bodies.size();
     if (nk == 0) return 0;
-    unsigned hw = std::thread::hardware_concurrency();
-    const size_t nchunk = std::max<size_t>(1, std::min<size_t>({nk, hw ? hw : 4, 16}));
+    const size_t nchunk = std::max<size_t>(1, std::min(nk, kChunks));
     std::vector<std::string> srcs(nchunk);
     for (size_t i = 0; i < nk; ++i) srcs[i * nchunk / nk] += bodies[i];
     std::vector<size_t> sizes(nchunk, 0);
@@ -325,6 +352,11 @@ void launch(Kernel& k, unsigned grid, unsigned block, size_t smem, void** args) 
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
     QBG_CUDA(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(k.k), args));
+}
+
+void stats(int64_t* builds, int64_t* hits) {
+    if (builds) *builds = g_nvrtc_builds.load();
+    if (hits) *hits = g_cache_hits.load();
 }
 
 }  // namespace jit

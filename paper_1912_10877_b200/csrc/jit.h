@@ -33,6 +33,8 @@ std::vector<Kernel> compile_parallel(const std::vector<std::string>& bodies, con
 
 // NVRTC only (no device): compiles `src` to an sm_100a cubin and returns its size.
 size_t compile_only(const std::string& src);
+// NVRTC compilations and kernel-cache hits (cubin files) since the library was loaded
+void stats(int64_t* builds, int64_t* hits);
 // ... one kernel body per entry, compiled in concurrent chunks; total cubin bytes
 size_t compile_only_parallel(const std::vector<std::string>& bodies);
 

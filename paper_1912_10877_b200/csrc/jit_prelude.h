@@ -34,20 +34,6 @@ __device__ __forceinline__ void dense1(V* x, V m00, V m10, V m01, V m11) {
     x[j | (1 << K)] = cfma(cmul(m10, a), m11, b);
   }
 }
-// the same 2x2 on two register tiles at once (reverse pass: ψ and φ̄), pairs interleaved
-template <class V, int R, int K, int CM, int CV>
-__device__ __forceinline__ void dense1x2(V* x, V* y, V m00, V m10, V m01, V m11) {
-#pragma unroll
-  for (int j = 0; j < R; ++j) {
-    if (j & (1 << K)) continue;
-    if ((j & CM) != CV) continue;
-    V a = x[j], b = x[j | (1 << K)], c = y[j], d = y[j | (1 << K)];
-    x[j] = cfma(cmul(m00, a), m01, b);
-    y[j] = cfma(cmul(m00, c), m01, d);
-    x[j | (1 << K)] = cfma(cmul(m10, a), m11, b);
-    y[j | (1 << K)] = cfma(cmul(m10, c), m11, d);
-  }
-}
 template <class V, int R, int K, int CM, int CV>
 __device__ __forceinline__ void swap1(V* x) {
 #pragma unroll
@@ -55,18 +41,6 @@ __device__ __forceinline__ void swap1(V* x) {
     if (j & (1 << K)) continue;
     if ((j & CM) != CV) continue;
     V a = x[j]; x[j] = x[j | (1 << K)]; x[j | (1 << K)] = a;
-  }
-}
-// swap1 under a per-thread predicate, by selects instead of a branch (keeps the stage one basic block)
-template <class V, int R, int K, int CM, int CV>
-__device__ __forceinline__ void cswap1(V* x, bool p) {
-#pragma unroll
-  for (int j = 0; j < R; ++j) {
-    if (j & (1 << K)) continue;
-    if ((j & CM) != CV) continue;
-    const V a = x[j], b = x[j | (1 << K)];
-    x[j].x = p ? b.x : a.x; x[j].y = p ? b.y : a.y;
-    x[j | (1 << K)].x = p ? a.x : b.x; x[j | (1 << K)].y = p ? a.y : b.y;
   }
 }
 template <class V, int R, int K, int CM, int CV>
@@ -178,33 +152,6 @@ __device__ __forceinline__ void gcross1(const V* p, const V* a, double* c) {
 // Hermitian-run cross statistics (4 components instead of 8): for Hermitian M,
 //   Im Σ_ab M_ab C_ab = M00 Im C00 + M11 Im C11 + Re M01 Im(C01 + C10) + Im M01 Re(C01 − C10)
 // c[0] = Im C00, c[1] = Im C11, c[2] = Im(C01 + C10), c[3] = Re(C01 − C10): 12 DFMA per pair.
-template <class V, int R, int K>
-__device__ __forceinline__ void gcrossh2(const V* p, const V* a, double* c) {
-  // the in-thread sum over the R/2 pairs runs in the element type (complex64: FP32 — 8 terms,
-  // far inside its 1e-5 tolerance); the warp and tile reductions that follow are in double
-  typedef typename RT<V>::T T;
-  // two accumulator sets (alternating pairs) halve the dependent FMA chains
-  T c0[2] = {0, 0}, c1[2] = {0, 0}, i01[2] = {0, 0}, i10[2] = {0, 0}, r01[2] = {0, 0}, r10[2] = {0, 0};
-  int h = 0;
-#pragma unroll
-  for (int j = 0; j < R; ++j) {
-    if (j & (1 << K)) continue;
-    const T a0x = a[j].x, a0y = a[j].y, a1x = a[j | (1 << K)].x, a1y = a[j | (1 << K)].y;
-    const T p0x = p[j].x, p0y = p[j].y, p1x = p[j | (1 << K)].x, p1y = p[j | (1 << K)].y;
-    c0[h] = fma(a0x, p0y, fma(-a0y, p0x, c0[h]));
-    c1[h] = fma(a1x, p1y, fma(-a1y, p1x, c1[h]));
-    i01[h] = fma(a0x, p1y, fma(-a0y, p1x, i01[h]));
-    i10[h] = fma(a1x, p0y, fma(-a1y, p0x, i10[h]));
-    r01[h] = fma(a0x, p1x, fma(a0y, p1y, r01[h]));
-    r10[h] = fma(a1x, p0x, fma(a1y, p0y, r10[h]));
-    h ^= 1;
-  }
-  // assigned, not accumulated: every caller hands in a fresh c (0 + s costs a DADD, -0 rules)
-  c[0] = (double)c0[0] + (double)c0[1];
-  c[1] = (double)c1[0] + (double)c1[1];
-  c[2] = ((double)i01[0] + (double)i01[1]) + ((double)i10[0] + (double)i10[1]);
-  c[3] = ((double)r01[0] + (double)r01[1]) - ((double)r10[0] + (double)r10[1]);
-}
 template <class V, int R, int K>
 __device__ __forceinline__ void gcrossh1(const V* p, const V* a, double* c) {
   typedef typename RT<V>::T T;
@@ -350,6 +297,13 @@ __device__ __forceinline__ void reg_dealloc() { asm volatile("setmaxnreg.dec.syn
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" :: "n"(N) : "memory"); }
+// one writer per reduction group: every lane reads the cell (harmless), the lane with w set stores
+// cell + v by a predicated st.shared — no branch, so the stage stays one basic block
+__device__ __forceinline__ void sg_acc(double* cell, double v, bool w) {
+  const double nv = *cell + v;
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q st.shared.f64 [%0], %1;\n}\n"
+               :: "r"(smem_u32(cell)), "d"(nv), "r"((unsigned)w) : "memory");
+}
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -97,7 +97,14 @@ __device__ __forceinline__ void apply_sub(const GateArgs& a, V* x, V* y) {
         for (int r = 0; r < D; ++r) {
             V acc = mk<V>(0, 0);
 #pragma unroll
-            for (int j = 0; j < D; ++j) acc = cfma(acc, mat_at<V, T>(a, j * D + r), x[j]);
+            for (int j = 0; j < D; ++j) {
+                // the reference's dense path skips exactly-zero inputs (register.hpp:379): a
+                // non-finite matrix column then contributes nothing where x == 0 (select, no branch)
+                const V t = cfma(acc, mat_at<V, T>(a, j * D + r), x[j]);
+                const bool zero = x[j].x == 0 && x[j].y == 0;
+                acc.x = zero ? acc.x : t.x;
+                acc.y = zero ? acc.y : t.y;
+            }
             y[r] = acc;
         }
     }

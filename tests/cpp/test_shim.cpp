@@ -29,7 +29,7 @@ int main() {
     }
     // CNOT as instruct(X, (1,), (2,), (1,)) on |10> (qubit 2 set) -> |11>
     {
-        auto reg = qb::product_state(0b10, 2);
+        auto reg = qb::product_state(qb::BitStr(0b10, 2));
         std::size_t t[] = {1}, c[] = {2};
         int cfg[] = {1};
         qb::instruct(reg, "X", t, c, cfg);

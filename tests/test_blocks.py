@@ -122,3 +122,18 @@ def test_time_evolution_blocks_host():
         Bk.time_evolve(Bk.put(20, 1, Bk.H), 0.1)  # too large for a materialised matrix
     with _pt.raises(Er.UnsupportedError):
         Bk.segments(Bk.put(n, (1, 2), Bk.time_evolve(Cc.heisenberg(2), 0.1)))
+
+
+def test_subroutine_and_qft_host():
+    """Subroutine = put on its locations; qft(n) = bit reversal then the inverse DFT
+    scaled by sqrt(2^n) (SPEC App F oracle); gatecount(qft(3)) = {H: 3, Control{shift}: 3}."""
+    import numpy as np
+    import paper_1912_10877_b200 as qb
+    s = qb.subroutine(5, qb.dagger(qb.qft(4)), (1, 2, 3, 4))
+    assert np.abs(qb.mat(s) - qb.mat(qb.put(5, (1, 2, 3, 4), qb.dagger(qb.qft(4))))).max() == 0.0
+    assert qb.gatecount(qb.qft(3)) == {"H": 3, "Control{shift}": 3}
+    n = 5
+    N = 1 << n
+    x = np.random.default_rng(0).normal(size=N) + 1j * np.random.default_rng(1).normal(size=N)
+    rev = np.array([int(format(i, f"0{n}b")[::-1], 2) for i in range(N)])
+    assert np.abs(qb.mat(qb.qft(n)) @ x - np.fft.ifft(x[rev]) * np.sqrt(N)).max() < 1e-13

@@ -342,3 +342,22 @@ def test_one_call_forms(orc):
     check(lib().qbg_collapse(r1._h, g1._h, out1.ctypes.data))
     check(lib().qbg_measure_collapse(r2._h, g2._h, out2.ctypes.data))
     assert np.array_equal(out1, out2) and rel(r1.state(), r2.state()) == 0
+
+
+def test_subroutine_listing16_on_device():
+    """Listing 16: inverse QFT on a local scope (Subroutine) equals the explicit focus -> apply ->
+    relax of Listing 15, and the put-lowered program; an Add child takes the focus/relax path."""
+    st = O.restatement().rand_state(6, 2, 17)
+    a = qb.Register(6, 2).set_state(st)
+    qb.apply(a, qb.subroutine(6, qb.dagger(qb.qft(4)), (2, 5, 1, 3)))
+    b = qb.Register(6, 2).set_state(st)
+    b.focus(2, 5, 1, 3)
+    qb.apply(b, qb.dagger(qb.qft(4)))
+    b.relax(2, 5, 1, 3, to_nactive=6)
+    assert rel(a.state(), b.state()) < 1e-14
+    want = (qb.mat(qb.put(6, (2, 5, 1, 3), qb.dagger(qb.qft(4)))) @ st.T).T
+    assert rel(a.state(), want) < TOL
+    obs = qb.subroutine(6, qb.heisenberg(3), (4, 6, 2))
+    c = qb.Register(6, 2).set_state(st)
+    qb.apply(c, obs)
+    assert rel(c.state(), (qb.mat(obs) @ st.T).T) < TOL
