@@ -42,6 +42,11 @@ def parse():
                     help="register precision (the metric is quoted in c128; c64 is reported beside it)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU sample for cpu_baseline")
+    ap.add_argument("--no-sharded", action="store_true", help="skip the sharded-state weak-scaling measurement")
+    ap.add_argument("--sharded-local-qubits", type=int, default=33,
+                    help="qubits per GPU of the sharded state (33: 128 GiB per B200; n = this + log2 N)")
+    ap.add_argument("--sharded-depth", type=int, default=2)
+    ap.add_argument("--sharded-steps", type=int, default=3)
     return ap.parse_args()
 
 
@@ -211,6 +216,87 @@ def workload_config(args):
             "parallelism": f"replicas x{args.gpus}"}
 
 
+# ---- sharded states: SURVEY §8(e) / BASELINE cfg 5, weak scaling 33q/1, 34q/2, 35q/4, 36q/8 ------------
+def sharded_weak_scaling(args, rank, world, pg):
+    """variational_circuit(n, depth) forward + <heisenberg(n)> on one n-qubit state split over the N
+    GPUs (n = local + log2 N; each GPU holds a 2^local complex128 shard), global qubits moved by
+    the chunked all-to-all remaps of sharded.py over NCCL.  Device-timed (CUDA events on the
+    library stream), max over ranks.  gates/s counts the circuit's gates on the whole state."""
+    import torch
+    import paper_1912_10877_b200 as qb
+    from paper_1912_10877_b200.sharded import DeviceNcclBackend, ShardedState
+    g = world.bit_length() - 1
+    if world != 1 << g:
+        return {"skipped": "world size is not a power of two"}
+    nl, d = args.sharded_local_qubits, args.sharded_depth
+    n = nl + g
+    if n > qb.qubit_cap():
+        qb.set_qubit_cap(n)
+    circ = qb.variational_circuit(n, d)
+    qb.dispatch(circ, "random", rng=qb.Rng(42))
+    h = qb.heisenberg(n)
+    terms = qb.pauli_terms(h)
+    be = DeviceNcclBackend(n, g)
+    st = ShardedState(be, n, g)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if pg is not None:
+            pg.barrier()
+
+    def one():
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        st.reset_zero()
+        e[0].record(stream)
+        st.apply(circ)
+        e[1].record(stream)
+        energy = st.expect_pauli(terms)
+        e[2].record(stream)
+        return e, energy
+
+    one()  # warm-up: segment programs, kernels, staging arena
+    torch.cuda.synchronize()
+    barrier()
+    ex0_b = be.exchange.bytes_sent
+    be.exchange.events = []
+    apply_ms, exp_ms, energy = [], [], None
+    for _ in range(args.sharded_steps):
+        e, energy = one()
+        torch.cuda.synchronize()
+        apply_ms.append(e[0].elapsed_time(e[1]))
+        exp_ms.append(e[1].elapsed_time(e[2]))
+    barrier()
+    a, x = statistics.median(apply_ms), statistics.median(exp_ms)
+    if pg is not None:
+        t = torch.tensor([a, x], device="cuda")
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        a, x = float(t[0]), float(t[1])
+    G = n * (1 + 4 * d)
+    S_local = 16 << nl
+    remaps = [len(p) for p in st.sched.exchanges]
+    per_step_bytes = (be.exchange.bytes_sent - ex0_b) / max(1, args.sharded_steps)
+    out = {"workload": f"variational_circuit({n},{d}) forward + <heisenberg({n})> open, complex128, "
+                       f"{world} GPU(s) x 2^{nl} amplitudes", "qubits": n, "local_qubits": nl, "global_qubits": g,
+           "gates": G, "apply_ms": a, "expect_ms": x, "step_ms": a + x, "gates_per_s": G / (a / 1e3),
+           "energy": energy, "scaling": "weak",
+           "hbm_gbs_alg_per_gpu": G * 2 * S_local / (a / 1e3) / 1e9,
+           "exchange_bytes_per_step_per_gpu": per_step_bytes,
+           "exchanges_per_step": len(remaps) // (args.sharded_steps + 1) if remaps else 0,
+           "staging_bytes": be.exchange.staging_bytes,
+           "memory_note": "per GPU: shard (16 x 2^local B) + staging arena; the tile engine's plan tables"}
+    if be.exchange.events:
+        # pack + NCCL send/recv + unpack of every remap (device-timed on the library stream)
+        ex_ms = sum(e0.elapsed_time(e1) for e0, e1 in be.exchange.events) / args.sharded_steps
+        if pg is not None:
+            t = torch.tensor([ex_ms], device="cuda")
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+            ex_ms = float(t[0])
+        out["exchange_ms_per_step"] = ex_ms
+        out["nvlink_gbs_per_gpu"] = per_step_bytes / (ex_ms / 1e3) / 1e9  # bytes sent per direction
+    del st, be
+    return out
+
+
 # ---- our arm ------------------------------------------------------------------------------------
 def main():
     args = parse()
@@ -224,7 +310,8 @@ def main():
     pg = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from datetime import timedelta
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local), timeout=timedelta(minutes=10))
         pg = dist
 
     import paper_1912_10877_b200 as qb
@@ -381,6 +468,18 @@ def main():
                "sample": r["sample"] + "; 1 core (unbatched state: the reference parallelises over columns only)",
                "cpu_model": cb.cpu_model(), "job_seconds_extrapolated": r["job_seconds_extrapolated"]}
 
+    sharded = None
+    prog_stats = prog.stats()
+    if not args.no_sharded and args.dtype == "c128":
+        del reg, prog
+        import gc
+        gc.collect()
+        L.qbg_release_workspace()
+        try:
+            sharded = sharded_weak_scaling(args, rank, world, pg)
+        except Exception as e:  # reported, never fatal to the metric line
+            sharded = {"error": f"{type(e).__name__}: {e}"[:300]}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": world, "steps": args.steps,
@@ -392,8 +491,9 @@ def main():
                         "> 1 because fusion applies ~34 gates per HBM pass; the real HBM rates are "
                         "roofline.achieved (dominant kernel) and roofline.step (whole step)",
             "energy": float(res.energies[0]),
-            "fusion": not args.no_fusion, "prog_stats": prog.stats(),
+            "fusion": not args.no_fusion, "prog_stats": prog_stats,
             "e2e": e2e, "gpu_launches": launches, "clocks": ck, "roofline": roofline, "cpu_baseline": cpu,
+            "sharded_state": sharded,
         }
         print(json.dumps(line), flush=True)
     if pg is not None:

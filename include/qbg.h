@@ -206,6 +206,22 @@ int qbg_load(const char* path, uint64_t seed, int32_t dtype, qbg_reg** out);
 /* The same format from memory (Register::load(std::istream&) of the C++ shim). */
 int qbg_load_memory(const void* data, int64_t nbytes, uint64_t seed, int32_t dtype, qbg_reg** out);
 
+/* ---- sharded states (SPEC.md:290 makes distributed state a non-goal of the
+   reference, so these have no reference counterpart) ---------------------------------------------
+   A state of n qubits over 2^g ranks is one register of n-g local qubits per rank.  Moving global
+   qubits k_1..k_j against local qubits l_1..l_j exchanges, with each partner, the sub-block of rows
+   whose local qubits l_i are fixed to the partner's bits.  pack copies sub-block rows
+   [row0, row0 + nrows) (rows in increasing order; each row carries its nbatch amplitudes) into the
+   device buffer dst; unpack writes them back.  fix_locs are 1-based local qubits (<= 8), bit i of
+   fix_val is the value of fix_locs[i].  Stream-ordered on the library stream. */
+int qbg_shard_pack(const qbg_reg* reg, const int32_t* fix_locs, int32_t nfix, uint64_t fix_val, int64_t row0,
+                   int64_t nrows, void* dst);
+int qbg_shard_unpack(qbg_reg* reg, const int32_t* fix_locs, int32_t nfix, uint64_t fix_val, int64_t row0,
+                     int64_t nrows, const void* src);
+/* device staging buffers owned by the library (exchange chunks) */
+int qbg_buffer_alloc(int64_t bytes, void** out);
+int qbg_buffer_free(void* ptr);
+
 /* ---- gate programs: apply(reg, block) lowered to instruct, SPEC.md:315-323 --------------- */
 int qbg_prog_create(int32_t nqubits, const qbg_op* ops, int64_t nops, const double* vals,
                     int64_t nvals, const int64_t* perms, int64_t nperms, qbg_prog** out);

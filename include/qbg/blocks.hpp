@@ -924,10 +924,21 @@ inline GradResult expect_grad(const BlockPtr& obs, const Register& reg, const Bl
 
 // parameter-shift gradient, exact mode: ½(<O>_{θ+π/2} − <O>_{θ−π/2}) per
 // parameter, summed over the batch; every parameter must be a rotation with a reflexive generator
+namespace detail {
+// a rotation under a Control node has the generator P_ctrl ⊗ Σ, which is not reflexive
+inline bool controlled_param(const BlockPtr& b, bool under) {
+    if (b->parameterised()) return under;
+    for (auto& c : b->children)
+        if (controlled_param(c, under || b->kind == BlockKind::Control)) return true;
+    return false;
+}
+}  // namespace detail
 inline std::vector<double> faithful_grad(const BlockPtr& obs, const Register& reg, const BlockPtr& circuit) {
     auto nodes = parameter_nodes(circuit);
     for (auto* p : nodes)
         if (p->kind != BlockKind::Rotation) throw UnsupportedError("faithful_grad: shift/phase parameters have no shift rule");
+    if (detail::controlled_param(circuit, false))
+        throw UnsupportedError("faithful_grad: a controlled rotation's generator is not reflexive (no shift rule)");
     std::vector<double> g(nodes.size(), 0.0);
     for (std::size_t k = 0; k < nodes.size(); ++k) {
         const double th = nodes[k]->theta;

@@ -5,7 +5,7 @@ mirror of the reference interface (qblock register.hpp / gates.hpp and SPEC.md b
 autodiff) over its C-ABI (include/qbg.h)."""
 from . import errors
 from ._capi import LIB_PATH, lib
-from .ad import GradResult, backward, expect, expect_grad, faithful_grad, obs_apply
+from .ad import GradResult, backward, eigenbasis, expect, expect_grad, faithful_grad, obs_apply, sampled_expect
 from .blocks import (CNOT, CZ, SWAP, Add, Block, Chain, Control, Daggered, GeneralMatrix, H, I2, Kron, P0, P1,
                      Pd, Phase, Program, Pu, Put, Repeat, Rotation, Rx, Ry, Rz, S, Scale, Sdag, Shift, T, Tdag,
                      Toffoli, X, Y, Z, apply, chain, compile_block, compile_observable, control, dagger,

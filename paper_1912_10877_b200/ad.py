@@ -77,11 +77,80 @@ def expect_grad(obs: Block, pair, want_state_grad: bool = False, inplace: bool =
     return GradResult(energies, grads[: p.nparams], sg)
 
 
-def faithful_grad(obs: Block, pair) -> np.ndarray:
-    """Parameter-shift ("faithful") gradient, exact mode (PAPER eq. shiftrule):
+def _controlled_param(b, under=False) -> bool:
+    """A rotation under a Control node has the generator P_ctrl ⊗ Σ, which is not reflexive."""
+    from .blocks import Control, Phase, Rotation, Shift
+    if isinstance(b, (Rotation, Shift, Phase)):
+        return under
+    return any(_controlled_param(c, under or isinstance(b, Control)) for c in b.subblocks())
+
+
+def eigenbasis(obs: Block):
+    """eigenbasis(O) -> (E, U) with O = U E U† (SPEC.md blocks.eigenbasis, Listing 10) for a Pauli
+    string or a sum of them: per qubit X -> (Z, H), Y -> (Z, chain(H, S)), Z -> (Z, I).  Returns a
+    list of (E_terms, U) measurement settings: the terms are grouped qubit-wise compatibly (all
+    terms of a group share the basis of every qubit they touch), E_terms are the (c, zmask)
+    diagonal terms in that basis, and U is the basis-change circuit (apply U† = dagger(U) before
+    sampling in the computational basis)."""
+    from .blocks import H as Hg, S as Sg, chain, dagger, pauli_terms, put
+    n = obs.nqubits
+    groups = []  # [(basis dict qubit -> 'X'|'Y'|'Z', [(c, support mask)])]
+    for c, x, z in pauli_terms(obs):
+        basis = {}
+        for q in range(n):
+            if (x >> q) & 1:
+                basis[q] = "Y" if (z >> q) & 1 else "X"
+            elif (z >> q) & 1:
+                basis[q] = "Z"
+        for gb, ts in groups:
+            if all(gb.get(q, b) == b for q, b in basis.items()):
+                gb.update(basis)
+                ts.append((c, x | z))
+                break
+        else:
+            groups.append((dict(basis), [(c, x | z)]))
+    out = []
+    for gb, ts in groups:
+        blocks = []
+        for q, b in sorted(gb.items()):
+            if b == "X":
+                blocks.append(put(n, q + 1, Hg))
+            elif b == "Y":
+                blocks.append(put(n, q + 1, chain(Hg, Sg)))
+        U = chain(n, *blocks) if blocks else None
+        out.append((ts, U, None if U is None else dagger(U)))
+    return out
+
+
+def sampled_expect(obs: Block, reg: Register, nshots: int, rng=None) -> np.ndarray:
+    """⟨O⟩ per batch estimated from nshots computational-basis samples per measurement setting
+    (Listing 10 pipeline): rotate a copy by U† of each eigenbasis group, sample
+    on the device (bit-exact stream, register.hpp:436-459), average the diagonal eigenvalues
+    Σ c (-1)^{popcount(bits & support)}."""
+    from .register import measure
+    est = np.zeros(reg.nbatch)
+    for ts, _, Udag in eigenbasis(obs):
+        work = reg.copy()
+        if Udag is not None:
+            apply(work, Udag)
+        bits = measure(work, nshots, rng)  # (nbatch, nshots)
+        for c, m in ts:
+            par = np.zeros(bits.shape, dtype=np.int64)
+            v = bits & np.uint64(m)
+            while v.any():  # popcount parity
+                par ^= (v & np.uint64(1)).astype(np.int64)
+                v = v >> np.uint64(1)
+            est += np.real(c) * (1.0 - 2.0 * par).mean(axis=1)
+    return est
+
+
+def faithful_grad(obs: Block, pair, nshots: int | None = None, rng=None) -> np.ndarray:
+    """Parameter-shift ("faithful") gradient (PAPER eq. shiftrule):
     θ̄_k = ½(⟨O⟩_{θ_k+π/2} − ⟨O⟩_{θ_k−π/2}), summed over the batch.  Every parameter must belong to
     a Rotation with a reflexive generator; Shift / Phase parameters raise UnsupportedError.
-    2P device evaluations of the circuit (the forward-mode cost the paper contrasts with AD)."""
+    2P device evaluations of the circuit (the forward-mode cost the paper contrasts with AD).
+    ``nshots=None`` is the exact mode (expect); an integer estimates each ⟨O⟩ from nshots samples
+    per eigenbasis setting (``sampled_expect``; ``rng`` a :class:`Rng`, default Rng(42))."""
     from .blocks import Rotation, dispatch, parameter_nodes, parameters
     from .mmd import MMD, mmd_grad
     if isinstance(obs, MMD):
@@ -91,17 +160,30 @@ def faithful_grad(obs: Block, pair) -> np.ndarray:
     for nd in nodes:
         if not isinstance(nd, Rotation):
             raise errors.UnsupportedError("faithful_grad: shift rule needs Rotation parameters only")
+    if _controlled_param(circuit):
+        raise errors.UnsupportedError("faithful_grad: a controlled rotation's generator is not reflexive (no shift rule)")
     theta = parameters(circuit)
     grads = np.empty(theta.size)
+    if nshots is not None:
+        from .register import Rng
+        rng = rng if rng is not None else Rng(42)
+
+    def value():
+        if nshots is None:
+            return float(np.sum(expect(obs, (reg, circuit))))
+        psi = reg.copy()
+        apply(psi, circuit)
+        return float(np.sum(sampled_expect(obs, psi, nshots, rng)))
+
     try:
         for k in range(theta.size):
             t = theta.copy()
             t[k] = theta[k] + np.pi / 2
             dispatch(circuit, t)
-            ep = float(np.sum(expect(obs, (reg, circuit))))
+            ep = value()
             t[k] = theta[k] - np.pi / 2
             dispatch(circuit, t)
-            em = float(np.sum(expect(obs, (reg, circuit))))
+            em = value()
             grads[k] = 0.5 * (ep - em)
     finally:
         dispatch(circuit, theta)

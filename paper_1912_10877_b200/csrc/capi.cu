@@ -1060,6 +1060,44 @@ int qbg_relax(qbg_reg* r, const int32_t* locs, int32_t nloc, int32_t to_nactive)
     });
 }
 
+// ---- sharded states: sub-block pack / unpack and staging buffers ---------------
+int qbg_shard_pack(const qbg_reg* r, const int32_t* fix_locs, int32_t nfix, uint64_t fix_val, int64_t row0,
+                   int64_t nrows, void* dst) {
+    return guarded([&] {
+        check_reg(r);
+        if (nfix > 0 && !fix_locs) raise(QBG_ERR_VALIDATION, "shard pack: null locations");
+        int pos[8];
+        for (int i = 0; i < nfix && i < 8; ++i) pos[i] = fix_locs[i] - 1;
+        if (row0 < 0 || nrows < 0) raise(QBG_ERR_RANGE, "shard pack: negative row range");
+        launch_shard_copy(r->s, true, pos, nfix, fix_val, static_cast<uint64_t>(row0), static_cast<uint64_t>(nrows), dst);
+    });
+}
+int qbg_shard_unpack(qbg_reg* r, const int32_t* fix_locs, int32_t nfix, uint64_t fix_val, int64_t row0, int64_t nrows,
+                     const void* src) {
+    return guarded([&] {
+        check_reg(r);
+        if (nfix > 0 && !fix_locs) raise(QBG_ERR_VALIDATION, "shard unpack: null locations");
+        int pos[8];
+        for (int i = 0; i < nfix && i < 8; ++i) pos[i] = fix_locs[i] - 1;
+        if (row0 < 0 || nrows < 0) raise(QBG_ERR_RANGE, "shard unpack: negative row range");
+        launch_shard_copy(r->s, false, pos, nfix, fix_val, static_cast<uint64_t>(row0), static_cast<uint64_t>(nrows),
+                          const_cast<void*>(src));
+    });
+}
+int qbg_buffer_alloc(int64_t bytes, void** out) {
+    return guarded([&] {
+        if (bytes <= 0 || !out) raise(QBG_ERR_VALIDATION, "buffer: size must be positive");
+        *out = dev_alloc(static_cast<size_t>(bytes), false);
+    });
+}
+int qbg_buffer_free(void* p) {
+    return guarded([&] {
+        if (!p) return;
+        QBG_CUDA(cudaStreamSynchronize(g_stream));
+        QBG_CUDA(cudaFree(p));
+    });
+}
+
 // ---- state files (register.hpp:181-205) -------------------------------------------------------------
 int qbg_save(const qbg_reg* r, const char* path) {
     return guarded([&] {

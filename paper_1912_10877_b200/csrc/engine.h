@@ -78,6 +78,11 @@ void multi_axpy(const DevState& w, const std::vector<DevState>& vs, const std::v
 void launch_spmv(const DevState& x, const DevState& y, const int64_t* d_rowptr, const int32_t* d_col,
                  const double* d_val, int64_t nnz);
 
+// ---- sharded states (shard.cu): copy the rows of a sub-block (nfix fixed 0-based row bits with
+// values fix_val bit i -> fix_pos[i]) in sub-row range [h0, h0 + count) to / from a flat buffer ----
+void launch_shard_copy(const DevState& s, bool pack, const int* fix_pos, int nfix, uint64_t fix_val, uint64_t h0,
+                       uint64_t count, void* buf);
+
 // scratch device memory owned by the library (grows; stream-ordered reuse)
 void* scratch(size_t bytes, int slot);
 

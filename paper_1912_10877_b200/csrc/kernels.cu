@@ -130,9 +130,19 @@ __global__ void __launch_bounds__(256) k_gate(V* __restrict__ st, const __grid_c
 
 // ---- reverse step (fallback of fused.cu's backward tiles) ---------------------------------
 struct KArgs {
-    int kind;  // 0 none, DIAGONAL or DENSE
+    int kind;          // 0 none, DIAGONAL or DENSE
+    const cdbl* ext;   // dense generators wider than 3 qubits (32 x 32 at t = 5) live in global memory
     cdbl m[64];
 };
+
+template <int T>
+__device__ __forceinline__ cdbl k_at(const KArgs& k, int idx) {
+    if constexpr ((1 << T) * (1 << T) <= 64) {
+        return k.m[idx];
+    } else {
+        return k.ext[idx];
+    }
+}
 
 template <typename V, int T>
 __device__ __forceinline__ double grad_term(const KArgs& k, const V* ps, const V* ad) {
@@ -149,7 +159,7 @@ __device__ __forceinline__ double grad_term(const KArgs& k, const V* ps, const V
         for (int r = 0; r < D; ++r) {
             V kp = mk<V>(0, 0);
 #pragma unroll
-            for (int j = 0; j < D; ++j) kp = cfma(kp, from_cd<V>(k.m[j * D + r]), ps[j]);
+            for (int j = 0; j < D; ++j) kp = cfma(kp, from_cd<V>(k_at<T>(k, j * D + r)), ps[j]);
             s += static_cast<double>(ad[r].x) * kp.y - static_cast<double>(ad[r].y) * kp.x;
         }
     }
@@ -183,20 +193,26 @@ __global__ void __launch_bounds__(256)
         uint64_t base = deposit_zeros(r, a.fixpos, a.nfix) | a.cval;
         uint64_t e0 = base * static_cast<uint64_t>(a.B) + b;
         V xp[D], xa[D], y[D];
-        if (kk.kind) {
-            V ps[D], ad[D];
-#pragma unroll
-            for (int k = 0; k < D; ++k) {
-                ps[k] = psi[e0 + a.offB[k]];
-                ad[k] = adj[e0 + a.offB[k]];
-            }
-            g += grad_term<V, T>(kk, ps, ad);
-        }
+        // gather once in the order apply_sub reads (permuted for PERMUTATION); the gradient term
+        // needs the natural order, which for DENSE / DIAGONAL is the same registers
 #pragma unroll
         for (int k = 0; k < D; ++k) {
             int64_t o = KIND == QBG_MAT_PERMUTATION ? a.poffB[k] : a.offB[k];
             xp[k] = psi[e0 + o];
             xa[k] = adj[e0 + o];
+        }
+        if (kk.kind) {
+            if constexpr (KIND == QBG_MAT_PERMUTATION) {
+                V ps[D], ad[D];
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    ps[k] = psi[e0 + a.offB[k]];
+                    ad[k] = adj[e0 + a.offB[k]];
+                }
+                g += grad_term<V, T>(kk, ps, ad);
+            } else {
+                g += grad_term<V, T>(kk, xp, xa);
+            }
         }
         apply_sub<V, T, KIND>(a, xp, y);
 #pragma unroll
@@ -274,16 +290,24 @@ void dispatch_back(const DevState& psi, const DevState& adj, const Gate& g, cons
     KArgs kk;
     std::memset(&kk, 0, sizeof(kk));
     if (K) {
-        if (K->dim * K->dim > 64) raise(QBG_ERR_UNSUPPORTED, "backward: generator wider than 3 qubits");
         if (K->kind == QBG_MAT_DIAGONAL || K->kind == QBG_MAT_IDENTITY) {
             kk.kind = QBG_MAT_DIAGONAL;
             for (int r = 0; r < K->dim; ++r) kk.m[r] = K->kind == QBG_MAT_IDENTITY ? cdbl{1, 0} : K->m[r];
         } else {
             kk.kind = QBG_MAT_DENSE;
+            std::vector<cdbl> dn(static_cast<size_t>(K->dim) * K->dim, cdbl{0, 0});
             if (K->kind == QBG_MAT_DENSE) {
-                std::copy(K->m.begin(), K->m.end(), kk.m);
+                dn = K->m;
             } else {  // permutation -> dense
-                for (int r = 0; r < K->dim; ++r) kk.m[K->perm[r] * K->dim + r] = K->m[r];
+                for (int r = 0; r < K->dim; ++r) dn[K->perm[r] * K->dim + r] = K->m[r];
+            }
+            if (dn.size() <= 64) {
+                std::copy(dn.begin(), dn.end(), kk.m);
+            } else {  // 4- and 5-qubit generators: stream-ordered copy to a library scratch slot
+                void* d = scratch(dn.size() * sizeof(cdbl), 20);
+                QBG_CUDA(cudaMemcpyAsync(d, dn.data(), dn.size() * sizeof(cdbl), cudaMemcpyHostToDevice, stream()));
+                QBG_CUDA(cudaStreamSynchronize(stream()));  // dn is a host temporary
+                kk.ext = static_cast<const cdbl*>(d);
             }
         }
     }
@@ -293,7 +317,9 @@ void dispatch_back(const DevState& psi, const DevState& adj, const Gate& g, cons
         case 1: dispatch_back_kind<V, 1>(psi, adj, g, a, kk, partials, grid); break;
         case 2: dispatch_back_kind<V, 2>(psi, adj, g, a, kk, partials, grid); break;
         case 3: dispatch_back_kind<V, 3>(psi, adj, g, a, kk, partials, grid); break;
-        default: raise(QBG_ERR_UNSUPPORTED, "backward: more than 3 targets");
+        case 4: dispatch_back_kind<V, 4>(psi, adj, g, a, kk, partials, grid); break;
+        case 5: dispatch_back_kind<V, 5>(psi, adj, g, a, kk, partials, grid); break;
+        default: raise(QBG_ERR_UNSUPPORTED, "backward: more than 5 targets");
     }
 }
 

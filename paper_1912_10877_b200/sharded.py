@@ -9,21 +9,33 @@ Per gate (SPEC.md:315-323 semantics, lowered ops):
     the gate, a matching rank drops the control;
   * diagonal gates on global qubits need no communication: the rank's bits select a
     sub-diagonal (or a scalar phase) on the remaining local targets;
-  * a non-diagonal target on a global qubit is first SWAPPED with a local qubit: partner ranks
-    r and r ^ (1 << k) exchange one half of their local state (the half whose local bit l
-    differs from their own global bit k): S_local / 2 per direction per rank (SURVEY §8(e)
-    "default: swap"), then the map records the exchange; later gates on that qubit are local.
-Expectation values of Pauli sums: terms are grouped by X support, the X support is swapped
-local, each rank evaluates its local terms (global Z bits become signs) and the energies are
-summed over ranks.
+  * a non-diagonal target on a global qubit must first become local.  The schedule
+    (`ShardedSchedule`) treats the local positions as a cache of the qubits the gates touch:
+    on a miss it evicts the local qubit whose next non-diagonal use is furthest ahead (Belady's
+    rule, over the whole op list) and, in the same exchange, also fetches every other global
+    qubit needed before the next-chosen victim would be (up to g pairs per exchange).  One
+    exchange of j pairs is an all-to-all inside groups of 2^j ranks: each rank keeps 1/2^j of
+    its shard and trades one 1/2^j sub-block with each of its 2^j - 1 partners — (1 - 2^-j) S_local
+    per direction, against j/2 S_local for j separate pairwise swaps.
+Expectation values of Pauli sums: terms are grouped by X support; the groups are scheduled the
+same way (their X support must be local), each rank evaluates its local terms (global Z bits
+become signs) and the energies are summed over ranks.
 
-The schedule is host logic independent of where the shards live.  Backends:
-  * ``DeviceVirtualBackend``: G shard registers on one GPU, exchanges by device copies (CI for
-    the multi-GPU path on one B200; also runs 33-qubit states as 8 x 30-qubit shards);
-  * ``DeviceNcclBackend``: one shard per process / GPU, exchanges with NCCL send/recv over
-    NVLink through torch.distributed (zero-copy views of the shard registers);
-  * tests add a numpy / CPU-oracle backend to check the schedule on CPU (gloo).
-All gate arithmetic runs in libqbg (the device backends); the backends only move bytes.
+Exchanges are chunked (`ChunkedExchange`): a fixed staging budget (default 2 GiB, two slots of
+send + receive buffers per partner) bounds the extra memory to shard + staging, whatever the
+shard size — at 36 qubits over 8 GPUs a shard is 128 GiB of a 180 GB B200.  A chunk is packed
+from the shard by a libqbg gather kernel (qbg_shard_pack), exchanged with NCCL send/recv through
+torch.distributed on the NCCL stream while the next chunk is packed, and scattered back
+(qbg_shard_unpack) into the sub-block it came from.
+
+The schedule and the exchange are host logic independent of where the shards live:
+  * ``DeviceNcclBackend``: one shard per process / GPU (libqbg register), NCCL transport;
+  * ``DeviceVirtualBackend``: 2^g shard registers on one GPU, the same pack / unpack kernels and
+    chunk loop with the partner's packed chunk read in place (the single-GPU CI of the path; also
+    runs 33-qubit states as 8 x 30-qubit shards);
+  * the tests run `DistShardBackend` itself (chunk loop, staging, transport) on gloo with a CPU
+    shard that implements only the local pack / unpack / gate primitives.
+All gate arithmetic runs in libqbg on the device backends; the exchange only moves bytes.
 """
 from __future__ import annotations
 
@@ -117,48 +129,104 @@ class QubitMap:
         return self.phys.index(pos)
 
 
+_INF = float("inf")
+
+
 class ShardedSchedule:
-    """Turns realised logical ops into per-rank local op lists and swap steps."""
+    """Turns realised logical ops into per-rank local op lists and exchange steps.
 
-    def __init__(self, n: int, g: int, lookahead: int = 64):
-        if g < 1 or g >= n:
-            raise errors.ValidationError("sharded: need 1 <= g < n global qubits")
+    Local positions are a cache of logical qubits; the "accesses" are the non-diagonal targets of
+    the ops in order (controls and diagonal targets may stay global).  A miss evicts by Belady's
+    rule (furthest next access, the whole list known ahead) and prefetches the global qubits that
+    are needed before the remaining victims' next access, batching up to g pairs per exchange."""
+
+    def __init__(self, n: int, g: int, min_pos: int = 3):
+        if g < 0 or g >= n:
+            raise errors.ValidationError("sharded: need 0 <= g < n global qubits")
         self.map = QubitMap(n, g)
-        self.lookahead = lookahead
+        # positions below min_pos (the tile engine's coalescing qubits) are not swapped out while
+        # others are available: a victim at position l makes the packed runs 2^l rows long
+        self.min_pos = min(min_pos, max(0, n - g - g))
+        self.exchanges = []  # [(pairs)] of the steps yielded so far (for reports / tests)
 
-    def _choose_local(self, ops, i, avoid):
-        """Local position to swap out: the highest one whose logical qubit is not used soon."""
+    def reset(self):
+        self.map.phys = list(range(self.map.n))
+
+    @staticmethod
+    def _accesses(needs):
+        """needs: list of sets of logical qubits that must be local at step i -> per-qubit sorted
+        step lists (the next-use table)."""
+        uses = {}
+        for i, s in enumerate(needs):
+            for q in s:
+                uses.setdefault(q, []).append(i)
+        return uses
+
+    @staticmethod
+    def _next_use(uses, q, i):
+        import bisect
+        lst = uses.get(q)
+        if not lst:
+            return _INF
+        k = bisect.bisect_left(lst, i)
+        return lst[k] if k < len(lst) else _INF
+
+    def plan_remap(self, needs, uses, i):
+        """Pairs (k, l) (global bit, local position) that make needs[i] local at step i."""
         m = self.map
-        soon = set()
-        for (_, _, _, t, c, _) in ops[i:i + self.lookahead]:
-            soon.update(q - 1 for q in t)
-            soon.update(q - 1 for q in c)
-        cands = [p for p in range(m.nl - 1, -1, -1) if m.logical_at(p) not in avoid]
-        for p in cands:
-            if m.logical_at(p) not in soon:
-                return p
-        return cands[0]
+        nl = m.nl
+        missing = sorted((q for q in needs[i] if m.is_global(q)), key=lambda q: m.phys[q])
+        if not missing:
+            return []
+        pinned = set(needs[i])
+
+        def victims():
+            c = []
+            for pos in range(nl):
+                lq = m.logical_at(pos)
+                if lq in pinned:
+                    continue
+                c.append((pos >= self.min_pos, self._next_use(uses, lq, i), pos, lq))
+            c.sort(key=lambda t: (t[0], t[1], t[2]), reverse=True)  # preferred: high pos, furthest use
+            return c
+
+        cand = victims()
+        if len(cand) < len(missing):
+            raise errors.ValidationError("sharded: an op has more non-diagonal targets than local qubits")
+        pairs = []
+        chosen = []
+        for q in missing:
+            v = cand.pop(0)
+            chosen.append(v)
+            pairs.append((q, v))
+        # prefetch: other global qubits whose next access precedes the next victim's
+        others = sorted((self._next_use(uses, q, i), q) for q in range(m.n) if m.is_global(q) and q not in missing)
+        for nu, q in others:
+            if len(pairs) >= m.g or not cand or nu == _INF:
+                break
+            if nu < cand[0][1]:
+                pairs.append((q, cand.pop(0)))
+        out = []
+        for q, (_, _, pos, lq) in pairs:
+            k = m.phys[q] - nl
+            m.phys[q], m.phys[lq] = pos, nl + k
+            out.append((k, pos))
+        self.exchanges.append(out)
+        return out
 
     def steps(self, ops):
-        """Yields ('swap', k, l) and ('ops', [per-op logical tuples]) in order; the per-rank
+        """Yields ('remap', [(k, l), ...]) and ('ops', [logical ops], phys) in order; the per-rank
         specialisation happens in `rank_ops` with the map valid at that point."""
+        needs = [set(q - 1 for q in t) if kind != MAT_DIAGONAL else set() for (kind, _, _, t, _, _) in ops]
+        uses = self._accesses(needs)
         m = self.map
         seg = []
         for i, op in enumerate(ops):
-            kind, mat, perm, t, c, f = op
-            if kind != MAT_DIAGONAL:
-                need = [q - 1 for q in t if m.is_global(q - 1)]
-                if need:
-                    if seg:
-                        yield ("ops", seg, list(m.phys))
-                        seg = []
-                    avoid = set(q - 1 for q in t) | set(q - 1 for q in c)
-                    for q in need:
-                        k = m.phys[q] - m.nl
-                        pl = self._choose_local(ops, i, avoid)
-                        lq = m.logical_at(pl)
-                        m.phys[q], m.phys[lq] = pl, m.nl + k
-                        yield ("swap", k, pl)
+            if any(m.is_global(q) for q in needs[i]):
+                if seg:
+                    yield ("ops", seg, list(m.phys))
+                    seg = []
+                yield ("remap", self.plan_remap(needs, uses, i))
             seg.append(op)
         if seg:
             yield ("ops", seg, list(m.phys))
@@ -215,25 +283,39 @@ class ShardedState:
         self.backend = backend
         self.n, self.g = n, g
         self.sched = ShardedSchedule(n, g)
+        self._ops_cache = {}
 
     @property
     def phys(self):
         return self.sched.map.phys
 
-    def apply(self, block, theta=None):
+    def reset_zero(self):
+        """|0...0>: every qubit map describes it, so the map returns to the identity too."""
+        self.backend.set_zero()
+        self.sched.reset()
+        return self
+
+    def _realised(self, block, theta):
         from .blocks import _Emitter, _lower, parameter_nodes, parameters
-        nodes = parameter_nodes(block)
-        em = _Emitter({id(p): k for k, p in enumerate(nodes)})
-        _lower(block, tuple(range(1, block.nqubits + 1)), (), (), em)
+        key = id(block)
+        em = self._ops_cache.get(key)
+        if em is None:
+            nodes = parameter_nodes(block)
+            em = _Emitter({id(p): k for k, p in enumerate(nodes)})
+            _lower(block, tuple(range(1, block.nqubits + 1)), (), (), em)
+            self._ops_cache = {key: em}
         th = parameters(block) if theta is None else np.asarray(theta, float)
-        ops = realise_ops(em, th)
+        return realise_ops(em, th)
+
+    def apply(self, block, theta=None):
+        ops = self._realised(block, theta)
         nl = self.n - self.g
         for st in self.sched.steps(ops):
-            if st[0] == "swap":
-                self.backend.swap(st[1], st[2])
+            if st[0] == "remap":
+                self.backend.remap(st[1])
             else:
                 _, seg, phys = st
-                self.backend.apply_local(lambda r: ShardedSchedule.rank_ops(seg, phys, nl, r))
+                self.backend.apply_local(lambda r, seg=seg, phys=phys: ShardedSchedule.rank_ops(seg, phys, nl, r))
         return self
 
     def expect_pauli(self, terms) -> float:
@@ -243,18 +325,27 @@ class ShardedState:
         groups = {}
         for c, x, z in terms:
             groups.setdefault(x, []).append((c, x, z))
+        # order: groups already local first, then by the schedule (Belady over the X supports)
+        order = sorted(groups, key=lambda x: sum(1 for q in range(self.n) if (x >> q) & 1 and m.is_global(q)))
+        needs = [set(q for q in range(self.n) if (x >> q) & 1) for x in order]
+        uses = ShardedSchedule._accesses(needs)
         total = 0.0
-        for x, ts in groups.items():
-            glob = [q for q in range(self.n) if (x >> q) & 1 and m.is_global(q)]
-            for q in glob:
-                k = m.phys[q] - nl
-                pl = next(p for p in range(nl - 1, -1, -1) if not (x >> m.logical_at(p)) & 1)
-                lq = m.logical_at(pl)
-                m.phys[q], m.phys[lq] = pl, nl + k
-                self.backend.swap(k, pl)
+        batch = []  # local-term builders of the groups evaluated together (one fused seed pass set)
+
+        def flush():
+            nonlocal total, batch
+            if batch:
+                fns = batch
+                total += self.backend.expect_local(lambda r: [t for f in fns for t in f(r)])
+                batch = []
+
+        for i, x in enumerate(order):
+            if any(m.is_global(q) for q in needs[i]):
+                flush()
+                self.backend.remap(self.sched.plan_remap(needs, uses, i))
             phys = list(m.phys)
 
-            def local_terms(r, ts=ts, phys=phys):
+            def local_terms(r, ts=groups[x], phys=phys):
                 out = []
                 for c, xx, zz in ts:
                     xl = zl = 0
@@ -274,8 +365,9 @@ class ShardedState:
                     out.append((c * sgn, xl, zl))
                 return out
 
-            total += self.backend.expect_local(local_terms)
-        return total
+            batch.append(local_terms)
+        flush()
+        return self.backend.reduce_sum(total)
 
     def state(self) -> np.ndarray:
         """Full logical state (small n): gather the shards and undo the qubit map."""
@@ -291,98 +383,306 @@ class ShardedState:
         return full
 
 
-def _half_view(t, nl, l, v):
-    """View of the amplitudes whose local bit l == v in a shard viewed as complex pairs."""
-    return t.view(1 << (nl - l - 1), 2, 1 << l, 2)[:, v]
+# ---------------------------------------------------------------------------------------------------
+# chunked exchange
+# ---------------------------------------------------------------------------------------------------
+DEFAULT_STAGING_BYTES = 2 << 30
 
 
-class DeviceVirtualBackend:
-    """All 2^g shards as libqbg registers on the current GPU; exchanges are device copies."""
+def remap_groups(rank: int, pairs):
+    """For a remap of pairs (k_i, l_i): the partners of `rank` and, per partner, the fixed local
+    positions and their values selecting the sub-block traded with it (the partner's k-bits)."""
+    ks = [k for k, _ in pairs]
+    ls = [l for _, l in pairs]
+    mine = sum(((rank >> k) & 1) << i for i, k in enumerate(ks))
+    out = []
+    for pat in range(1 << len(pairs)):
+        if pat == mine:
+            continue
+        prank = rank
+        for i, k in enumerate(ks):
+            prank = (prank & ~(1 << k)) | (((pat >> i) & 1) << k)
+        out.append((prank, ls, pat))
+    return out
 
-    def __init__(self, n: int, g: int, init: str = "zero", seed: int = 42):
+
+class ChunkedExchange:
+    """The chunk loop of a remap, shared by the backends.  `local` provides rows_per_shard,
+    row_bytes, arena(nbytes) (a flat staging buffer of 8-byte words, allocated once),
+    pack(ls, pat, row0, nrows, buf) and unpack(ls, pat, row0, nrows, buf); `transport` provides
+    start(sends, recvs, peers, nbytes) -> handle and finish(handle).  The staging arena holds two
+    slots of (send, receive) chunk buffers per partner.  Per chunk: pack for every partner, post
+    the transfers, then — while the next chunk is packed into the other slot — wait for the
+    previous chunk and unpack it.  Extra memory: the arena, nothing else."""
+
+    def __init__(self, local, transport, rank: int, staging_bytes: int = DEFAULT_STAGING_BYTES):
+        self.local, self.transport, self.rank = local, transport, rank
+        self.staging_bytes = int(staging_bytes)
+        self.bytes_sent = 0
+        self.chunks = 0
+        self.events = None  # a list: every remap appends its (start, end) CUDA events (measurement)
+
+    def chunk_rows(self, npartners):
+        per = self.staging_bytes // (2 * 2 * npartners)  # 2 slots x (send + recv) per partner
+        rows = max(1, per // self.local.row_bytes)
+        return 1 << (rows.bit_length() - 1)  # power of two: chunks tile the sub-block evenly
+
+    def remap(self, pairs):
+        if not pairs:
+            return
+        groups = remap_groups(self.rank, pairs)
+        sub_rows = self.local.rows_per_shard >> len(pairs)
+        cr = min(sub_rows, self.chunk_rows(len(groups)))
+        words = cr * self.local.row_bytes // 8
+        arena = self.local.arena(4 * len(groups) * words * 8)
+        slots = [[(arena[((s * len(groups) + i) * 2) * words:((s * len(groups) + i) * 2 + 1) * words],
+                   arena[((s * len(groups) + i) * 2 + 1) * words:((s * len(groups) + i) * 2 + 2) * words])
+                  for i in range(len(groups))] for s in range(2)]
+        pending = None
+        ev = None
+        if self.events is not None:
+            import torch
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record()
+        for ci, row0 in enumerate(range(0, sub_rows, cr)):
+            nrows = min(cr, sub_rows - row0)
+            slot = slots[ci & 1]
+            for (prank, ls, pat), (sbuf, _) in zip(groups, slot):
+                self.local.pack(ls, pat, row0, nrows, sbuf)
+            h = self.transport.start([sb for sb, _ in slot], [rb for _, rb in slot], [g[0] for g in groups],
+                                     nrows * self.local.row_bytes)
+            if pending is not None:
+                self._drain(pending)
+            pending = (h, groups, slot, row0, nrows)
+            self.bytes_sent += nrows * self.local.row_bytes * len(groups)
+            self.chunks += 1
+        self._drain(pending)
+        if ev is not None:
+            ev[1].record()
+            self.events.append(ev)
+
+    def _drain(self, pending):
+        h, groups, slot, row0, nrows = pending
+        self.transport.finish(h)
+        for (prank, ls, pat), (_, rbuf) in zip(groups, slot):
+            self.local.unpack(ls, pat, row0, nrows, rbuf)
+
+
+class TorchDistTransport:
+    """Point-to-point transfers over torch.distributed (NCCL on GPUs, gloo in the CPU tests):
+    all partners of a chunk in one batched group; finish() makes the current stream wait (NCCL)
+    or blocks (gloo)."""
+
+    def __init__(self):
+        import torch.distributed as dist
+        self.dist = dist
+
+    def start(self, sends, recvs, peers, nbytes):
+        ops = []
+        for sb, rb, p in zip(sends, recvs, peers):
+            n = nbytes // sb.element_size()
+            ops.append(self.dist.P2POp(self.dist.isend, sb[:n], p))
+            ops.append(self.dist.P2POp(self.dist.irecv, rb[:n], p))
+        return self.dist.batch_isend_irecv(ops)
+
+    def finish(self, works):
+        for w in works:
+            w.wait()
+
+
+class DeviceShardLocal:
+    """A shard = one libqbg register of the local qubits; pack / unpack are libqbg kernels into
+    library-owned staging buffers (viewed as torch tensors for NCCL)."""
+
+    def __init__(self, nl: int, seed: int = 42, dtype: str = "c128"):
         import torch
-        from ._capi import check, lib
         from .register import Register
         self.torch = torch
-        self.n, self.g, self.nl = n, g, n - g
-        check(lib().qbg_set_stream(torch.cuda.current_stream().cuda_stream))
-        # |0...0>: amplitude 1 on rank 0 (all global bits 0), the other shards are zero
-        self.regs = [Register(self.nl, 1, seed) for _ in range(1 << g)]
-        check(lib().qbg_set_zero(self.regs[0]._h))
-        self.views = [self._view(reg) for reg in self.regs]
+        self.nl = nl
+        self.reg = Register(nl, 1, seed, dtype)  # zero-filled by qbg_reg_create
+        self.rows_per_shard = 1 << nl
+        self.elem = 16 if dtype == "c128" else 8
+        self.row_bytes = self.elem  # B = 1
+        self._arena = None
+        self.staging_high_water = 0
 
-    def _view(self, reg):
-        return self.torch.as_tensor(_CudaBuf(reg.device_ptr, 2 << self.nl), device="cuda")
+    def arena(self, nbytes):
+        """The staging arena (library-owned device memory, grown only if a larger one is asked)."""
+        import ctypes
+        from ._capi import check, lib
+        if self._arena is not None and self._arena[1] >= nbytes:
+            return self._arena[2]
+        self.release_staging()
+        ptr = ctypes.c_void_p()
+        check(lib().qbg_buffer_alloc(nbytes, ctypes.byref(ptr)))
+        t = self.torch.as_tensor(_CudaBuf(ptr.value, nbytes // 8), device="cuda")
+        self._arena = (ptr, nbytes, t)
+        self.staging_high_water = max(self.staging_high_water, nbytes)
+        return t
+
+    def release_staging(self):
+        from ._capi import lib
+        if self._arena is not None:
+            lib().qbg_buffer_free(self._arena[0])
+            self._arena = None
+
+    def _fix(self, ls):
+        import ctypes
+        arr = (ctypes.c_int32 * max(1, len(ls)))(*[l + 1 for l in ls])
+        return arr, len(ls)
+
+    def pack(self, ls, pat, row0, nrows, buf):
+        from ._capi import check, lib
+        arr, nf = self._fix(ls)
+        check(lib().qbg_shard_pack(self.reg._h, arr, nf, pat, row0, nrows, buf.data_ptr()))
+
+    def unpack(self, ls, pat, row0, nrows, buf):
+        from ._capi import check, lib
+        arr, nf = self._fix(ls)
+        check(lib().qbg_shard_unpack(self.reg._h, arr, nf, pat, row0, nrows, buf.data_ptr()))
+
+    def set_zero(self, amplitude_one: bool):
+        from ._capi import check, lib
+        if amplitude_one:
+            check(lib().qbg_set_zero(self.reg._h))
+        else:
+            self.reg.scale(0.0)
+
+    def apply(self, lops):
+        apply_lops(self.reg, lops)
+
+    def expect(self, terms) -> float:
+        return expect_terms(self.reg, terms)
+
+    def amplitudes(self) -> np.ndarray:
+        return self.reg.state()[0]
+
+
+class DistShardBackend:
+    """One shard per rank; exchanges through `transport`.  The product configuration is
+    DeviceNcclBackend (libqbg shard, NCCL); the CPU tests run this class with a gloo transport
+    and a CPU shard, so the chunk loop, staging and transfers they check are this code."""
+
+    def __init__(self, local, transport, rank: int, world: int, g: int, staging_bytes: int = DEFAULT_STAGING_BYTES,
+                 allreduce=None):
+        if world != 1 << g:
+            raise errors.ValidationError("sharded: world size must be 2^g")
+        self.local, self.rank, self.world, self.g = local, rank, world, g
+        self.exchange = ChunkedExchange(local, transport, rank, staging_bytes)
+        self._allreduce = allreduce
+        self.set_zero()
+
+    def set_zero(self):
+        self.local.set_zero(self.rank == 0)
+
+    def remap(self, pairs):
+        self.exchange.remap(pairs)
 
     def apply_local(self, rank_ops):
-        for r, reg in enumerate(self.regs):
-            apply_lops(reg, rank_ops(r))
-
-    def swap(self, k, l):
-        for r in range(1 << self.g):
-            if (r >> k) & 1:
-                continue
-            p = r | (1 << k)
-            a = _half_view(self.views[r], self.nl, l, 1)   # rank bit 0 sends its l = 1 half
-            b = _half_view(self.views[p], self.nl, l, 0)   # partner (bit 1) sends its l = 0 half
-            tmp = a.clone()
-            a.copy_(b)
-            b.copy_(tmp)
+        self.local.apply(rank_ops(self.rank))
 
     def expect_local(self, local_terms):
-        total = 0.0
-        for r, reg in enumerate(self.regs):
-            total += float(expect_terms(reg, local_terms(r)))
-        return total
+        return float(self.local.expect(local_terms(self.rank)))
+
+    def reduce_sum(self, v: float) -> float:
+        return self._allreduce(v) if self._allreduce else v
 
     def gather(self):
-        return [reg.state()[0] for reg in self.regs]
+        import torch
+        import torch.distributed as dist
+        mine = torch.from_numpy(np.ascontiguousarray(self.local.amplitudes()).view(np.float64).copy())
+        out = [torch.zeros_like(mine) for _ in range(self.world)]
+        dist.all_gather(out, mine)
+        return [o.numpy().view(np.complex128) for o in out]
 
 
-class DeviceNcclBackend:
-    """One shard per rank (this process's GPU); exchanges with NCCL over NVLink via
-    torch.distributed (zero-copy views of the shard register)."""
+def _nccl_allreduce(v: float) -> float:
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return float(t.item())
 
-    def __init__(self, n: int, g: int, init: str = "zero", seed: int = 42):
+
+class DeviceNcclBackend(DistShardBackend):
+    """One shard per process / GPU (libqbg register), exchanges with NCCL send/recv over NVLink
+    through torch.distributed, staged in library-owned chunk buffers."""
+
+    def __init__(self, n: int, g: int, seed: int = 42, dtype: str = "c128", staging_bytes: int = DEFAULT_STAGING_BYTES):
         import torch
         import torch.distributed as dist
         from ._capi import check, lib
-        from .register import Register
-        self.torch, self.dist = torch, dist
-        self.n, self.g, self.nl = n, g, n - g
-        self.rank, self.world = dist.get_rank(), dist.get_world_size()
-        if self.world != 1 << g:
-            raise errors.ValidationError("sharded: world size must be 2^g")
         check(lib().qbg_set_stream(torch.cuda.current_stream().cuda_stream))
-        self.reg = Register(self.nl, 1, seed)  # zero-filled by qbg_reg_create
-        if self.rank == 0:
-            check(lib().qbg_set_zero(self.reg._h))
-        self.view = torch.as_tensor(_CudaBuf(self.reg.device_ptr, 2 << self.nl), device="cuda")
-
-    def apply_local(self, rank_ops):
-        apply_lops(self.reg, rank_ops(self.rank))
-
-    def swap(self, k, l):
-        b = (self.rank >> k) & 1
-        part = self.rank ^ (1 << k)
-        mine = _half_view(self.view, self.nl, l, 1 - b)
-        send = mine.contiguous()
-        recv = self.torch.empty_like(send)
-        ops = [self.dist.P2POp(self.dist.isend, send, part), self.dist.P2POp(self.dist.irecv, recv, part)]
-        for w in self.dist.batch_isend_irecv(ops):
-            w.wait()
-        mine.copy_(recv)
-
-    def expect_local(self, local_terms):
-        e = self.torch.tensor([float(expect_terms(self.reg, local_terms(self.rank)))], dtype=self.torch.float64,
-                              device="cuda")
-        self.dist.all_reduce(e)
-        return float(e.item())
+        rank, world = (dist.get_rank(), dist.get_world_size()) if dist.is_initialized() else (0, 1)
+        self.n, self.nl = n, n - g
+        super().__init__(DeviceShardLocal(n - g, seed, dtype), TorchDistTransport(), rank, world, g, staging_bytes,
+                         allreduce=_nccl_allreduce if world > 1 else None)
 
     def gather(self):
-        out = [self.torch.zeros_like(self.view) for _ in range(self.world)]
-        self.dist.all_gather(out, self.view.contiguous())
+        import torch
+        import torch.distributed as dist
+        v = self.local.reg.state()[0]
+        mine = torch.from_numpy(np.ascontiguousarray(v).view(np.float64).copy()).cuda()
+        out = [torch.zeros_like(mine) for _ in range(self.world)]
+        dist.all_gather(out, mine)
         return [o.cpu().numpy().view(np.complex128) for o in out]
+
+
+class DeviceVirtualBackend:
+    """All 2^g shards as libqbg registers on the current GPU; a remap runs the same chunked
+    pack / unpack kernels, each rank unpacking straight from its partner's packed chunk."""
+
+    def __init__(self, n: int, g: int, seed: int = 42, dtype: str = "c128", staging_bytes: int = DEFAULT_STAGING_BYTES):
+        import torch
+        from ._capi import check, lib
+        check(lib().qbg_set_stream(torch.cuda.current_stream().cuda_stream))
+        self.n, self.g, self.nl = n, g, n - g
+        self.locals = [DeviceShardLocal(self.nl, seed, dtype) for _ in range(1 << g)]
+        self.staging_bytes = staging_bytes
+        self.bytes_moved = 0
+        self.set_zero()
+
+    def set_zero(self):
+        for r, lo in enumerate(self.locals):
+            lo.set_zero(r == 0)
+
+    def remap(self, pairs):
+        if not pairs:
+            return
+        G = 1 << self.g
+        sub_rows = (1 << self.nl) >> len(pairs)
+        npart = (1 << len(pairs)) - 1
+        per = self.staging_bytes // (G * npart)  # one packed chunk per (rank, partner)
+        cr = max(1, per // self.locals[0].row_bytes)
+        cr = min(sub_rows, 1 << (cr.bit_length() - 1))
+        words = cr * self.locals[0].row_bytes // 8
+        groups = [remap_groups(r, pairs) for r in range(G)]
+        arenas = [lo.arena(npart * words * 8) for lo in self.locals]
+        for row0 in range(0, sub_rows, cr):
+            nrows = min(cr, sub_rows - row0)
+            bufs = {}
+            for r in range(G):
+                for i, (prank, ls, pat) in enumerate(groups[r]):
+                    b = arenas[r][i * words:(i + 1) * words]
+                    self.locals[r].pack(ls, pat, row0, nrows, b)
+                    bufs[(r, prank)] = b
+            for r in range(G):  # each rank unpacks its partner's packed chunk in place
+                for prank, ls, pat in groups[r]:
+                    self.locals[r].unpack(ls, pat, row0, nrows, bufs[(prank, r)])
+                    self.bytes_moved += nrows * self.locals[r].row_bytes
+
+    def apply_local(self, rank_ops):
+        for r, lo in enumerate(self.locals):
+            lo.apply(rank_ops(r))
+
+    def expect_local(self, local_terms):
+        return sum(float(lo.expect(local_terms(r))) for r, lo in enumerate(self.locals))
+
+    def reduce_sum(self, v: float) -> float:
+        return v
+
+    def gather(self):
+        return [lo.amplitudes() for lo in self.locals]
 
 
 # ---- helpers ----------------------------------------------------------------------------------------
@@ -392,6 +692,18 @@ class _CudaBuf:
     def __init__(self, ptr: int, n: int):
         self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3,
                                          "strides": None}
+
+
+def _lops_key(nqubits, lops):
+    import hashlib
+    h = hashlib.blake2b(digest_size=16)
+    h.update(str(nqubits).encode())
+    for o in lops:
+        h.update(repr((o.kind, o.targets, o.ctrls, o.cfg)).encode())
+        h.update(np.ascontiguousarray(o.mat, dtype=complex).tobytes())
+        if o.perm is not None:
+            h.update(np.ascontiguousarray(o.perm, dtype=np.int64).tobytes())
+    return h.digest()
 
 
 def lops_program(nqubits: int, lops):
@@ -426,32 +738,62 @@ def lops_program(nqubits: int, lops):
     return h
 
 
+class _ProgCache:
+    """Compiled segment programs by content (a repeated step re-uses its plans and kernels)."""
+
+    def __init__(self, cap=512):
+        from collections import OrderedDict
+        self.d, self.cap = OrderedDict(), cap
+
+    def get(self, nqubits, lops):
+        from ._capi import lib
+        k = _lops_key(nqubits, lops)
+        h = self.d.get(k)
+        if h is not None:
+            self.d.move_to_end(k)
+            return h
+        h = lops_program(nqubits, lops)
+        self.d[k] = h
+        while len(self.d) > self.cap:
+            _, old = self.d.popitem(last=False)
+            lib().qbg_prog_destroy(old)
+        return h
+
+
+_PROGS = _ProgCache()
+
+
 def apply_lops(reg, lops):
     """Applies realised local ops to a libqbg register as one fused program."""
     from ._capi import check, lib
     if not lops:
         return
-    h = lops_program(reg.nqubits, lops)
-    try:
-        check(lib().qbg_apply(reg._h, h))
-    finally:
-        lib().qbg_prog_destroy(h)
+    check(lib().qbg_apply(reg._h, _PROGS.get(reg.nqubits, lops)))
+
+
+_OBS = {}
 
 
 def expect_terms(reg, terms) -> float:
-    """Re Σ c <ψ|P|ψ> for Pauli terms given as (c, xmask, zmask) over the register's qubits."""
+    """Re Σ c <ψ|P|ψ> for Pauli terms given as (c, xmask, zmask) over the register's qubits; the
+    compiled observable (and its seed plans) is cached by content."""
     import ctypes
     from ._capi import QbgPauliTerm, check, lib
     if not terms:
         return 0.0
-    arr = (QbgPauliTerm * len(terms))()
-    for k, (c, x, z) in enumerate(terms):
-        arr[k] = QbgPauliTerm(complex(c).real, complex(c).imag, x, z)
-    h = ctypes.c_void_p()
-    check(lib().qbg_obs_create(reg.nqubits, arr, len(terms), ctypes.byref(h)))
-    try:
-        out = np.empty(reg.nbatch)
-        check(lib().qbg_expect(reg._h, h, out.ctypes.data))
-    finally:
-        lib().qbg_obs_destroy(h)
+    key = (reg.nqubits, tuple((complex(c), int(x), int(z)) for c, x, z in terms))
+    h = _OBS.get(key)
+    if h is None:
+        arr = (QbgPauliTerm * len(terms))()
+        for k, (c, x, z) in enumerate(terms):
+            arr[k] = QbgPauliTerm(complex(c).real, complex(c).imag, x, z)
+        h = ctypes.c_void_p()
+        check(lib().qbg_obs_create(reg.nqubits, arr, len(terms), ctypes.byref(h)))
+        if len(_OBS) > 256:
+            for old in _OBS.values():
+                lib().qbg_obs_destroy(old)
+            _OBS.clear()
+        _OBS[key] = h
+    out = np.empty(reg.nbatch)
+    check(lib().qbg_expect(reg._h, h, out.ctypes.data))
     return float(out.sum())

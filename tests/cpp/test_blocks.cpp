@@ -42,9 +42,24 @@ int main(int argc, char** argv) {
         for (int k = 0; k < 3; ++k) CHECK(std::abs(r.param_grads[k] - want[k]) <= 1e-12);
         // expect through the pair form agrees with the forward value of expect'
         CHECK(std::abs(qb::expect(h, qb::zero_state(3), circ)[0] - r.energies[0]) <= 1e-13);
-        // shift rule (exact mode) = reverse mode (gradient triangle)
-        auto fg = qb::faithful_grad(h, qb::zero_state(3), circ);
-        for (int k = 0; k < 3; ++k) CHECK(std::abs(fg[k] - r.param_grads[k]) <= 1e-10);
+        // the controlled Ry has no shift rule (generator P1 ⊗ Y is not reflexive): rejected
+        bool threw = false;
+        try {
+            qb::faithful_grad(h, qb::zero_state(3), circ);
+        } catch (const qb::UnsupportedError&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
+    // shift rule (exact mode) = reverse mode on an all-rotation circuit (gradient triangle)
+    {
+        auto c = qb::variational_circuit(4, 2);
+        qb::Rng rng(3);
+        qb::dispatch(c, "random", rng);
+        auto h = qb::heisenberg(4);
+        auto r = qb::expect_grad(h, qb::rand_state(4, 2, 1), c);
+        auto fg = qb::faithful_grad(h, qb::rand_state(4, 2, 1), c);
+        for (std::size_t k = 0; k < fg.size(); ++k) CHECK(std::abs(fg[k] - r.param_grads[k]) <= 1e-12);
     }
     // SPEC.md:459 / 469: <Z> after Rx(0.4) = cos 0.4, θ̄ = −sin 0.4; heisenberg(2) on |00> = 1
     {

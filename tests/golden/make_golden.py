@@ -36,13 +36,13 @@ def random_gate(rng: np.random.Generator, t: int):
     return M.Dense(q)
 
 
-def instruct_cases(ref, count=240, seed=1234):
+def instruct_cases(ref, count=240, seed=1234, tmin=1, tmax=3, nmax=6):
     rng = np.random.default_rng(seed)
     rows = []
     for _ in range(count):
-        n = int(rng.integers(2, 7))
+        n = int(rng.integers(max(2, tmin), nmax + 1))
         B_ = int(rng.integers(1, 4))
-        t = int(rng.integers(1, min(3, n) + 1))
+        t = int(rng.integers(tmin, min(tmax, n) + 1))
         nc = int(rng.integers(0, min(2, n - t) + 1))
         qs = rng.permutation(np.arange(1, n + 1))
         locs, ctrls = [int(v) for v in qs[:t]], [int(v) for v in qs[t:t + nc]]
@@ -74,6 +74,12 @@ def main():
     for k, r in enumerate(rows):
         obj[k] = r
     np.save(os.path.join(OUT, "instruct_cases.npy"), obj, allow_pickle=True)
+    # 4- and 5-qubit gates (the dense fallback's widest blocks, register.hpp:371-384)
+    rows = instruct_cases(ref, count=80, seed=4545, tmin=4, tmax=5, nmax=8)
+    obj = np.empty(len(rows), dtype=object)
+    for k, r in enumerate(rows):
+        obj[k] = r
+    np.save(os.path.join(OUT, "instruct_cases_t45.npy"), obj, allow_pickle=True)
 
     # 2. Rng / dispatch("random") / rand_state
     r = ref.rng(42)

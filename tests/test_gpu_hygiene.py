@@ -85,6 +85,7 @@ def test_aot_kernel_cache_serves_a_fresh_process():
         import paper_1912_10877_b200 as qb
         from paper_1912_10877_b200._capi import lib
         c = qb.variational_circuit(25, 10); qb.dispatch(c, "random", rng=qb.Rng(42))
+        qb.zero_state(1); qb.synchronize()  # CUDA context creation is not the engine's first step
         t0 = time.perf_counter()
         qb.expect_grad(qb.heisenberg(25), (qb.zero_state(25), c)); qb.synchronize()
         t1 = time.perf_counter()

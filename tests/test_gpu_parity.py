@@ -56,6 +56,15 @@ def test_instruct_reference_goldens(golden):
         assert rel(reg.state(), c["out"]) < TOL
 
 
+def test_instruct_t45_reference_goldens(golden, fusion):
+    """4- and 5-qubit gates (dense / diagonal / permutation, with controls and batches) through the
+    per-gate kernels and the fused engine's fallback, vs the reference's own outputs."""
+    for c in golden("instruct_cases_t45.npy"):
+        reg = qb.Register(c["n"], c["B"]).set_state(c["inp"])
+        qb.instruct(reg, gate_of(c), c["locs"], c["ctrls"], c["cfg"])
+        assert rel(reg.state(), c["out"]) < TOL
+
+
 @pytest.mark.parametrize("tag,params", [("X", ()), ("Y", ()), ("Z", ()), ("H", ()), ("S", ()), ("Sdag", ()),
                                         ("T", ()), ("Tdag", ()), ("I2", ()), ("P0", ()), ("P1", ()), ("Pu", ()),
                                         ("Pd", ()), ("Rx", (0.5,)), ("Ry", (1.1,)), ("Rz", (2.3,)),

@@ -66,6 +66,56 @@ def random_circuit(n, ngates, seed):
     return B.chain(n, *blocks)
 
 
+def wide_circuit(n, ngates, seed):
+    """Random circuits with 3-, 4- and 5-qubit blocks: dense unitaries, controlled dense blocks and
+    rotations whose generators act on 3-5 qubits (forward and reverse through t <= 5)."""
+    rng = np.random.default_rng(seed)
+    blocks = []
+
+    def locs(k):
+        return tuple(int(v) for v in rng.choice(np.arange(1, n + 1), size=k, replace=False))
+
+    paulis = [B.X, B.Y, B.Z]
+    for _ in range(ngates):
+        kind = rng.integers(0, 5)
+        th = float(rng.uniform(0, 2 * np.pi))
+        t = int(rng.integers(3, 6))
+        if kind == 0:
+            blocks.append(B.put(n, locs(t), B.matblock(unitary(rng, 1 << t))))
+        elif kind == 1:
+            q = locs(t + 1)
+            blocks.append(B.control(n, q[t], q[:t], B.matblock(unitary(rng, 1 << t))))
+        elif kind == 2:
+            gen = B.kron(*[paulis[int(rng.integers(0, 3))] for _ in range(t)])
+            blocks.append(B.put(n, locs(t), B.rot(gen, th)))
+        elif kind == 3:
+            q = locs(t + 1)
+            gen = B.kron(*[paulis[int(rng.integers(0, 3))] for _ in range(t)])
+            blocks.append(B.control(n, -q[t], q[:t], B.rot(gen, th)))
+        else:
+            blocks.append(B.put(n, locs(1)[0], [B.Rx, B.Ry, B.Rz][rng.integers(0, 3)](th)))
+    return B.chain(n, *blocks)
+
+
+@pytest.mark.parametrize("n,ngates,nb,seed", [(7, 30, 1, 71), (12, 40, 2, 72), (16, 30, 1, 73)])
+def test_wide_gates_forward_and_grad(orc, n, ngates, nb, seed):
+    """expect' through 3-5-qubit gates (reverse mode with t <= 5 and 5-qubit generators) vs the oracle."""
+    circ = wide_circuit(n, ngates, seed)
+    th = B.parameters(circ)
+    em = lowered(circ)
+    st = orc.rand_state(n, nb, seed)
+    want = orc.apply_program(st, n, em, th)
+    reg = qb.Register(n, nb).set_state(st)
+    qb.apply(reg, circ)
+    assert rel(reg.state(), want) < TOL
+    h = C.heisenberg(n)
+    e, g, _, sg = orc.expect_grad(st, n, em, th, B.pauli_terms(h))
+    res = qb.expect_grad(h, (qb.Register(n, nb).set_state(st), circ), want_state_grad=True)
+    assert np.abs(res.energies - e).max() <= TOL * max(1.0, np.abs(e).max())
+    assert np.abs(res.param_grads - g).max() <= TOL * max(1.0, np.abs(g).max())
+    assert rel(res.state_grad.state(), sg) < TOL
+
+
 CASES = [(5, 60, 1, 1), (9, 120, 2, 2), (12, 150, 1, 3), (14, 200, 4, 4), (20, 250, 1, 5), (22, 160, 1, 6)] + \
     [(n, 120, nb, 10 + s) for s, (n, nb) in enumerate([(12, 1), (13, 2), (14, 1), (15, 3), (16, 1), (16, 8),
                                                       (17, 1), (12, 32), (11, 1), (11, 4), (13, 6)])]

@@ -34,6 +34,15 @@ def test_instruct_matches_reference_goldens(orc, golden):
         assert np.array_equal(out, c["out"]), (c["n"], c["locs"], c["ctrls"])
 
 
+def test_instruct_t45_goldens_bit_exact(orc, golden):
+    """4- and 5-qubit gates (the widest dense blocks, register.hpp:371-384), reference-generated."""
+    cases = golden("instruct_cases_t45.npy")
+    assert len(cases) >= 60 and {len(c["locs"]) for c in cases} == {4, 5}
+    for c in cases:
+        out = orc.instruct(c["inp"], c["n"], gate_of(c), c["locs"], c["ctrls"], c["cfg"])
+        assert np.array_equal(out, c["out"]), (c["n"], c["locs"], c["ctrls"])
+
+
 def test_rng_and_rand_state_bit_exact(orc, golden):
     g = golden("rng.npz")
     r = orc.rng(42)
