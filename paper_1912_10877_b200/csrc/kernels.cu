@@ -9,6 +9,7 @@
 // every target stride.  Used for single instruct calls and as the fallback of the fused
 // engine (fused.cu) for gates it does not tile (t >= 3).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "engine.h"
@@ -513,6 +514,13 @@ Gate adjoint(const Gate& g) {
 
 void launch_gate(const DevState& s, const Gate& g) {
     if (g.kind == QBG_MAT_IDENTITY) return;
+    // 3..5-qubit non-diagonal gates in complex128: the FP64 tensor-core kernel (dense_mma.cu);
+    // QBG_DENSE_MMA=0 keeps the CUDA-core per-gate kernel (A/B, profiles/r02_dense)
+    static const bool mma = [] {
+        const char* e = std::getenv("QBG_DENSE_MMA");
+        return !(e && e[0] == '0');
+    }();
+    if (mma && g.t >= 3 && g.kind == QBG_MAT_DENSE && launch_dense_mma(s, g)) return;
     if (s.dtype == QBG_C128)
         dispatch_t<double2>(s, g);
     else

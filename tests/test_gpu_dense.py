@@ -1,0 +1,50 @@
+"""Dense 3..5-qubit blocks on the FP64 tensor cores (dense_mma.cu, DMMA m8n8k4) and gate fusion
+into dense k-qubit blocks (densefuse.py, BASELINE cfg 4), vs the CPU oracle (1e-12)."""
+import numpy as np
+import pytest
+
+import paper_1912_10877_b200 as qb
+from paper_1912_10877_b200 import blocks as B
+from paper_1912_10877_b200.densefuse import fuse_dense
+
+from test_gpu_parity import lowered, rel
+from test_gpu_random_circuits import unitary
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def per_gate():
+    qb.set_fusion(False)  # every dense 3..5-qubit gate is its own launch of the DMMA kernel
+    yield
+    qb.set_fusion(True)
+
+
+@pytest.mark.parametrize("n,nb", [(9, 1), (12, 2), (16, 1), (10, 4)])
+def test_dense_blocks_every_placement(orc, per_gate, n, nb):
+    rng = np.random.default_rng(n * 10 + nb)
+    blocks = []
+    for t in (3, 4, 5):
+        for locs in [tuple(range(1, t + 1)), tuple(range(n - t + 1, n + 1)),
+                     tuple(int(v) for v in rng.choice(np.arange(1, n + 1), size=t, replace=False))]:
+            blocks.append(B.put(n, locs, B.matblock(unitary(rng, 1 << t))))
+        q = [int(v) for v in rng.choice(np.arange(1, n + 1), size=t + 2, replace=False)]
+        blocks.append(B.control(n, (q[t], -q[t + 1]), tuple(q[:t]), B.matblock(unitary(rng, 1 << t))))
+    circ = B.chain(n, *blocks)
+    st = orc.rand_state(n, nb, n)
+    want = orc.apply_program(st, n, lowered(circ), B.parameters(circ))
+    reg = qb.Register(n, nb).set_state(st)
+    qb.apply(reg, circ)
+    assert rel(reg.state(), want) < 1e-12
+
+
+@pytest.mark.parametrize("n,d,k", [(12, 3, 5), (14, 2, 4), (13, 2, 3)])
+def test_fuse_dense_variational(orc, per_gate, n, d, k):
+    circ = qb.variational_circuit(n, d)
+    qb.dispatch(circ, "random", rng=qb.Rng(n))
+    fused = fuse_dense(circ, k)
+    assert all(len(b.locs) <= k for b in fused.blocks)
+    want = orc.apply_program(orc.zero_state(n), n, lowered(circ), B.parameters(circ))
+    reg = qb.zero_state(n)
+    qb.apply(reg, fused)
+    assert rel(reg.state(), want) < 1e-12
