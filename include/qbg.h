@@ -128,6 +128,11 @@ int qbg_set_stream(void* stream);
 int qbg_synchronize(void);
 /* Fusion switch: 1 (default) = tiled multi-gate passes, 0 = one kernel per gate. */
 int qbg_set_fusion(int32_t enabled);
+/* Kernel for dense 3..5-qubit gates (register.hpp:371-384 as one GEMM over all bases):
+   1 (default) FP64 tensor cores, DMMA m8n8k4 (complex64 is widened to FP64 and rounded once);
+   2 complex64 on tcgen05 kind::tf32 with a 3-piece operand split (faster; the tensor cores' fp32
+   accumulation drifts the norm by ~6e-7 per block); 0 the CUDA-core per-gate kernel. */
+int qbg_set_dense_path(int32_t path);
 /* Per-kernel CUDA-event timing of the library's own launches (measurement hook). */
 int qbg_profile_enable(int32_t enabled);
 int qbg_profile_reset(void);

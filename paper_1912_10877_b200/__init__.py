@@ -23,6 +23,16 @@ def set_fusion(enabled: bool) -> None:
     lib().qbg_set_fusion(1 if enabled else 0)
 
 
+DENSE_PATHS = {"cuda": 0, "fp64-tensor": 1, "tf32-tensor": 2}
+
+
+def set_dense_path(path: str) -> None:
+    """Kernel for dense 3..5-qubit gates: "fp64-tensor" (default; DMMA, complex64 widened to FP64),
+    "tf32-tensor" (complex64 on tcgen05 kind::tf32, 3-piece split) or "cuda" (CUDA cores)."""
+    from ._capi import check
+    check(lib().qbg_set_dense_path(DENSE_PATHS[path]))
+
+
 def synchronize() -> None:
     from ._capi import check
     check(lib().qbg_synchronize())

@@ -598,6 +598,12 @@ int qbg_synchronize(void) {
         stream_sync();
     });
 }
+int qbg_set_dense_path(int32_t path) {
+    return guarded([&] {
+        if (path < 0 || path > 2) raise(QBG_ERR_VALIDATION, "dense path must be 0 (CUDA cores), 1 (FP64 tensor cores) or 2 (tcgen05 TF32)");
+        set_dense_path(path);
+    });
+}
 int qbg_set_fusion(int32_t on) {
     g_fusion = on != 0;
     return QBG_OK;

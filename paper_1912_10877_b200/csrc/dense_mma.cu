@@ -17,6 +17,7 @@
 // real matrix sits in shared memory (row stride padded by 4 doubles: conflict-free fragments).
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 #include <vector>
 
 #include "engine.h"
@@ -43,8 +44,10 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                  : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
 
-template <int T>
-__global__ void __launch_bounds__(kWarps * 32) k_dense_mma(double2* __restrict__ st, const double* __restrict__ areal,
+// V = double2 (complex128) or float2 (complex64: widened to FP64 in shared memory, one rounding
+// on the store — more accurate than an FP32 GEMM and free on an FP64-bound kernel)
+template <int T, typename V>
+__global__ void __launch_bounds__(kWarps * 32) k_dense_mma(V* __restrict__ st, const double* __restrict__ areal,
                                                           const __grid_constant__ MmaArgs a) {
     constexpr int D = 1 << T, KR = 2 * D, MB = KR / 8, KS = KR / 4;
     constexpr int AS = KR + 4;  // padded row stride (doubles) of the real matrix and of a column
@@ -76,9 +79,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_dense_mma(double2* __restrict__
             uint64_t off;
             int slot;
             where(e, off, slot);
-            const double2 v = st[base + off];
-            sc[slot] = v.x;
-            sc[slot + 1] = v.y;
+            const V v = st[base + off];
+            sc[slot] = static_cast<double>(v.x);
+            sc[slot + 1] = static_cast<double>(v.y);
         }
         __syncwarp();
         double acc[2][MB][2];
@@ -113,7 +116,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_dense_mma(double2* __restrict__
             uint64_t off;
             int slot;
             where(e, off, slot);
-            st[base + off] = make_double2(sc[slot], sc[slot + 1]);
+            V r;
+            r.x = static_cast<typename real_of<V>::type>(sc[slot]);
+            r.y = static_cast<typename real_of<V>::type>(sc[slot + 1]);
+            st[base + off] = r;
         }
         __syncwarp();
     }
@@ -121,10 +127,10 @@ __global__ void __launch_bounds__(kWarps * 32) k_dense_mma(double2* __restrict__
 
 }  // namespace
 
-// true when the gate ran on the tensor-core kernel (c128, dense-able 3..5-qubit gate, power-of-two
-// batch, finite matrix, enough free bits for a 16-column warp tile)
+// true when the gate ran on the tensor-core kernel (dense-able 3..5-qubit gate, power-of-two batch,
+// finite matrix, enough free bits for a 16-column warp tile); complex64 computes in FP64 too
 bool launch_dense_mma(const DevState& s, const Gate& g) {
-    if (s.dtype != QBG_C128 || g.t < 3 || g.t > 5 || g.kind == QBG_MAT_IDENTITY) return false;
+    if (g.t < 3 || g.t > 5 || g.kind == QBG_MAT_IDENTITY) return false;
     if (s.B & (s.B - 1)) return false;
     int bb = 0;
     while ((int64_t{1} << bb) < s.B) ++bb;
@@ -185,30 +191,28 @@ bool launch_dense_mma(const DevState& s, const Gate& g) {
     const size_t smem = static_cast<size_t>(KR * AS + kWarps * kCols * AS) * sizeof(double);
     const uint64_t want = (a.ntiles + kWarps - 1) / kWarps;
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(want, static_cast<uint64_t>(num_sms()) * 2));
-    auto* p = static_cast<double2*>(s.ptr);
-    // algorithmic work of the processed columns: 2 x 16 B per amplitude, 8 D^2 flop per column
+    // algorithmic work of the processed columns: 2 x element bytes per amplitude, 8 D^2 flop per column
     const double cols = static_cast<double>(a.ntiles) * kCols;
-    LaunchScope ls("dense_mma", 2.0 * 16.0 * D * cols, 8.0 * D * D * cols);
-    static bool attr_set[6] = {false, false, false, false, false, false};
-    auto attr = [&](const void* k) {
-        if (!attr_set[g.t]) {
-            QBG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-            attr_set[g.t] = true;
-        }
+    LaunchScope ls("dense_mma", 2.0 * s.elem() * D * cols, 8.0 * D * D * cols);
+    auto go = [&](auto* p) {
+        using V = std::remove_pointer_t<decltype(p)>;
+        static bool attr_set[6] = {false, false, false, false, false, false};
+        auto run = [&](auto kern) {
+            if (!attr_set[g.t]) {
+                QBG_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(kern), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(smem)));
+                attr_set[g.t] = true;
+            }
+            kern<<<grid, kWarps * 32, smem, stream()>>>(p, d_ar, a);
+        };
+        if (g.t == 3) run(k_dense_mma<3, V>);
+        else if (g.t == 4) run(k_dense_mma<4, V>);
+        else run(k_dense_mma<5, V>);
     };
-    switch (g.t) {
-        case 3:
-            attr(reinterpret_cast<const void*>(k_dense_mma<3>));
-            k_dense_mma<3><<<grid, kWarps * 32, smem, stream()>>>(p, d_ar, a);
-            break;
-        case 4:
-            attr(reinterpret_cast<const void*>(k_dense_mma<4>));
-            k_dense_mma<4><<<grid, kWarps * 32, smem, stream()>>>(p, d_ar, a);
-            break;
-        default:
-            attr(reinterpret_cast<const void*>(k_dense_mma<5>));
-            k_dense_mma<5><<<grid, kWarps * 32, smem, stream()>>>(p, d_ar, a);
-    }
+    if (s.dtype == QBG_C128)
+        go(static_cast<double2*>(s.ptr));
+    else
+        go(static_cast<float2*>(s.ptr));
     QBG_CUDA(cudaGetLastError());
     return true;
 }

@@ -37,9 +37,13 @@ bool is_diagonal(const Gate& g);  // IDENTITY or DIAGONAL
 
 // ---- generic per-gate kernels (register.hpp:352-385 on the device) --------------------
 void launch_gate(const DevState& s, const Gate& g);
+int dense_path();            // qbg_set_dense_path
+void set_dense_path(int p);
 // 3..5-qubit gate as a GEMM on the FP64 tensor cores (DMMA); false when not applicable (c64,
 // non-power-of-two batch, non-finite matrix, too few free bits) — the caller falls back
 bool launch_dense_mma(const DevState& s, const Gate& g);
+// the same on tcgen05 (kind::tf32, 3xTF32 split, TMEM accumulators) for complex64 registers
+bool launch_dense_tc(const DevState& s, const Gate& g);
 // Reverse step of one gate on (psi, adj): grad_slot (if >= 0) receives, per block, the
 // partial Im <adj| K |psi> (K restricted to the control subspace) BEFORE the uncompute;
 // then psi <- U^† psi, adj <- U^† adj with U^† = gdag.

@@ -9,6 +9,7 @@
 // every target stride.  Used for single instruct calls and as the fallback of the fused
 // engine (fused.cu) for gates it does not tile (t >= 3).
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 
@@ -512,15 +513,21 @@ Gate adjoint(const Gate& g) {
     return a;
 }
 
+namespace {
+std::atomic<int> g_dense_path{1};
+}
+int dense_path() { return g_dense_path.load(); }
+void set_dense_path(int p) { g_dense_path.store(p); }
+
 void launch_gate(const DevState& s, const Gate& g) {
     if (g.kind == QBG_MAT_IDENTITY) return;
-    // 3..5-qubit non-diagonal gates in complex128: the FP64 tensor-core kernel (dense_mma.cu);
-    // QBG_DENSE_MMA=0 keeps the CUDA-core per-gate kernel (A/B, profiles/r02_dense)
-    static const bool mma = [] {
-        const char* e = std::getenv("QBG_DENSE_MMA");
-        return !(e && e[0] == '0');
-    }();
-    if (mma && g.t >= 3 && g.kind == QBG_MAT_DENSE && launch_dense_mma(s, g)) return;
+    // dense 3..5-qubit gates (qbg_set_dense_path): 1 (default) the FP64 tensor cores (dense_mma.cu,
+    // complex64 widened to FP64), 2 complex64 on tcgen05 (kind::tf32, 3-piece split, dense_tc.cu;
+    // faster than the CUDA cores but the tensor cores' fp32 accumulation drifts the norm by ~6e-7
+    // per block, profiles/r02/cfg4_30q_dense_ab_c64.jsonl), 0 the CUDA-core kernel below
+    const int path = dense_path();
+    if (path == 2 && g.t >= 3 && g.kind == QBG_MAT_DENSE && launch_dense_tc(s, g)) return;
+    if (path >= 1 && g.t >= 3 && g.kind == QBG_MAT_DENSE && launch_dense_mma(s, g)) return;
     if (s.dtype == QBG_C128)
         dispatch_t<double2>(s, g);
     else

@@ -48,3 +48,39 @@ def test_fuse_dense_variational(orc, per_gate, n, d, k):
     reg = qb.zero_state(n)
     qb.apply(reg, fused)
     assert rel(reg.state(), want) < 1e-12
+
+
+@pytest.mark.parametrize("n,nb", [(11, 1), (13, 2), (12, 4)])
+@pytest.mark.parametrize("path", ["tf32-tensor", "fp64-tensor", "cuda"])
+def test_dense_blocks_c64_paths(orc, per_gate, n, nb, path):
+    """complex64 dense 3..5-qubit blocks through every dense path — tcgen05 (kind::tf32, 3-piece
+    split), the FP64 tensor cores (widened), the CUDA cores — within 1e-5 of the complex128 oracle
+    (plain TF32 would be ~1e-3)."""
+    qb.set_dense_path(path)
+    rng = np.random.default_rng(n * 7 + nb)
+    blocks = []
+    for t in (3, 4, 5):
+        for locs in [tuple(range(1, t + 1)), tuple(range(n - t + 1, n + 1)),
+                     tuple(int(v) for v in rng.choice(np.arange(1, n + 1), size=t, replace=False))]:
+            blocks.append(B.put(n, locs, B.matblock(unitary(rng, 1 << t))))
+        q = [int(v) for v in rng.choice(np.arange(1, n + 1), size=t + 2, replace=False)]
+        blocks.append(B.control(n, (q[t], -q[t + 1]), tuple(q[:t]), B.matblock(unitary(rng, 1 << t))))
+    circ = B.chain(n, *blocks)
+    st = orc.rand_state(n, nb, n)
+    want = orc.apply_program(st, n, lowered(circ), B.parameters(circ))
+    try:
+        reg = qb.Register(n, nb, dtype="c64").set_state(st)
+        qb.apply(reg, circ)
+    finally:
+        qb.set_dense_path("fp64-tensor")
+    assert rel(reg.state(), want) < 1e-5
+
+
+def test_fuse_dense_variational_c64(orc, per_gate):
+    n = 14
+    circ = qb.variational_circuit(n, 3)
+    qb.dispatch(circ, "random", rng=qb.Rng(3))
+    want = orc.apply_program(orc.zero_state(n), n, lowered(circ), B.parameters(circ))
+    reg = qb.zero_state(n, dtype="c64")
+    qb.apply(reg, fuse_dense(circ, 5))
+    assert rel(reg.state(), want) < 1e-5

@@ -1,12 +1,14 @@
 """BASELINE cfg 4 A/B: variational_circuit(n, d) forward on one B200, three ways —
   tile : the default tile engine (fused.cu: 2x2 / 4x4 gate runs inside shared-memory tiles);
-  dmma : gate fusion into dense 5-qubit blocks (densefuse.py), each block one HBM pass on the FP64
-         tensor cores (dense_mma.cu);
-  dfma : the same dense blocks on the CUDA-core per-gate kernel (run with QBG_DENSE_MMA=0).
+  dense: gate fusion into dense 5-qubit blocks (densefuse.py), each block one HBM pass on the tensor
+         cores — DMMA m8n8k4 in complex128 (dense_mma.cu), tcgen05 kind::tf32 with a 3-piece split
+         in complex64 (dense_tc.cu);
+  cuda : the same dense blocks on the CUDA-core per-gate kernel;
+  tf32 : (complex64) the dense blocks on tcgen05 kind::tf32 with a 3-piece split.
 Prints one JSON line per mode (device-timed, median of --reps) and checks the dense-block state
 against the tile engine's (<ψ_tile|ψ_dense> = 1 and equal energies).
 
-    python tools/cfg4_dense.py --n 30 --depth 10 [--modes tile,dmma] [--reps 3]
+    python tools/cfg4_dense.py --n 30 --depth 10 [--modes tile,dense] [--reps 3] [--dtype c64]
 """
 import argparse
 import json
@@ -61,7 +63,7 @@ def main():
     ap.add_argument("--n", type=int, default=30)
     ap.add_argument("--depth", type=int, default=10)
     ap.add_argument("--k", type=int, default=5)
-    ap.add_argument("--modes", default="tile,dmma")
+    ap.add_argument("--modes", default="tile,dense")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--dtype", default="c128")
     args = ap.parse_args()
@@ -80,6 +82,7 @@ def main():
     ref = None
     for mode in args.modes.split(","):
         qb.set_fusion(mode == "tile")
+        qb.set_dense_path({"cuda": "cuda", "tf32": "tf32-tensor"}.get(mode, "fp64-tensor"))
         blk = circ if mode == "tile" else dense
         reg = qb.zero_state(n, dtype=args.dtype)
         qb.apply(reg, blk)  # warm-up: plans, kernels
@@ -94,7 +97,7 @@ def main():
         e = float(qb.expect(h, reg)[0])
         line = {"mode": mode, "n": n, "depth": d, "dtype": args.dtype, "gates": G, "forward_ms": ms,
                 "gates_per_s": G / (ms / 1e3), "energy": e, "kernels": prof,
-                "hbm_passes": sum(v["launches"] for k, v in prof.items() if k in ("fused_fwd", "dense_mma", "gate")),
+                "hbm_passes": sum(v["launches"] for k, v in prof.items() if k in ("fused_fwd", "dense_mma", "dense_tc", "gate")),
                 "dense_blocks": len(dense.blocks) if mode != "tile" else None,
                 "host_fusion_s": plan_s if mode != "tile" else None,
                 "per_gate_roofline_ms": 2 * G * S / 6553.3e9 * 1e3}
@@ -106,6 +109,7 @@ def main():
             del reg
         print(json.dumps(line), flush=True)
     qb.set_fusion(True)
+    qb.set_dense_path("fp64-tensor")
 
 
 if __name__ == "__main__":
