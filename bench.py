@@ -136,6 +136,18 @@ class Clocks:
 
 
 # ---- reference arm: the reference's CPU implementation on the host cores --------------------------
+def cpu_validation():
+    """The bounded CPU sample's extrapolation checked against full timed reference runs
+    (profiles/r02/cpu_baseline_validation.json: 20q and 25q apply+grad, one core)."""
+    try:
+        v = json.load(open(os.path.join(ROOT, "profiles", "r02", "cpu_baseline_validation.json")))
+        return {k: round(x["ratio_extrap_over_full"], 3) for k, x in v.items()} | {
+            "note": "extrapolated job time / full timed reference run: < 1 means the reported reference rate is "
+                    "optimistic (the reference is slower than stated)"}
+    except Exception:
+        return None
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -167,7 +179,7 @@ def run_reference(args, rank, world):
                          "sample": samples["sample"] + f"; {threads} threads requested (the reference parallelises "
                                                        "over register columns only, so an unbatched state runs on "
                                                        "1 core, utils.hpp:37-64)",
-                         "cpu_model": cb.cpu_model()},
+                         "cpu_model": cb.cpu_model(), "extrapolation_check": cpu_validation()},
         "e2e": {"value": v, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -466,7 +478,8 @@ def main():
         r = cb.sample_apply_grad(orc, n, d, k, 3, threads=1)
         cpu = {"value": r["value"], "unit": "gates/s", "cores": 1, "kind": kind,
                "sample": r["sample"] + "; 1 core (unbatched state: the reference parallelises over columns only)",
-               "cpu_model": cb.cpu_model(), "job_seconds_extrapolated": r["job_seconds_extrapolated"]}
+               "cpu_model": cb.cpu_model(), "job_seconds_extrapolated": r["job_seconds_extrapolated"],
+               "extrapolation_check": cpu_validation()}
 
     sharded = None
     prog_stats = prog.stats()

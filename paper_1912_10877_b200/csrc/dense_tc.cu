@@ -189,9 +189,9 @@ __global__ void __launch_bounds__(128, 1) k_dense_tc(float2* __restrict__ st, co
             uint32_t done = 0;
             unsigned long long spins = 0;
             while (!done) {
-                asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-                             : "=r"(done) : "r"(su32(&mbar)), "r"(phase) : "memory");
-                if (++spins > (1ull << 26)) __trap();  // a lost commit traps instead of hanging the GPU
+                asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+                             : "=r"(done) : "r"(su32(&mbar)), "r"(phase), "r"(0x989680u) : "memory");
+                if (++spins > 4096) __trap();  // ~40 s of suspended waits: a lost commit traps, never hangs
             }
             phase ^= 1u;
         }

@@ -956,6 +956,10 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         s << "if (tid_all >= " << NG * TH << ") {  // producer warpgroup\n";
         if (NG > 1 && 65536 / (NG * TH + NP) / 8 * 8 > producer_regs()) s << "reg_dealloc<" << producer_regs() << ">();\n";
         s << "const int lane = tid_all - " << NG * TH << ";\n";
+        // with TMA only lane 0 issues copies: producer warps 1..3 retire here instead of spinning on the
+        // slot barriers (24% of the reverse pass's executed instructions were such spins, taking issue
+        // slots from the FP64 warps on their SMSPs; profiles/r02/ncu_baseline/bwd_instruction_mix.txt)
+        if (use_tma && (!pstore || tstore)) s << "if (lane >= 32) return;\n";
         // iteration it: store the results of tile it - nbuf (slot computed), then load tile it
         s << "const u64 nt = (" << P.ntiles << "ull - blockIdx.x + gridDim.x - 1) / gridDim.x;\n";
         // element l = lane + NP*k (linear local index): thread part once, k part literal

@@ -209,6 +209,8 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
 }
 // bounded wait: a schedule bug traps (kernel error) instead of hanging the GPU
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  // spin (no suspend-time hint: measured 0.611 -> 0.63 ms per reverse pass with the 10-ms hint —
+  // the waiting consumer wakes late on the critical path)
   unsigned done = 0;
   unsigned long long spins = 0;
   while (true) {
