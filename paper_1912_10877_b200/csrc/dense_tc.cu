@@ -78,23 +78,29 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, float* v) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// accumulators per tile: the K dimension is split over NACC TMEM accumulators summed in registers
+// (round to nearest) — each one accumulates fewer steps in the tensor cores' truncating fp32 adder
 template <int T>
-__global__ void __launch_bounds__(128, 1) k_dense_tc(float2* __restrict__ st, const float* __restrict__ w3,
+constexpr int tc_nacc() { return T == 5 ? 4 : 2; }
+
+template <int T>
+__global__ void __launch_bounds__(128, 2) k_dense_tc(float2* __restrict__ st, const float* __restrict__ w3,
                                                      const __grid_constant__ TcArgs a) {
     constexpr int D = 1 << T, KR = 2 * D, N = KR, KS = KR / 8;
+    constexpr int NACC = tc_nacc<T>();
     constexpr int OS = KR + 4;         // staging row stride (floats)
     constexpr int XSZ = KR * kCols;    // floats of one X piece ([KR/4][128][4])
     constexpr int WSZ = KR * N;        // floats of one W piece ([KR/4][N][4])
     constexpr int PER = D;             // complex elements per thread per tile (D * 128 / 128)
     extern __shared__ __align__(128) unsigned char smraw[];
-    float* xs = reinterpret_cast<float*>(smraw);   // X pieces 0..2
-    float* ws = xs + 3 * XSZ;                      // W pieces 0..2
+    float* xs = reinterpret_cast<float*>(smraw);   // X pieces 0..1
+    float* ws = xs + 2 * XSZ;                      // W pieces 0..2
     float* out = xs;                               // staging [128][OS], reuses the X pieces after the MMAs
     __shared__ __align__(8) unsigned long long mbar;
     __shared__ uint32_t tmem_base_s;
     const int tid = threadIdx.x, warp = tid >> 5;
+    constexpr uint32_t cols = NACC * N < 32 ? 32 : NACC * N;
     if (warp == 0) {
-        constexpr uint32_t cols = N < 32 ? 32 : N;
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" :: "r"(su32(&tmem_base_s)), "r"(cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
@@ -148,20 +154,17 @@ __global__ void __launch_bounds__(128, 1) k_dense_tc(float2* __restrict__ st, co
     if (tile < a.ntiles) load(tile);
     for (; tile < a.ntiles; tile += gridDim.x) {
         const uint64_t base = deposit_zeros(tile, a.fixpos, a.nfix) | a.cval;
-        // split x = x0 + x1 + x2 (each tf32) and store the pieces K-major: (re, im) of amplitude j
-        // are k = 2j, 2j + 1 -> chunk j / 2, lanes 2 (j & 1) + {0, 1}
+        // split x = x0 + x1 (tf32 pieces; the second keeps the residual's leading 11 bits) and store
+        // them K-major: (re, im) of amplitude j are k = 2j, 2j + 1 -> chunk j / 2, lanes 2 (j & 1) + {0, 1}
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
             uint64_t off;
             int m, j;
             part_i(i, off, m, j);
             const float r0 = tf32_rna(v[i].x), i0 = tf32_rna(v[i].y);
-            const float rr = v[i].x - r0, ir = v[i].y - i0;
-            const float r1 = tf32_rna(rr), i1 = tf32_rna(ir);
             const int o = (((j >> 1) * kCols + m) << 2) + ((j & 1) << 1);
             *reinterpret_cast<float2*>(xs + o) = make_float2(r0, i0);
-            *reinterpret_cast<float2*>(xs + XSZ + o) = make_float2(r1, i1);
-            *reinterpret_cast<float2*>(xs + 2 * XSZ + o) = make_float2(tf32_rna(rr - r1), tf32_rna(ir - i1));
+            *reinterpret_cast<float2*>(xs + XSZ + o) = make_float2(tf32_rna(v[i].x - r0), tf32_rna(v[i].y - i0));
         }
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> tensor-core reads
         __syncthreads();
@@ -169,17 +172,21 @@ __global__ void __launch_bounds__(128, 1) k_dense_tc(float2* __restrict__ st, co
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             constexpr uint32_t XL = kCols * 16, WL = N * 16;  // LBO: next 16-B K chunk
             const uint32_t x0 = su32(xs), w0 = su32(ws);
-            // D = x0 w0 + (x0 w1 + x1 w0) + (x0 w2 + x1 w1 + x2 w0): every product above 2^-33
+            // D = x0 w0 + x0 w1 + x1 w0 + x0 w2 + x1 w1, K split over the NACC accumulators
 #pragma unroll
-            for (int pr = 0; pr < 6; ++pr) {
-                const int px = pr == 0 ? 0 : pr == 1 ? 0 : pr == 2 ? 1 : pr == 3 ? 0 : pr == 4 ? 1 : 2;
-                const int pw = pr == 0 ? 0 : pr == 1 ? 1 : pr == 2 ? 0 : pr == 3 ? 2 : pr == 4 ? 1 : 0;
+            for (int ac = 0; ac < NACC; ++ac)
 #pragma unroll
-                for (int s2 = 0; s2 < KS; ++s2) {
-                    const uint32_t xo = px * XSZ * 4 + s2 * 2 * XL, wo = pw * WSZ * 4 + s2 * 2 * WL;
-                    mma_tf32(tmem, umma_desc(x0 + xo, XL, 128), umma_desc(w0 + wo, WL, 128), idesc, pr > 0 || s2 > 0);
+                for (int pr = 0; pr < 5; ++pr) {
+                    const int px = pr == 2 || pr == 4 ? 1 : 0;
+                    const int pw = pr == 1 || pr == 4 ? 1 : pr == 3 ? 2 : 0;
+#pragma unroll
+                    for (int s3 = 0; s3 < KS / NACC; ++s3) {
+                        const int s2 = ac * (KS / NACC) + s3;
+                        const uint32_t xo = px * XSZ * 4 + s2 * 2 * XL, wo = pw * WSZ * 4 + s2 * 2 * WL;
+                        mma_tf32(tmem + ac * N, umma_desc(x0 + xo, XL, 128), umma_desc(w0 + wo, WL, 128), idesc,
+                                 pr > 0 || s3 > 0);
+                    }
                 }
-            }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
                          :: "r"(su32(&mbar)) : "memory");
         }
@@ -203,6 +210,13 @@ __global__ void __launch_bounds__(128, 1) k_dense_tc(float2* __restrict__ st, co
             float r[16];
             tmem_ld16(lane_addr + c0, r);
 #pragma unroll
+            for (int ac = 1; ac < NACC; ++ac) {
+                float r2[16];
+                tmem_ld16(lane_addr + ac * N + c0, r2);
+#pragma unroll
+                for (int q = 0; q < 16; ++q) r[q] += r2[q];
+            }
+#pragma unroll
             for (int q = 0; q < 16; q += 4)
                 *reinterpret_cast<float4*>(out + tid * OS + c0 + q) = make_float4(r[q], r[q + 1], r[q + 2], r[q + 3]);
         }
@@ -218,10 +232,7 @@ __global__ void __launch_bounds__(128, 1) k_dense_tc(float2* __restrict__ st, co
         __syncthreads();
     }
     __syncthreads();
-    if (warp == 0) {
-        constexpr uint32_t cols = N < 32 ? 32 : N;
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" :: "r"(tmem), "r"(cols));
-    }
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" :: "r"(tmem), "r"(cols));
 }
 
 float tf32_host(float x) {  // cvt.rna.tf32.f32 on the host: round to 10 mantissa bits, ties away
@@ -290,9 +301,9 @@ bool launch_dense_tc(const DevState& s, const Gate& g) {
     float* dw = static_cast<float*>(scratch(w3.size() * sizeof(float), 22));
     QBG_CUDA(cudaMemcpyAsync(dw, w3.data(), w3.size() * sizeof(float), cudaMemcpyHostToDevice, stream()));
     QBG_CUDA(cudaStreamSynchronize(stream()));  // w3 is a host temporary
-    const size_t smem = std::max<size_t>(static_cast<size_t>(3 * KR * kCols + 3 * KR * N) * sizeof(float),
+    const size_t smem = std::max<size_t>(static_cast<size_t>(2 * KR * kCols + 3 * KR * N) * sizeof(float),
                                          static_cast<size_t>(kCols * (KR + 4)) * sizeof(float));
-    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(a.ntiles, static_cast<uint64_t>(num_sms())));
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(a.ntiles, static_cast<uint64_t>(num_sms()) * 2));
     const double cols = static_cast<double>(a.ntiles) * kCols;
     // algorithmic: 2 x 8 B per amplitude; 8 D^2 flop per column (the tensor cores run 6 TF32 products)
     LaunchScope ls("dense_tc", 2.0 * 8.0 * D * cols, 8.0 * D * D * cols);
