@@ -3,7 +3,7 @@
 #   tools/bench_grid.sh "QBG_PIPE=0" "QBG_PIPE=2 QBG_BWD_RB=3" ...
 #   (BENCH_ARGS="--dtype c64" adds bench.py arguments)
 for cfg in "$@"; do
-  out=$(env $cfg timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline $BENCH_ARGS 2>/dev/null | tail -1)
+  out=$(env $cfg timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-sharded $BENCH_ARGS 2>/dev/null | tail -1)
   python - "$cfg" "$out" <<'PY'
 import json, sys
 cfg, out = sys.argv[1], sys.argv[2]
