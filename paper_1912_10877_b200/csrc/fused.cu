@@ -1036,15 +1036,8 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         s << "const int warp = tid >> 5, lane = tid & 31;\n";
     }
     // hoisted thread parts of every stage's offsets
-    // Empty leading / trailing stages (no ops: the planner's first stage often only sets up the
-    // layout of the second) are skipped: the tile is loaded straight into the first non-empty
-    // stage's layout and stored from the last non-empty one — one shared-memory transpose (store,
-    // load, two barriers per group) less per empty end stage.
-    int fs = 0, ls_ = P.nstages - 1;
-    while (fs < P.nstages - 1 && P.st[fs].op_begin == P.st[fs].op_end) ++fs;
-    while (ls_ > fs && P.st[ls_].op_begin == P.st[ls_].op_end) --ls_;
-    const DStage& S0 = P.st[fs];
-    const DStage& SL = P.st[ls_];
+    const DStage& S0 = P.st[0];
+    const DStage& SL = P.st[P.nstages - 1];
     s << "const i64 g0 = " << tid_sum(S0.gthr, W, false) << ";\n";
     s << "const i64 gL = " << tid_sum(SL.gthr, W, false) << ";\n";
     for (int k = 0; k < P.nstages; ++k) s << "const unsigned st" << k << " = " << tid_sum(P.st[k].sthr, W, true) << ";\n";
@@ -1111,11 +1104,11 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             }
             s << "\n";
         }
-        if (ls_ > fs) s << SYNC;  // the transposes overwrite the slot
+        if (P.nstages > 1) s << SYNC;  // the transposes overwrite the slot
     }
-    for (int st = fs; st <= ls_; ++st) {
+    for (int st = 0; st < P.nstages; ++st) {
         const DStage& S = P.st[st];
-        if (st > fs && exp_mode != 4 && exp_mode != 6) {  // (QBG_EXP=4/6, diagnostics: no transposes)
+        if (st > 0 && exp_mode != 4 && exp_mode != 6) {  // (QBG_EXP=4/6, diagnostics: no transposes)
             const DStage& Sp = P.st[st - 1];
             for (int j = 0; j < R; ++j) {
                 s << "sx[SI(st" << st - 1 << " ^ " << soff(Sp, j) << "u)] = x[" << j << "];";
@@ -1311,8 +1304,8 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
     if (pstore) {
         // results go back into the slot (swizzled: element l at swz(l)); the producer writes
         // them to global memory while this group computes its next tile
-        const int ls = ls_;
-        if (ls_ == fs) s << SYNC;  // other threads may still read the first stage from the slot
+        const int ls = P.nstages - 1;
+        if (P.nstages == 1) s << SYNC;  // other threads may still read stage 0 from the slot
         if (tstore) {  // linear layout (the TMA box order); the last stage's thread bits hold the low qubits
             uint32_t lwl[kMaxW];
             for (int p = 0; p < W; ++p) lwl[p] = 1u << SL.lthr[p];
