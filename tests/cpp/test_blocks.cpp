@@ -1,7 +1,8 @@
 // C++ consumer of the block / autodiff API (include/qbg/blocks.hpp) on the B200 engine: the paper's
 // and the SPEC's examples written against the C++ API alone (no Python on the path).
 //   argv[1]: output file for variational_circuit(16,10) expect' (energy, 16*31 gradients as raw
-//   doubles) that the pytest wrapper compares with the reference-generated golden.
+//   doubles) that the pytest wrapper compares with the reference-generated golden;
+//   argv[2]: a QBREG1 file written by the reference (loaded and re-saved byte-identically).
 // Exit code 0 = all checks passed.
 #include <cmath>
 #include <cstdio>
@@ -155,6 +156,17 @@ int main(int argc, char** argv) {
         a.save(ss);
         auto c = qb::Register::load(ss);
         CHECK(maxdiff(c.amplitudes(), a.amplitudes()) == 0.0 && c.nactive() == 6);
+    }
+    // a QBREG1 file written by the reference itself (tests/golden/state_qbreg1.bin, nactive 3 of 4)
+    if (argc > 2) {
+        std::ifstream f(argv[2], std::ios::binary);
+        auto r = qb::Register::load(f, 7);
+        CHECK(r.nqubits() == 4 && r.nactive() == 3 && r.nbatch() == 2);
+        std::stringstream back;
+        r.save(back);
+        std::ifstream f2(argv[2], std::ios::binary);
+        std::string orig((std::istreambuf_iterator<char>(f2)), std::istreambuf_iterator<char>());
+        CHECK(back.str() == orig);  // byte-identical round trip
     }
     // variational_circuit(16, 10), θ = dispatch("random") from Rng(42): expect' through the C++ API
     {

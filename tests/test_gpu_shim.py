@@ -31,7 +31,8 @@ def test_cpp_block_api(tmp_path, golden):
                            "-L" + os.path.join(ROOT, "paper_1912_10877_b200"), "-lqbg",
                            "-Wl,-rpath," + os.path.join(ROOT, "paper_1912_10877_b200"), "-o", str(exe)])
     res = tmp_path / "q16.bin"
-    out = subprocess.run([str(exe), str(res)], capture_output=True, text=True, timeout=600)
+    qbreg = os.path.join(ROOT, "tests", "golden", "state_qbreg1.bin")
+    out = subprocess.run([str(exe), str(res), qbreg], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "blocks ok" in out.stdout
     v = np.fromfile(res, dtype=np.float64)
