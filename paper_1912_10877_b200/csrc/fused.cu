@@ -423,7 +423,15 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
     for (int b = 0; b < coal - nb; ++b) Qc |= uint64_t{1} << b;
     std::vector<int> remaining(pl.gates.size());
     for (size_t i = 0; i < remaining.size(); ++i) remaining[i] = static_cast<int>(i);
-    auto tileable = [&](const PG& g) { return g.gate().t <= 2 || is_diagonal(g.gate()); };
+    // 3-qubit non-diagonal gates (dense matblocks, 3-qubit permutations) are a stage op over three
+    // register slots in the specialised kernels; with a gradient (a parameterised 3-qubit
+    // generator) they keep their own pass
+    static const bool dense3 = env_int("QBG_TILE_DENSE3", 1) != 0;  // (diagnostics: A/B of the stage op)
+    auto tileable = [&](const PG& g) {
+        const Gate& u = g.gate();
+        return u.t <= 2 || is_diagonal(u) ||
+               (dense3 && u.t == 3 && RB >= 3 && jit::enabled() && !g.k && g.run.empty());
+    };
     while (!remaining.empty()) {
         // phase 1: grow Q greedily
         uint64_t Q = Qc;
@@ -751,10 +759,16 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
                         o.code = OP_DENSE1;
                         o.mat = emit_mat(g.m, MS_G);
                     }
-                } else {
+                } else if (g.t == 2) {
                     o.code = OP_DENSE2;
                     o.a = static_cast<uint8_t>(slot_of[tg.local[g.tbit[0]]]);
                     o.b = static_cast<uint8_t>(slot_of[tg.local[g.tbit[1]]]);
+                    o.mat = emit_mat(dense_of(g), MS_GDENSE);
+                } else {
+                    o.code = OP_DENSE3;
+                    o.a = static_cast<uint8_t>(slot_of[tg.local[g.tbit[0]]]);
+                    o.b = static_cast<uint8_t>(slot_of[tg.local[g.tbit[1]]]);
+                    o.aux = static_cast<uint64_t>(slot_of[tg.local[g.tbit[2]]]);
                     o.mat = emit_mat(dense_of(g), MS_GDENSE);
                 }
                 pl.ops.push_back(o);
@@ -1143,11 +1157,13 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             // time, on the host, instead of generating undefined register indexing)
             {
                 const bool reg_a = op.code == OP_DENSE1 || op.code == OP_X1 || op.code == OP_PERM1 ||
-                                   op.code == OP_DIAG1R || op.code == OP_DENSE2 || op.code == G_DENSE1 ||
+                                   op.code == OP_DIAG1R || op.code == OP_DENSE2 || op.code == OP_DENSE3 || op.code == G_DENSE1 ||
                                    op.code == G_DIAG1R || op.code == G_DENSE2 || op.code == G_CROSS1 ||
                                    op.code == G_CROSSH || (op.code == G_CROSSD && op.b == LOC_REG);
-                const bool reg_b = op.code == OP_DENSE2 || op.code == G_DENSE2;
-                if ((reg_a && op.a >= RB) || (reg_b && op.b >= RB) || (op.creg_mask >> RB) != 0 ||
+                const bool reg_b = op.code == OP_DENSE2 || op.code == G_DENSE2 || op.code == OP_DENSE3;
+                const bool reg_c = op.code == OP_DENSE3;
+                if ((reg_a && op.a >= RB) || (reg_b && op.b >= RB) || (reg_c && op.aux >= static_cast<uint64_t>(RB)) ||
+                    (op.creg_mask >> RB) != 0 ||
                     (op.cthr_mask >> W) != 0 || ((op.code == OP_DIAG1T || (op.code == G_CROSSD && op.b == LOC_THR)) && op.a >= W))
                     raise(QBG_ERR_INTERNAL, "fused plan: op " + std::to_string(op.code) + " refers to a register / thread slot "
                                             "outside the stage layout");
@@ -1200,6 +1216,14 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                                                            : "((outer >> " + std::to_string(op.a) + ") & 1ull)";
                     s << "if (" << cond << ") { const V d = " << bit << " ? MV(" << o + 1 << ") : MV(" << o << "); ";
                     both("scale<V, R, " + t5 + ">(x, d);", "scale<V, R, " + t5 + ">(y, d);");
+                    s << " }\n";
+                    break;
+                }
+                case OP_DENSE3: {
+                    std::string tp = "<V, R, " + std::to_string(op.a) + ", " + std::to_string(op.b) + ", " +
+                                     std::to_string(op.aux) + ", " + t5 + ">";
+                    s << "if (" << cond << ") { const V m[64] = {" << mvs(o, 64) << "}; ";
+                    both("dense3" + tp + "(x, m);", "dense3" + tp + "(y, m);");
                     s << " }\n";
                     break;
                 }
@@ -1366,6 +1390,7 @@ double pass_flops(const DPass& P, const DOp* ops, int M, bool back) {
             case OP_DENSE1: f = 14; break;
             case OP_PERM1: case OP_DIAG1R: case OP_DIAG1T: case OP_DIAG1G: case OP_DIAGK: f = 6; break;
             case OP_DENSE2: f = 30; break;
+            case OP_DENSE3: f = 62; break;
             case OP_X1: f = 0; break;
             default: f = 0;
         }

@@ -25,6 +25,7 @@ enum : uint8_t {
     OP_DIAG1G,      // diag on tile-outer global bit a (uniform per tile)
     OP_DENSE2,      // 4x4 on slots (a = matrix qubit 0, b = matrix qubit 1)
     OP_DIAGK,       // diag over t targets at mixed locations (aux)
+    OP_DENSE3,      // 8x8 on slots (a, b, aux & 0xff) = matrix qubits 0, 1, 2 (JIT kernels only)
     G_DENSE1 = 16,  // gradient Im<adj|K psi>, K 2x2 on slot a
     G_DIAG1R,       // K diag on slot a
     G_DIAG1U,       // K diag on a thread bit (b = 0) or a tile bit (b = 1) at position a

@@ -78,6 +78,25 @@ __device__ __forceinline__ void dense2(V* x, const V* m) {
     x[i0] = r[0]; x[i1] = r[1]; x[i2] = r[2]; x[i3] = r[3];
   }
 }
+// 8x8 (column-major m[c * 8 + r]) on the register slots K0, K1, K2 (matrix qubits 0, 1, 2)
+template <class V, int R, int K0, int K1, int K2, int CM, int CV>
+__device__ __forceinline__ void dense3(V* x, const V* m) {
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    if (j & ((1 << K0) | (1 << K1) | (1 << K2))) continue;
+    if ((j & CM) != CV) continue;
+    V a[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) a[c] = x[j | ((c & 1) << K0) | (((c >> 1) & 1) << K1) | (((c >> 2) & 1) << K2)];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      V acc = cmul(m[r], a[0]);
+#pragma unroll
+      for (int c = 1; c < 8; ++c) acc = cfma(acc, m[8 * c + r], a[c]);
+      x[j | ((r & 1) << K0) | (((r >> 1) & 1) << K1) | (((r >> 2) & 1) << K2)] = acc;
+    }
+  }
+}
 // ---- gradient terms Σ Im(conj(adj) (K psi)) ----
 template <class V, int R, int K, int CM, int CV>
 __device__ __forceinline__ double gdense1(const V* p, const V* a, V k00, V k10, V k01, V k11) {

@@ -84,3 +84,33 @@ def test_fuse_dense_variational_c64(orc, per_gate):
     reg = qb.zero_state(n, dtype="c64")
     qb.apply(reg, fuse_dense(circ, 5))
     assert rel(reg.state(), want) < 1e-5
+
+
+@pytest.mark.parametrize("n,nb,dtype", [(14, 1, "c128"), (13, 2, "c128"), (12, 1, "c64")])
+def test_three_qubit_dense_blocks_fused_in_tiles(orc, n, nb, dtype):
+    """3-qubit dense gates (matblocks, with and without controls) are a stage op of the tile passes
+    (OP_DENSE3): forward and expect' (rotations between them) vs the oracle, fused vs per-gate."""
+    rng = np.random.default_rng(n + nb)
+    blocks = []
+    for layer in range(3):
+        for s in range(0, n - 2, 3):
+            q = tuple(int(v) for v in rng.permutation(np.arange(1, n + 1))[:3])
+            blocks.append(B.put(n, q, B.matblock(unitary(rng, 8))))
+        c = [int(v) for v in rng.permutation(np.arange(1, n + 1))[:4]]
+        blocks.append(B.control(n, c[3], tuple(c[:3]), B.matblock(unitary(rng, 8))))
+        for q in range(1, n + 1):
+            blocks.append(B.put(n, q, [B.Rx, B.Ry, B.Rz][int(rng.integers(0, 3))](float(rng.uniform(0, 6.28)))))
+    circ = B.chain(n, *blocks)
+    plan = qb.compile_block(circ).plan_preview(nb, dtype)
+    assert "single gate" not in plan.split("plan dir=2")[0]  # every forward gate tiled
+    st = orc.rand_state(n, nb, n)
+    want = orc.apply_program(st, n, lowered(circ), B.parameters(circ))
+    tol = 1e-12 if dtype == "c128" else 1e-5
+    reg = qb.Register(n, nb, dtype=dtype).set_state(st)
+    qb.apply(reg, circ)
+    assert rel(reg.state(), want) < tol
+    h = qb.heisenberg(n)
+    e, g, _, _ = orc.expect_grad(st, n, lowered(circ), B.parameters(circ), B.pauli_terms(h))
+    res = qb.expect_grad(h, (qb.Register(n, nb, dtype=dtype).set_state(st), circ))
+    assert np.abs(res.energies - e).max() <= tol * max(1.0, np.abs(e).max())
+    assert np.abs(res.param_grads - g).max() <= tol * max(1.0, np.abs(g).max())
