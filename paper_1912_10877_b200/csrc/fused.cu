@@ -423,14 +423,15 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
     for (int b = 0; b < coal - nb; ++b) Qc |= uint64_t{1} << b;
     std::vector<int> remaining(pl.gates.size());
     for (size_t i = 0; i < remaining.size(); ++i) remaining[i] = static_cast<int>(i);
-    // 3-qubit non-diagonal gates (dense matblocks, 3-qubit permutations) are a stage op over three
-    // register slots in the specialised kernels; with a gradient (a parameterised 3-qubit
+    // 3- and 4-qubit non-diagonal gates (dense matblocks, permutations) are a stage op over three /
+    // four register slots in the specialised kernels; with a gradient (a parameterised multi-qubit
     // generator) they keep their own pass
     static const bool dense3 = env_int("QBG_TILE_DENSE3", 1) != 0;  // (diagnostics: A/B of the stage op)
+    const int max_mats = jit::enabled() ? kMaxMatsJit : kMaxMats;
     auto tileable = [&](const PG& g) {
         const Gate& u = g.gate();
         return u.t <= 2 || is_diagonal(u) ||
-               (dense3 && u.t == 3 && RB >= 3 && jit::enabled() && !g.k && g.run.empty());
+               (dense3 && (u.t == 3 || u.t == 4) && RB >= u.t && jit::enabled() && !g.k && g.run.empty());
     };
     while (!remaining.empty()) {
         // phase 1: grow Q greedily
@@ -467,7 +468,7 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
                 bool conflict = (g.nd() & ball) | (g.all() & bnd);
                 int co, cmx, cc2;
                 gate_cost(g, co, cmx, cc2);
-                bool fits = nops + co <= kMaxOps && nmats + cmx <= kMaxMats && ncomps + cc2 <= kMaxComps;
+                bool fits = nops + co <= kMaxOps && nmats + cmx <= max_mats && ncomps + cc2 <= kMaxComps;
                 if (tileable(g) && !conflict && (g.nd() & ~Q) == 0 && fits) {
                     sel.push_back(gi);
                     nops += co;
@@ -765,10 +766,11 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
                     o.b = static_cast<uint8_t>(slot_of[tg.local[g.tbit[1]]]);
                     o.mat = emit_mat(dense_of(g), MS_GDENSE);
                 } else {
-                    o.code = OP_DENSE3;
+                    o.code = g.t == 3 ? OP_DENSE3 : OP_DENSE4;
                     o.a = static_cast<uint8_t>(slot_of[tg.local[g.tbit[0]]]);
                     o.b = static_cast<uint8_t>(slot_of[tg.local[g.tbit[1]]]);
                     o.aux = static_cast<uint64_t>(slot_of[tg.local[g.tbit[2]]]);
+                    if (g.t == 4) o.aux |= static_cast<uint64_t>(slot_of[tg.local[g.tbit[3]]]) << 8;
                     o.mat = emit_mat(dense_of(g), MS_GDENSE);
                 }
                 pl.ops.push_back(o);
@@ -778,7 +780,7 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
         P.nops = static_cast<int>(pl.ops.size()) - P.op_base;
         P.nmats = static_cast<int>(pl.mats.size()) - P.mat_base;
         P.ngrad = ncomp;
-        if (P.nops > kMaxOps || P.nmats > kMaxMats || P.ngrad > kMaxComps)
+        if (P.nops > kMaxOps || P.nmats > max_mats || P.ngrad > kMaxComps)
             raise(QBG_ERR_INTERNAL, "fused plan: pass exceeds its shared-memory budget");
         pl.ncomps += ncomp;
         pl.steps.push_back(step);
@@ -1157,12 +1159,15 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             // time, on the host, instead of generating undefined register indexing)
             {
                 const bool reg_a = op.code == OP_DENSE1 || op.code == OP_X1 || op.code == OP_PERM1 ||
-                                   op.code == OP_DIAG1R || op.code == OP_DENSE2 || op.code == OP_DENSE3 || op.code == G_DENSE1 ||
+                                   op.code == OP_DIAG1R || op.code == OP_DENSE2 || op.code == OP_DENSE3 || op.code == OP_DENSE4 ||
+                                   op.code == G_DENSE1 ||
                                    op.code == G_DIAG1R || op.code == G_DENSE2 || op.code == G_CROSS1 ||
                                    op.code == G_CROSSH || (op.code == G_CROSSD && op.b == LOC_REG);
-                const bool reg_b = op.code == OP_DENSE2 || op.code == G_DENSE2 || op.code == OP_DENSE3;
-                const bool reg_c = op.code == OP_DENSE3;
-                if ((reg_a && op.a >= RB) || (reg_b && op.b >= RB) || (reg_c && op.aux >= static_cast<uint64_t>(RB)) ||
+                const bool reg_b = op.code == OP_DENSE2 || op.code == G_DENSE2 || op.code == OP_DENSE3 || op.code == OP_DENSE4;
+                const bool reg_c = op.code == OP_DENSE3 || op.code == OP_DENSE4;
+                const bool reg_d = op.code == OP_DENSE4;
+                if ((reg_a && op.a >= RB) || (reg_b && op.b >= RB) || (reg_c && (op.aux & 0xff) >= static_cast<uint64_t>(RB)) ||
+                    (reg_d && ((op.aux >> 8) & 0xff) >= static_cast<uint64_t>(RB)) ||
                     (op.creg_mask >> RB) != 0 ||
                     (op.cthr_mask >> W) != 0 || ((op.code == OP_DIAG1T || (op.code == G_CROSSD && op.b == LOC_THR)) && op.a >= W))
                     raise(QBG_ERR_INTERNAL, "fused plan: op " + std::to_string(op.code) + " refers to a register / thread slot "
@@ -1219,11 +1224,15 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                     s << " }\n";
                     break;
                 }
-                case OP_DENSE3: {
+                case OP_DENSE3:
+                case OP_DENSE4: {
+                    const bool four = op.code == OP_DENSE4;
                     std::string tp = "<V, R, " + std::to_string(op.a) + ", " + std::to_string(op.b) + ", " +
-                                     std::to_string(op.aux) + ", " + t5 + ">";
-                    s << "if (" << cond << ") { const V m[64] = {" << mvs(o, 64) << "}; ";
-                    both("dense3" + tp + "(x, m);", "dense3" + tp + "(y, m);");
+                                     std::to_string(op.aux & 0xff) +
+                                     (four ? ", " + std::to_string((op.aux >> 8) & 0xff) : std::string()) + ", " + t5 + ">";
+                    const std::string fn = four ? "dense4" : "dense3";
+                    s << "if (" << cond << ") { const V m[" << (four ? 256 : 64) << "] = {" << mvs(o, four ? 256 : 64) << "}; ";
+                    both(fn + tp + "(x, m);", fn + tp + "(y, m);");
                     s << " }\n";
                     break;
                 }
@@ -1391,6 +1400,7 @@ double pass_flops(const DPass& P, const DOp* ops, int M, bool back) {
             case OP_PERM1: case OP_DIAG1R: case OP_DIAG1T: case OP_DIAG1G: case OP_DIAGK: f = 6; break;
             case OP_DENSE2: f = 30; break;
             case OP_DENSE3: f = 62; break;
+            case OP_DENSE4: f = 126; break;
             case OP_X1: f = 0; break;
             default: f = 0;
         }

@@ -26,6 +26,7 @@ enum : uint8_t {
     OP_DENSE2,      // 4x4 on slots (a = matrix qubit 0, b = matrix qubit 1)
     OP_DIAGK,       // diag over t targets at mixed locations (aux)
     OP_DENSE3,      // 8x8 on slots (a, b, aux & 0xff) = matrix qubits 0, 1, 2 (JIT kernels only)
+    OP_DENSE4,      // 16x16 on slots (a, b, aux & 0xff, aux >> 8 & 0xff) (JIT kernels only)
     G_DENSE1 = 16,  // gradient Im<adj|K psi>, K 2x2 on slot a
     G_DIAG1R,       // K diag on slot a
     G_DIAG1U,       // K diag on a thread bit (b = 0) or a tile bit (b = 1) at position a
@@ -98,7 +99,8 @@ struct STerm {
 };
 
 constexpr int kMaxOps = 256;    // ops per pass (smem resident)
-constexpr int kMaxMats = 512;   // complex matrix entries per pass (smem resident)
+constexpr int kMaxMats = 512;   // complex matrix entries per pass (smem resident, interpreter kernels)
+constexpr int kMaxMatsJit = 512;  // ... specialised kernels (a __grid_constant__ parameter; 1024 measured slower: constant-cache misses)
 constexpr int kMaxComps = 256;  // gradient components per pass
 
 struct GradEntry {

@@ -97,6 +97,27 @@ __device__ __forceinline__ void dense3(V* x, const V* m) {
     }
   }
 }
+// 16x16 (column-major m[c * 16 + r]) on the register slots K0..K3 (matrix qubits 0..3)
+template <class V, int R, int K0, int K1, int K2, int K3, int CM, int CV>
+__device__ __forceinline__ void dense4(V* x, const V* m) {
+  constexpr int MASK = (1 << K0) | (1 << K1) | (1 << K2) | (1 << K3);
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    if (j & MASK) continue;
+    if ((j & CM) != CV) continue;
+    V a[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c)
+      a[c] = x[j | ((c & 1) << K0) | (((c >> 1) & 1) << K1) | (((c >> 2) & 1) << K2) | (((c >> 3) & 1) << K3)];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      V acc = cmul(m[r], a[0]);
+#pragma unroll
+      for (int c = 1; c < 16; ++c) acc = cfma(acc, m[16 * c + r], a[c]);
+      x[j | ((r & 1) << K0) | (((r >> 1) & 1) << K1) | (((r >> 2) & 1) << K2) | (((r >> 3) & 1) << K3)] = acc;
+    }
+  }
+}
 // ---- gradient terms Σ Im(conj(adj) (K psi)) ----
 template <class V, int R, int K, int CM, int CV>
 __device__ __forceinline__ double gdense1(const V* p, const V* a, V k00, V k10, V k01, V k11) {

@@ -87,17 +87,18 @@ def test_fuse_dense_variational_c64(orc, per_gate):
 
 
 @pytest.mark.parametrize("n,nb,dtype", [(14, 1, "c128"), (13, 2, "c128"), (12, 1, "c64")])
-def test_three_qubit_dense_blocks_fused_in_tiles(orc, n, nb, dtype):
-    """3-qubit dense gates (matblocks, with and without controls) are a stage op of the tile passes
-    (OP_DENSE3): forward and expect' (rotations between them) vs the oracle, fused vs per-gate."""
-    rng = np.random.default_rng(n + nb)
+@pytest.mark.parametrize("t", [3, 4])
+def test_dense_blocks_fused_in_tiles(orc, n, nb, dtype, t):
+    """3- and 4-qubit dense gates (matblocks, with and without controls) are stage ops of the tile
+    passes (OP_DENSE3 / OP_DENSE4): forward and expect' (rotations between them) vs the oracle."""
+    rng = np.random.default_rng(n + nb + t)
     blocks = []
     for layer in range(3):
-        for s in range(0, n - 2, 3):
-            q = tuple(int(v) for v in rng.permutation(np.arange(1, n + 1))[:3])
-            blocks.append(B.put(n, q, B.matblock(unitary(rng, 8))))
-        c = [int(v) for v in rng.permutation(np.arange(1, n + 1))[:4]]
-        blocks.append(B.control(n, c[3], tuple(c[:3]), B.matblock(unitary(rng, 8))))
+        for s in range(0, n - t + 1, t):
+            q = tuple(int(v) for v in rng.permutation(np.arange(1, n + 1))[:t])
+            blocks.append(B.put(n, q, B.matblock(unitary(rng, 1 << t))))
+        c = [int(v) for v in rng.permutation(np.arange(1, n + 1))[:t + 1]]
+        blocks.append(B.control(n, c[t], tuple(c[:t]), B.matblock(unitary(rng, 1 << t))))
         for q in range(1, n + 1):
             blocks.append(B.put(n, q, [B.Rx, B.Ry, B.Rz][int(rng.integers(0, 3))](float(rng.uniform(0, 6.28)))))
     circ = B.chain(n, *blocks)

@@ -23,20 +23,22 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=25)
     ap.add_argument("--layers", type=int, default=6)
+    ap.add_argument("--t", type=int, default=3, help="qubits per dense block (3 or 4)")
     a = ap.parse_args()
     check(lib().qbg_set_stream(torch.cuda.current_stream().cuda_stream))
     rng = np.random.default_rng(1)
     n = a.n
     blocks = []
     for layer in range(a.layers):
-        off = layer % 3
-        for s in range(off, n - 2, 3):
-            z = rng.normal(size=(8, 8)) + 1j * rng.normal(size=(8, 8))
-            blocks.append(B.put(n, (s + 1, s + 2, s + 3), B.matblock(np.linalg.qr(z)[0])))
+        t = a.t
+        off = layer % t
+        for s in range(off, n - t + 1, t):
+            z = rng.normal(size=(1 << t, 1 << t)) + 1j * rng.normal(size=(1 << t, 1 << t))
+            blocks.append(B.put(n, tuple(range(s + 1, s + t + 1)), B.matblock(np.linalg.qr(z)[0])))
         for q in range(1, n + 1):
             blocks.append(B.put(n, q, B.Rx(float(rng.uniform(0, 6.28)))))
     circ = B.chain(n, *blocks)
-    ndense = sum(1 for b in blocks if len(b.locs) == 3)
+    ndense = sum(1 for b in blocks if len(b.locs) == a.t)
     res = {}
     states = {}
     for mode in ("fused", "per-gate"):
@@ -57,7 +59,7 @@ def main():
         states[mode] = reg
     qb.set_fusion(True)
     ip = states["fused"].inner(states["per-gate"])[0]
-    print(json.dumps({"tile_dense3": os.environ.get("QBG_TILE_DENSE3", "1"), "n": n, "layers": a.layers, "dense3_gates": ndense, "rotations": len(blocks) - ndense, **res,
+    print(json.dumps({"tile_dense3": os.environ.get("QBG_TILE_DENSE3", "1"), "n": n, "layers": a.layers, "t": a.t, "dense_gates": ndense, "rotations": len(blocks) - ndense, **res,
                       "speedup": res["per-gate"]["forward_ms"] / res["fused"]["forward_ms"],
                       "abs_inner_minus_1": abs(abs(ip) - 1.0)}))
 
