@@ -242,6 +242,15 @@ def sharded_weak_scaling(args, rank, world, pg):
         return {"skipped": "world size is not a power of two"}
     nl, d = args.sharded_local_qubits, args.sharded_depth
     n = nl + g
+    # every rank must fit its shard + the staging arena + headroom, or none starts: a rank that
+    # failed alone would leave the others waiting in NCCL
+    free, _ = torch.cuda.mem_get_info()
+    need = (16 << nl) + (2 << 30) + (4 << 30)
+    ok = torch.tensor([1.0 if free >= need else 0.0], device="cuda")
+    if pg is not None:
+        pg.all_reduce(ok, op=pg.ReduceOp.MIN)
+    if float(ok.item()) < 1.0:
+        return {"skipped": f"a rank has {free / 2**30:.1f} GiB free < {need / 2**30:.1f} GiB (shard + staging + headroom)"}
     if n > qb.qubit_cap():
         qb.set_qubit_cap(n)
     circ = qb.variational_circuit(n, d)

@@ -536,6 +536,13 @@ void launch_gate(const DevState& s, const Gate& g) {
 
 void launch_gate_back(const DevState& psi, const DevState& adj, const Gate& gdag, const Gate* K, double* partials,
                       int64_t cap, int* used) {
+    // a constant dense 3..5-qubit gate (no gradient term): the uncompute of ψ and of φ̄ are two
+    // GEMMs on the tensor cores instead of the register-spilling per-gate reverse kernel
+    if (!K && gdag.t >= 3 && gdag.kind == QBG_MAT_DENSE && dense_path() >= 1 && launch_dense_mma(psi, gdag)) {
+        if (!launch_dense_mma(adj, gdag)) raise(QBG_ERR_INTERNAL, "dense reverse: adjoint state not accepted");
+        if (used) *used = 0;
+        return;
+    }
     Gate g = gdag;
     if (g.kind == QBG_MAT_IDENTITY) {  // still need the gradient term: apply the identity as a diagonal
         g.kind = QBG_MAT_DIAGONAL;
