@@ -297,13 +297,14 @@ class ShardedState:
 
     def _realised(self, block, theta):
         from .blocks import _Emitter, _lower, parameter_nodes, parameters
-        key = id(block)
-        em = self._ops_cache.get(key)
-        if em is None:
+        cached = self._ops_cache.get("block")
+        if cached is block:  # identity, not id(): a freed block's id can be reused
+            em = self._ops_cache["em"]
+        else:
             nodes = parameter_nodes(block)
             em = _Emitter({id(p): k for k, p in enumerate(nodes)})
             _lower(block, tuple(range(1, block.nqubits + 1)), (), (), em)
-            self._ops_cache = {key: em}
+            self._ops_cache = {"block": block, "em": em}
         th = parameters(block) if theta is None else np.asarray(theta, float)
         return realise_ops(em, th)
 
