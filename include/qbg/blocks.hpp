@@ -24,6 +24,8 @@
 #include <memory>
 #include <optional>
 #include <string>
+#include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "qblock.hpp"
@@ -88,16 +90,14 @@ inline BlockPtr make(BlockKind k, std::size_t n) {
 }  // namespace detail
 
 // ---- primitives ---------------------------------------------------------------------------------------
+// a constant gate node from the registry (a new node each call: define_const_gate may redefine a
+// name, and constant nodes carry no parameters, so sharing them buys nothing)
 inline BlockPtr constant(const std::string& name) {
-    static std::map<std::string, BlockPtr> cache;
-    auto it = cache.find(name);
     const ConstGateDef* def = find_gate(name);
     if (!def) throw DispatchError("unknown constant gate: " + name);
-    if (it != cache.end()) return it->second;
     auto b = detail::make(BlockKind::Constant, def->nqubits);
     b->name = name;
     b->mat = def->mat;
-    cache[name] = b;
     return b;
 }
 inline BlockPtr X() { return constant("X"); }
@@ -319,19 +319,18 @@ inline BlockPtr dagger(const BlockPtr& b) {
 
 // ---- parameters ------------------------------------------------------------------------
 namespace detail {
-inline void param_nodes(const BlockPtr& b, std::vector<Block*>& out) {
+inline void param_nodes(const BlockPtr& b, std::vector<Block*>& out, std::unordered_set<const Block*>& seen) {
     if (b->parameterised()) {
-        for (auto* p : out)
-            if (p == b.get()) return;  // a shared node contributes once
-        out.push_back(b.get());
+        if (seen.insert(b.get()).second) out.push_back(b.get());  // a shared node contributes once
         return;
     }
-    for (auto& c : b->children) param_nodes(c, out);
+    for (auto& c : b->children) param_nodes(c, out, seen);
 }
 }  // namespace detail
 inline std::vector<Block*> parameter_nodes(const BlockPtr& b) {
     std::vector<Block*> out;
-    detail::param_nodes(b, out);
+    std::unordered_set<const Block*> seen;
+    detail::param_nodes(b, out, seen);
     return out;
 }
 inline std::vector<double> parameters(const BlockPtr& b) {
@@ -519,10 +518,15 @@ struct Emitter {
     std::vector<cplx> vals;
     std::vector<int64_t> perms;
     std::vector<Block*> slots;  // parameter nodes, in parameter order
+    std::unordered_map<const Block*, int> slot_index;
+    void set_slots(std::vector<Block*> s) {
+        slots = std::move(s);
+        for (std::size_t k = 0; k < slots.size(); ++k) slot_index.emplace(slots[k], static_cast<int>(k));
+    }
     int slot_of(const Block* b) const {
-        for (std::size_t k = 0; k < slots.size(); ++k)
-            if (slots[k] == b) return static_cast<int>(k);
-        throw InternalLoweringError();
+        auto it = slot_index.find(b);
+        if (it == slot_index.end()) throw InternalLoweringError();
+        return it->second;
     }
     struct InternalLoweringError : Error {
         InternalLoweringError() : Error("lowering: parameter node not found") {}
@@ -705,7 +709,7 @@ struct Compiled {
 inline detail::Compiled& compile_block(const BlockPtr& b) {
     if (!b->compiled) {
         detail::Emitter em;
-        em.slots = parameter_nodes(b);
+        em.set_slots(parameter_nodes(b));
         std::vector<std::size_t> qmap;
         for (std::size_t q = 1; q <= b->nqubits; ++q) qmap.push_back(q);
         detail::lower(b, qmap, {}, {}, em, false);
