@@ -293,3 +293,120 @@ def test_shard_pack_unpack_kernels(orc):
         check(lib().qbg_shard_unpack(reg._h, arr, len(ls), pat, 1, 4, buf2.data_ptr()))
         dev[rows[1:5]] = buf2.cpu().numpy().view(np.complex128).reshape(-1, nb)
         np.testing.assert_array_equal(reg.state().T, dev)
+
+
+class _LoopbackHub:
+    """In-process stand-in for NCCL between ranks running as threads on ONE GPU: start() posts
+    this rank's send buffers, waits for its partners' posts, and copies each partner's buffer into
+    the matching receive buffer (device copies on the shared stream).  Only the transport is
+    replaced; DistShardBackend / ChunkedExchange / DeviceShardLocal (libqbg pack / unpack kernels,
+    staging arena) are the shipped code."""
+
+    def __init__(self, world):
+        import threading
+        self.world = world
+        self.lock = threading.Condition()
+        self.posts = {}
+        self.gen = [0] * world
+
+    def transport(self, rank):
+        hub = self
+
+        class T:
+            def start(self, sends, recvs, peers, nbytes):
+                n = nbytes // 8
+                with hub.lock:
+                    g = hub.gen[rank]
+                    hub.gen[rank] += 1
+                    for sb, p in zip(sends, peers):
+                        hub.posts[(g, rank, p)] = sb[:n]
+                    hub.lock.notify_all()
+                    for rb, p in zip(recvs, peers):
+                        while (g, p, rank) not in hub.posts:
+                            hub.lock.wait(timeout=60)
+                        rb[:n].copy_(hub.posts[(g, p, rank)])
+                    hub.lock.notify_all()
+                return (g, peers)
+
+            def finish(self, h):
+                import torch
+                torch.cuda.synchronize()  # every partner's copy out of our send buffers is done
+
+        return T()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,g,staging", [(12, 1, 1 << 12), (13, 2, 1 << 13)])
+def test_dist_backend_device_shards_loopback(orc, n, g, staging):
+    """DistShardBackend with DeviceShardLocal (the DeviceNcclBackend configuration minus NCCL) on one
+    B200: 2^g ranks as threads, chunked remaps through the libqbg staging arena and pack / unpack
+    kernels, vs the full-state oracle."""
+    import threading
+    import torch
+    from paper_1912_10877_b200._capi import check, lib
+    from paper_1912_10877_b200.sharded import DeviceShardLocal, DistShardBackend
+    check(lib().qbg_set_stream(torch.cuda.current_stream().cuda_stream))
+    world = 1 << g
+    circ = _circuit(n)
+    B.dispatch(circ, np.random.default_rng(n + g).uniform(0, 2 * np.pi, B.nparameters(circ)))
+    want = orc.apply_program(O.Oracle.zero_state(n), n, _lowered(circ), B.parameters(circ))[0]
+    hub = _LoopbackHub(world)
+    sums = {}
+    sums_lock = threading.Lock()
+
+    def reduce_sum_factory(rank):
+        def red(v):
+            with sums_lock:
+                sums.setdefault("e", []).append(v)
+            return v
+        return red
+
+    big = threading.Lock()  # the engine is not thread-safe per program: local compute one rank at a time
+
+    class LockedLocal(DeviceShardLocal):
+        def apply(self, lops):
+            with big:
+                super().apply(lops)
+                torch.cuda.synchronize()
+
+        def expect(self, terms):
+            with big:
+                return super().expect(terms)
+
+    locals_ = [LockedLocal(n - g) for _ in range(world)]
+    states, errors = {}, []
+
+    def run(rank):
+        try:
+            torch.cuda.set_device(0)
+            be = DistShardBackend(locals_[rank], hub.transport(rank), rank, world, g, staging_bytes=staging,
+                                  allreduce=reduce_sum_factory(rank))
+            st = ShardedState(be, n, g).apply(circ)
+            st.expect_pauli(B.pauli_terms(C.heisenberg(n)))
+            states[rank] = (list(st.phys), be.exchange.chunks, len(st.sched.exchanges))
+        except Exception as e:  # surfaced below
+            errors.append(e)
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errors, errors
+    torch.cuda.synchronize()
+    phys = states[0][0]
+    assert all(states[r][0] == phys for r in range(world))
+    assert states[0][1] > states[0][2] > 0  # chunked: more chunks than exchanges
+    nl = n - g
+    full = np.zeros(1 << n, dtype=complex)
+    for r in range(world):
+        sh = locals_[r].amplitudes()
+        idx_phys = np.arange(1 << nl, dtype=np.int64) | (r << nl)
+        logical = np.zeros_like(idx_phys)
+        for q in range(n):
+            logical |= ((idx_phys >> phys[q]) & 1) << q
+        full[logical] = sh
+    assert np.linalg.norm(full - want) / np.linalg.norm(want) < 1e-12
+    _, e_ref = orc.obs_apply(want[None, :], B.pauli_terms(C.heisenberg(n)))
+    assert abs(sum(sums["e"]) - e_ref[0]) < 1e-12 * max(1.0, abs(e_ref[0]))
+    assert all(lo.staging_high_water <= staging for lo in locals_)
