@@ -146,6 +146,11 @@ void* dev_alloc(size_t bytes, bool state) {
 std::mutex g_ws_mu;
 std::vector<qbg_reg*> g_live;  // live registers (for the release rule)
 DevState g_ws[2];              // [0] forward work state (out-of-place expect'), [1] adjoint buffer
+// checkpoints of the checkpointed expect' (fused_ckpt_*): one allocation of k full states
+struct CkptArena {
+    void* ptr = nullptr;
+    size_t bytes = 0, state_bytes = 0;
+} g_ckpt;
 
 void ws_free(DevState& d) {
     if (!d.ptr) return;
@@ -162,6 +167,39 @@ DevState& ws_get(int k, const DevState& s) {
         d.ptr = dev_alloc(s.bytes(), true);
     }
     return d;
+}
+
+void ckpt_free() {
+    if (!g_ckpt.ptr) return;
+    QBG_CUDA(cudaStreamSynchronize(g_stream));
+    QBG_CUDA(cudaFree(g_ckpt.ptr));
+    g_ckpt = CkptArena{};
+}
+// k checkpoints shaped like s, or nullptr when they would not leave a reserve of device memory free
+// (max(4 GiB, 1/16 of the device)) — the caller then runs the uncompute design
+void* ckpt_get(int64_t k, const DevState& s) {
+    const size_t need = static_cast<size_t>(k) * s.bytes();
+    if (g_ckpt.ptr && g_ckpt.bytes >= need) {
+        g_ckpt.state_bytes = std::max(g_ckpt.state_bytes, s.bytes());
+        return g_ckpt.ptr;
+    }
+    ckpt_free();
+    ensure_device();
+    size_t fr = 0, tot = 0;
+    QBG_CUDA(cudaMemGetInfo(&fr, &tot));
+    const size_t reserve = std::max<size_t>(size_t{4} << 30, tot / 16);
+    if (need + reserve > fr) return nullptr;
+    void* p = nullptr;
+    if (cudaMalloc(&p, need) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    g_allocs.fetch_add(1);
+    g_bound.store(true);
+    g_ckpt.ptr = p;
+    g_ckpt.bytes = need;
+    g_ckpt.state_bytes = s.bytes();
+    return p;
 }
 
 void stream_sync() { QBG_CUDA(cudaStreamSynchronize(g_stream)); }
@@ -708,6 +746,7 @@ int qbg_reg_destroy(qbg_reg* r) {
         for (auto* x : g_live) need = std::max(need, x->s.bytes());
         for (auto& w : g_ws)
             if (w.ptr && w.bytes() > need) ws_free(w);
+        if (g_ckpt.ptr && g_ckpt.state_bytes > need) ckpt_free();
         release_krylov(need);
     });
 }
@@ -715,6 +754,7 @@ int qbg_release_workspace(void) {
     return guarded([&] {
         std::lock_guard<std::mutex> lk(g_ws_mu);
         for (auto& w : g_ws) ws_free(w);
+        ckpt_free();
         release_krylov(0);
         release_scratch();
     });
@@ -1357,10 +1397,33 @@ template <class Seed>
 void grad_driver(qbg_reg* r, Program& p, int32_t inplace, qbg_reg* state_grad, double* vals, double* grads,
                  Seed&& seed) {
     std::lock_guard<std::mutex> lk(g_ws_mu);
-    DevState psi = r->s;
-    if (!inplace) psi.ptr = ws_get(0, r->s).ptr;
     DevState adj = r->s;
     adj.ptr = state_grad ? state_grad->s.ptr : ws_get(1, r->s).ptr;
+    if (!p.realised) realise(p);
+    // checkpointed design (default when the checkpoints fit): the forward passes leave the state
+    // after every reverse segment in an arena, the reverse passes read ψ instead of uncomputing it;
+    // the caller's register is not modified (in place or not, it ends as it started)
+    if (g_fusion) {
+        const int64_t k = fused_ckpt_states(p, r->s);
+        void* arena = k > 0 ? ckpt_get(k, r->s) : nullptr;
+        if (arena) {
+            Nvtx nv("qbg.expect_grad.checkpointed");
+            fused_ckpt_forward(r->s, p, arena);
+            DevState psi = r->s;
+            psi.ptr = arena;  // checkpoint 0: the output state
+            double* e = static_cast<double*>(scratch(r->s.B * sizeof(double), 10));
+            seed(psi, adj, e);
+            double* dg = static_cast<double*>(scratch(std::max<int64_t>(1, p.nparams) * sizeof(double), 11));
+            QBG_CUDA(cudaMemsetAsync(dg, 0, std::max<int64_t>(1, p.nparams) * sizeof(double), g_stream));
+            fused_ckpt_backward(adj, p, arena, dg);
+            QBG_CUDA(cudaMemcpyAsync(vals, e, r->s.B * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+            QBG_CUDA(cudaMemcpyAsync(grads, dg, p.nparams * sizeof(double), cudaMemcpyDeviceToHost, g_stream));
+            stream_sync();
+            return;
+        }
+    }
+    DevState psi = r->s;
+    if (!inplace) psi.ptr = ws_get(0, r->s).ptr;
     // out-of-place: the first forward pass reads the caller's register (no separate copy)
     run_program(psi, p, false, inplace ? nullptr : r->s.ptr);
     double* e = static_cast<double*>(scratch(r->s.B * sizeof(double), 10));

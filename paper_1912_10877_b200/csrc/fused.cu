@@ -23,6 +23,7 @@
 // waits for that release (`done`) before the fill's parity wait.
 // See fused.h for the tile/stage vocabulary and DESIGN.md for the roofline numbers.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <array>
 #include <cstring>
@@ -153,6 +154,7 @@ struct PG {  // a gate as the planner sees it
     const Gate* k = nullptr;   // scalar gradient generator
     int param = -1;
     std::vector<RunGrad> run;  // cross-matrix gradients of a fused run (backward)
+    std::vector<int> src;      // program ops (indices into Program::real) fused into this gate
     const Gate& gate() const { return g ? *g : own; }
     uint64_t nd() const { return is_diagonal(gate()) ? 0 : gate().tmask; }
     uint64_t all() const { return gate().tmask | gate().cmask; }
@@ -233,6 +235,7 @@ std::vector<PG> fuse_runs(std::vector<PG> in, bool backward) {
                 continue;
             }
             PG& o = out[open[q]];
+            o.src.insert(o.src.end(), pg.src.begin(), pg.src.end());
             if (backward && pg.k) {
                 M2 Mp = m2_of(o.gate());  // uncompute so far
                 M2 W = m2_dag(Mp);
@@ -312,6 +315,8 @@ uint64_t pg_sig(const PG& pg) {
 struct Step {
     bool tile = false;
     DPass pass;
+    std::vector<int> members;    // the plan gates of a tile pass (checkpointed reverse plans)
+    int seg = -1;                // checkpoint segment of a mirror forward step (dir 4)
     int single = -1;
     int single_comp = -1;
     int jk = -1;                 // specialised kernel (index into the plan's kernel list)
@@ -336,6 +341,12 @@ struct FusedPlan {
     std::vector<MatSrc> msrc;
     std::vector<std::pair<int, int>> esrc;  // (gate, run index), (-1, -1): no value
     std::vector<uint64_t> sig;
+    // checkpointed expect' (dir 4 = forward mirror of the dir-5 reverse plan): per segment the
+    // program ops it applies (forward order), and the serial of the reverse plan it mirrors
+    std::vector<std::vector<int>> part;
+    std::vector<uint64_t> part_q;      // tile qubits of a segment's passes (0: a single-gate step)
+    std::vector<int> seg_steps;        // first step of each segment (+ end)
+    uint64_t serial = 0, mirror_of = 0;
     int64_t ncomps = 0;
     std::vector<jit::Kernel> jk;
     DOp* d_ops = nullptr;
@@ -413,9 +424,17 @@ void gate_cost(const PG& g, int& ops, int& mats, int& comps) {
     comps = (g.k ? 1 : 0) + (g.run.empty() ? 0 : 8);
 }
 
+bool pg_grad(const PG& g) { return !g.run.empty() || g.k != nullptr; }
+
+std::vector<int> emit_pass(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal, uint64_t Q,
+                           const std::vector<int>& sel);
+
 // Greedy pass construction (see fused.h): a gate joins the pass when it does not conflict with
 // any gate already passed over and its non-diagonal targets fit in the tile qubit set.
-void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal = 3) {
+// ck (checkpointed reverse plans): the pass's gradient statistics are all taken at its start,
+// against the checkpointed ψ, so a gate with a gradient joins only when no gate already in the
+// pass touches its qubits (a run's cross matrix is invariant under gates on other qubits only).
+void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal = 3, bool ck = false) {
     const int n = pl.n;
     const int mq = M - nb;
     const uint64_t full = n >= 64 ? ~uint64_t{0} : (uint64_t{1} << n) - 1;
@@ -433,23 +452,33 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
         return u.t <= 2 || is_diagonal(u) ||
                (dense3 && (u.t == 3 || u.t == 4) && RB >= u.t && jit::enabled() && !g.k && g.run.empty());
     };
-    while (!remaining.empty()) {
-        // phase 1: grow Q greedily
-        uint64_t Q = Qc;
+    // phase 1 grows Q greedily; phase 2 selects with Q fixed, within the pass's smem budgets.
+    // reserve: the gates with a gradient may claim at most mq - reserve qubits of Q (checkpointed
+    // plans try several: the CNOT ring after a rotation layer needs target qubits the rotations
+    // would otherwise take, and the ck rule keeps later rotations out of a pass with those CNOTs)
+    auto select = [&](int reserve, uint64_t& Q, std::vector<int>& sel, std::vector<int>& rest) {
+        Q = Qc;
+        sel.clear();
+        rest.clear();
         {
-            uint64_t bnd = 0, ball = 0;
+            uint64_t bnd = 0, ball = 0, touched = 0;
             for (int gi : remaining) {
                 const PG& g = pl.gates[gi];
                 bool conflict = (g.nd() & ball) | (g.all() & bnd);
+                if (ck && pg_grad(g) && (g.all() & touched)) conflict = true;
                 if (!tileable(g) || conflict) {
                     bnd |= g.nd();
                     ball |= g.all();
                     continue;
                 }
                 uint64_t need = g.nd();
-                if ((need & ~Q) == 0) continue;
-                if (popc(Q | need) <= mq) {
+                if ((need & ~Q) == 0) {
+                    touched |= g.all();
+                    continue;
+                }
+                if (popc(Q | need) <= (pg_grad(g) ? mq - reserve : mq)) {
                     Q |= need;
+                    touched |= g.all();
                 } else {
                     bnd |= g.nd();
                     ball |= g.all();
@@ -458,19 +487,19 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
         }
         for (int q = n - 1; q >= 0 && popc(Q) < mq; --q) Q |= uint64_t{1} << q;
         Q &= full;
-        // phase 2: select with Q fixed, within the pass's smem budgets
-        std::vector<int> sel, rest;
         {
-            uint64_t bnd = 0, ball = 0;
+            uint64_t bnd = 0, ball = 0, touched = 0;
             int nops = 0, nmats = 0, ncomps = 0;
             for (int gi : remaining) {
                 const PG& g = pl.gates[gi];
                 bool conflict = (g.nd() & ball) | (g.all() & bnd);
+                if (ck && pg_grad(g) && (g.all() & touched)) conflict = true;
                 int co, cmx, cc2;
                 gate_cost(g, co, cmx, cc2);
                 bool fits = nops + co <= kMaxOps && nmats + cmx <= max_mats && ncomps + cc2 <= kMaxComps;
                 if (tileable(g) && !conflict && (g.nd() & ~Q) == 0 && fits) {
                     sel.push_back(gi);
+                    touched |= g.all();
                     nops += co;
                     nmats += cmx;
                     ncomps += cc2;
@@ -481,6 +510,21 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
                 }
             }
         }
+    };
+    while (!remaining.empty()) {
+        uint64_t Q = 0;
+        std::vector<int> sel, rest;
+        select(0, Q, sel, rest);
+        for (int reserve = 1; ck && reserve <= 4 && reserve < mq - coal; ++reserve) {
+            uint64_t Q2 = 0;
+            std::vector<int> sel2, rest2;
+            select(reserve, Q2, sel2, rest2);
+            if (sel2.size() > sel.size()) {
+                Q = Q2;
+                sel.swap(sel2);
+                rest.swap(rest2);
+            }
+        }
         if (sel.empty()) {
             Step st;
             st.single = remaining.front();
@@ -488,8 +532,23 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
             remaining.erase(remaining.begin());
             continue;
         }
-        remaining = rest;
+        std::vector<int> back = emit_pass(pl, M, RB, nb, backward, coal, Q, sel);
+        std::vector<int> merged;
+        std::merge(back.begin(), back.end(), rest.begin(), rest.end(), std::back_inserter(merged));
+        remaining = merged;
+    }
+}
 
+// One tile pass over the gates `sel` (plan order) with tile qubits Q: stages, ops, matrices and
+// gradient entries appended to the plan.  Returns the gates beyond the stage budget (sorted), which
+// the caller plans into a later pass.
+std::vector<int> emit_pass(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal, uint64_t Q,
+                           const std::vector<int>& sel) {
+    const int n = pl.n;
+    const int mq = M - nb;
+    const int max_mats = jit::enabled() ? kMaxMatsJit : kMaxMats;
+    std::vector<int> back;
+    {
         // ---- stages ----
         TileGeom tg = geom(M, RB, nb, Q, pl.B);
         const int R = RB, Wn = M - RB;
@@ -536,14 +595,10 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
             }
         }
         if (static_cast<int>(stages.size()) > kMaxStages - 2) {
-            std::vector<int> back;
             for (size_t s = kMaxStages - 2; s < stages.size(); ++s)
                 back.insert(back.end(), stages[s].gates.begin(), stages[s].gates.end());
             stages.resize(kMaxStages - 2);
-            std::vector<int> merged;
             std::sort(back.begin(), back.end());
-            std::merge(back.begin(), back.end(), remaining.begin(), remaining.end(), std::back_inserter(merged));
-            remaining = merged;
         }
         // coalescing lane bits of the load / store layouts: the batch bits and the low qubits
         const uint32_t C = (1u << std::max(coal, nb)) - 1;
@@ -782,10 +837,12 @@ void plan_passes(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal =
         P.ngrad = ncomp;
         if (P.nops > kMaxOps || P.nmats > max_mats || P.ngrad > kMaxComps)
             raise(QBG_ERR_INTERNAL, "fused plan: pass exceeds its shared-memory budget");
+        for (const StagePlan& sp : stages) step.members.insert(step.members.end(), sp.gates.begin(), sp.gates.end());
         pl.ncomps += ncomp;
         pl.steps.push_back(step);
         pl.tile_passes++;
     }
+    return back;
 }
 
 // ---- code generation: one straight-line kernel per distinct pass structure -----------------------
@@ -885,12 +942,13 @@ bool tma_layout(const DPass& P, int M, bool c128, std::vector<TmaDim>& dims) {
     return dims.size() <= 5;
 }
 
-std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, bool back, bool c128) {
+std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, bool back, bool c128, bool ck = false) {
     const int R = 1 << RB, W = M - RB, TH = 1 << W, NW = TH / 32;
     const size_t elem = c128 ? 16 : 8;
     // pipe mode (warp-specialised, see pipeline_enabled): NG consumer groups of TH threads take
     // alternate tiles from a ring of nbuf shared-memory slots filled by a cp.async producer warpgroup
     const bool pipe = pipeline_enabled();
+    if (ck && (!back || !pipe)) raise(QBG_ERR_INTERNAL, "jit: a checkpointed pass is a pipelined reverse pass");
     const int NG = pipe ? consumer_groups(back) : 1;
     const int NWT = NG * NW;  // consumer warps
     const int CS = NWT + 1;   // gradient cell stride (odd: the lanes of a warp_sum hit distinct banks)
@@ -997,6 +1055,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                 if (((static_cast<int64_t>(k) * NP) >> b) & 1) gk += gw[b];
             return gk;
         };
+        if (pstore && tstore && ck) raise(QBG_ERR_INTERNAL, "jit: checkpointed pass with a TMA drain");
         if (pstore && tstore) {
             // one elected thread: the computed tile (linear layout) back as one TMA tensor store, and
             // its shared-memory reads retired before the slot is refilled
@@ -1008,8 +1067,11 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             // element by element: shared-memory read, then its global store
             for (int k = 0; k < (1 << M) / NP; ++k) {
                 const uint32_t sk = swz(static_cast<uint32_t>(k * NP));
-                s << "{ const V d = buf[SI(sl ^ " << sk << "u)]; " << (back ? "psi" : "outp") << "[GI(tb + gp + " << kgo(k)
-                  << "ll)] = d;";
+                if (!ck)
+                    s << "{ const V d = buf[SI(sl ^ " << sk << "u)]; " << (back ? "psi" : "outp") << "[GI(tb + gp + "
+                      << kgo(k) << "ll)] = d;";
+                else
+                    s << "{";
                 if (back)
                     s << " const V e = buf[SI(" << (1 << M) << " + (sl ^ " << sk << "u))]; adj[GI(tb + gp + " << kgo(k)
                       << "ll)] = e;";
@@ -1061,6 +1123,10 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         uint32_t lw[kMaxW];
         for (int p = 0; p < W; ++p) lw[p] = 1u << S0.lthr[p];
         s << "const unsigned lin0 = " << tid_sum(lw, W, true) << ";\n";
+        if (ck) {
+            for (int p = 0; p < W; ++p) lw[p] = 1u << SL.lthr[p];
+            s << "const unsigned linL = " << tid_sum(lw, W, true) << ";\n";
+        }
     }
     s << "V x[R];\n" << (back ? "V y[R];\n" : "");
     auto goff = [&](const DStage& S, int j) {
@@ -1110,37 +1176,39 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         s << "mbar_wait(full + slot, use & 1u);\n";
         s << "V* sx = ring + (size_t)slot * " << tile_elems << "u; V* sy = sx + " << (1 << M) << ";\n";
         s << "u64 outer; i64 tb; tile_geo(tile, outer, tb);\n";
-        for (int j = 0; j < R; ++j) {  // stage 0 from the linear (copied) layout
-            if (exp_mode == 5 || exp_mode == 6) {  // (diagnostics: synthetic tile, no slot reads / global stores)
-                s << "x[" << j << "] = mk<V>((double)(tid + " << j << ") * 1e-3, (double)tile * 1e-9);";
-                if (back) s << " y[" << j << "] = mk<V>((double)(tid - " << j << ") * 1e-3, 1e-9);";
-            } else {
-                s << "x[" << j << "] = sx[SI(lin0 | " << loff(S0, j) << "u)];";
-                if (back) s << " y[" << j << "] = sy[SI(lin0 | " << loff(S0, j) << "u)];";
+        if (!ck) {
+            for (int j = 0; j < R; ++j) {  // stage 0 from the linear (copied) layout
+                if (exp_mode == 5 || exp_mode == 6) {  // (diagnostics: synthetic tile, no slot reads / global stores)
+                    s << "x[" << j << "] = mk<V>((double)(tid + " << j << ") * 1e-3, (double)tile * 1e-9);";
+                    if (back) s << " y[" << j << "] = mk<V>((double)(tid - " << j << ") * 1e-3, 1e-9);";
+                } else {
+                    s << "x[" << j << "] = sx[SI(lin0 | " << loff(S0, j) << "u)];";
+                    if (back) s << " y[" << j << "] = sy[SI(lin0 | " << loff(S0, j) << "u)];";
+                }
+                s << "\n";
             }
+            if (P.nstages > 1) s << SYNC;  // the transposes overwrite the slot
+        }
+    }
+    // register tile <-> shared memory: written with stage a's layout, read back with stage b's
+    auto transpose = [&](int a, int b, bool tx, bool ty) {
+        const DStage& Sa = P.st[a];
+        const DStage& Sb = P.st[b];
+        for (int j = 0; j < R; ++j) {
+            if (tx) s << "sx[SI(st" << a << " ^ " << soff(Sa, j) << "u)] = x[" << j << "];";
+            if (ty) s << " sy[SI(st" << a << " ^ " << soff(Sa, j) << "u)] = y[" << j << "];";
             s << "\n";
         }
-        if (P.nstages > 1) s << SYNC;  // the transposes overwrite the slot
-    }
-    for (int st = 0; st < P.nstages; ++st) {
-        const DStage& S = P.st[st];
-        if (st > 0 && exp_mode != 4 && exp_mode != 6) {  // (QBG_EXP=4/6, diagnostics: no transposes)
-            const DStage& Sp = P.st[st - 1];
-            for (int j = 0; j < R; ++j) {
-                s << "sx[SI(st" << st - 1 << " ^ " << soff(Sp, j) << "u)] = x[" << j << "];";
-                if (back) s << " sy[SI(st" << st - 1 << " ^ " << soff(Sp, j) << "u)] = y[" << j << "];";
-                s << "\n";
-            }
-            s << SYNC;
-            for (int j = 0; j < R; ++j) {
-                s << "x[" << j << "] = sx[SI(st" << st << " ^ " << soff(S, j) << "u)];";
-                if (back) s << " y[" << j << "] = sy[SI(st" << st << " ^ " << soff(S, j) << "u)];";
-                s << "\n";
-            }
-            s << SYNC;
+        s << SYNC;
+        for (int j = 0; j < R; ++j) {
+            if (tx) s << "x[" << j << "] = sx[SI(st" << b << " ^ " << soff(Sb, j) << "u)];";
+            if (ty) s << " y[" << j << "] = sy[SI(st" << b << " ^ " << soff(Sb, j) << "u)];";
+            s << "\n";
         }
-        for (int i = S.op_begin; i < (exp_mode == 2 ? S.op_begin : S.op_end); ++i) {
-            const DOp& op = ops[i];
+        s << SYNC;
+    };
+    bool ex = true, ey = back;  // the states a gate op acts on (x = ψ, y = φ̄; checkpointed: φ̄ only)
+    auto emit_op = [&](const DOp& op) {
             const int o = op.mat;
             std::ostringstream ctl;
             bool has_ctl = false;
@@ -1174,8 +1242,8 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                                             "outside the stage layout");
             }
             auto both = [&](const std::string& call_x, const std::string& call_y) {
-                s << call_x;
-                if (back) s << " " << call_y;
+                if (ex) s << call_x;
+                if (ey) s << " " << call_y;
             };
             auto mvs = [&](int base, int n) {
                 std::ostringstream t;
@@ -1269,8 +1337,8 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                         if (grad)
                             s << "g += imcm(y[" << j << "], cmul(d, x[" << j << "])); }";
                         else {
-                            s << "x[" << j << "] = cmul(x[" << j << "], d);";
-                            if (back) s << " y[" << j << "] = cmul(y[" << j << "], d);";
+                            if (ex) s << "x[" << j << "] = cmul(x[" << j << "], d);";
+                            if (ey) s << " y[" << j << "] = cmul(y[" << j << "], d);";
                             s << " }";
                         }
                     }
@@ -1332,6 +1400,56 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                 default:
                     raise(QBG_ERR_INTERNAL, "jit: unknown op");
             }
+    };
+    auto is_stat = [](const DOp& op) { return op.code >= G_DENSE1; };
+    if (!ck) {
+        for (int st = 0; st < P.nstages; ++st) {
+            const DStage& S = P.st[st];
+            if (st > 0 && exp_mode != 4 && exp_mode != 6) transpose(st - 1, st, true, back);  // (QBG_EXP=4/6: none)
+            for (int i = S.op_begin; i < (exp_mode == 2 ? S.op_begin : S.op_end); ++i) emit_op(ops[i]);
+        }
+    } else {
+        // Checkpointed reverse pass (plan_passes' ck rule): every gradient statistic of the pass is
+        // taken first, against the checkpointed ψ (x) and the incoming φ̄ (y), visiting the stages
+        // that hold statistics from the last to the first (the tile arrives in the last stage's
+        // layout); then φ̄ alone is uncomputed through the stages in order.  ψ is neither
+        // uncomputed nor stored: 28 instead of 44 FP64 instructions per element pair and rotation run.
+        std::vector<int> vis;
+        for (int st = P.nstages - 1; st >= 0; --st)
+            for (int i = P.st[st].op_begin; i < P.st[st].op_end; ++i)
+                if (is_stat(ops[i])) {
+                    vis.push_back(st);
+                    break;
+                }
+        int cur = 0;
+        if (!vis.empty()) {
+            cur = P.nstages - 1;
+            for (int j = 0; j < R; ++j)
+                s << "x[" << j << "] = sx[SI(linL | " << loff(SL, j) << "u)]; y[" << j << "] = sy[SI(linL | "
+                  << loff(SL, j) << "u)];\n";
+        } else {
+            for (int j = 0; j < R; ++j) s << "y[" << j << "] = sy[SI(lin0 | " << loff(S0, j) << "u)];\n";
+        }
+        if (P.nstages > 1) s << SYNC;  // the transposes overwrite the slot
+        for (int st : vis) {
+            if (st != cur) {
+                transpose(cur, st, true, true);
+                cur = st;
+            }
+            for (int i = P.st[st].op_begin; i < P.st[st].op_end; ++i)
+                if (is_stat(ops[i])) emit_op(ops[i]);
+        }
+        ex = false;
+        for (int st = 0; st < P.nstages; ++st) {
+            bool any = false;
+            for (int i = P.st[st].op_begin; i < P.st[st].op_end; ++i) any |= !is_stat(ops[i]);
+            if (!any && st != P.nstages - 1) continue;
+            if (st != cur) {
+                transpose(cur, st, false, true);
+                cur = st;
+            }
+            for (int i = P.st[st].op_begin; i < P.st[st].op_end; ++i)
+                if (!is_stat(ops[i])) emit_op(ops[i]);
         }
     }
     if (pstore) {
@@ -1351,7 +1469,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             s << "}\n";
         } else {
             for (int j = 0; j < R; ++j) {
-                s << "sx[SI(st" << ls << " ^ " << soff(SL, j) << "u)] = x[" << j << "];";
+                if (!ck) s << "sx[SI(st" << ls << " ^ " << soff(SL, j) << "u)] = x[" << j << "];";
                 if (back) s << " sy[SI(st" << ls << " ^ " << soff(SL, j) << "u)] = y[" << j << "];";
                 s << "\n";
             }
@@ -1361,7 +1479,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
     } else {
         if (exp_mode == 1 || exp_mode == 5 || exp_mode == 6) s << "if (outer == ~0ull) {\n";
         for (int j = 0; j < R; ++j) {
-            s << (back ? "psi" : "outp") << "[GI(tb + gL + " << goff(SL, j) << "ll)] = x[" << j << "];";
+            if (!ck) s << (back ? "psi" : "outp") << "[GI(tb + gL + " << goff(SL, j) << "ll)] = x[" << j << "];";
             if (back) s << " adj[GI(tb + gL + " << goff(SL, j) << "ll)] = y[" << j << "];";
             s << "\n";
         }
@@ -1388,7 +1506,8 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
 // Generates, compiles (cached) and attaches the specialised kernels of a plan.
 // Algorithmic floating-point work of a pass (complex mul = 6, add = 2 flops; controls scale
 // by the fraction of elements they select): forward ops on one state, reverse ops on two
-// (uncompute of ψ and φ̄) plus the gradient statistics once.  Reported beside the bytes.
+// (uncompute of ψ and φ̄; one, φ̄, in a checkpointed pass: two = false) plus the gradient
+// statistics once.  Reported beside the bytes.
 double pass_flops(const DPass& P, const DOp* ops, int M, bool back) {
     double per_elem = 0;
     for (int i = 0; i < P.nops; ++i) {
@@ -1423,7 +1542,7 @@ double pass_flops(const DPass& P, const DOp* ops, int M, bool back) {
 
 // Structure key of a pass: everything gen_pass reads (not the matrix values), so a new
 // parameter vector finds its kernels without regenerating / hashing their source.
-uint64_t pass_key(const DPass& P, const DOp* ops, int M, int RB, bool back, bool c128) {
+uint64_t pass_key(const DPass& P, const DOp* ops, int M, int RB, bool back, bool c128, bool ck) {
     uint64_t h = 1469598103934665603ULL;
     auto mix = [&](const void* p, size_t n) {
         const unsigned char* c = static_cast<const unsigned char*>(p);
@@ -1434,7 +1553,7 @@ uint64_t pass_key(const DPass& P, const DOp* ops, int M, int RB, bool back, bool
     };
     auto mixv = [&](int64_t v) { mix(&v, sizeof(v)); };
     const int W = M - RB;
-    for (int64_t v : {int64_t{M}, int64_t{RB}, int64_t{back}, int64_t{c128}, int64_t{P.nstages}, int64_t{P.ngrad},
+    for (int64_t v : {int64_t{M}, int64_t{RB}, int64_t{back} + 2 * int64_t{ck}, int64_t{c128}, int64_t{P.nstages}, int64_t{P.ngrad},
                       int64_t{P.mq}, int64_t{P.nb}, P.B, P.nchunks, static_cast<int64_t>(P.ntiles), int64_t{P.nops},
                       int64_t{P.nmats}})
         mixv(v);
@@ -1481,7 +1600,7 @@ void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128, bool check_
     const size_t elem = c128 ? 16 : 8;
     auto fill = [&](Step& st) {  // matrix parameter blob + shared memory of one step
         const DPass& P = st.pass;
-        st.flops = pass_flops(P, pl.ops.data() + P.op_base, M, back);
+        st.flops = pass_flops(P, pl.ops.data() + P.op_base, M, back && pl.dir != 5);
         fill_blob(st, pl.mats, c128);
         const size_t tile_bytes = (back ? 2 : 1) * (elem << M);
         const int nwt = (pipeline_enabled() ? consumer_groups(back) : 1) * NW;
@@ -1500,7 +1619,7 @@ void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128, bool check_
             std::lock_guard<std::mutex> lk(g_pass_mu);
             for (auto& st : pl.steps) {
                 if (!st.tile) continue;
-                keys.push_back(pass_key(st.pass, pl.ops.data() + st.pass.op_base, M, RB, back, c128));
+                keys.push_back(pass_key(st.pass, pl.ops.data() + st.pass.op_base, M, RB, back, c128, pl.dir == 5));
                 if (!g_pass_kernels.count(keys.back())) all = false;
             }
             if (all) {  // re-parameterised circuit: every kernel is known
@@ -1521,7 +1640,7 @@ void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128, bool check_
     for (auto& st : pl.steps) {
         if (!st.tile) continue;
         const DPass& P = st.pass;
-        std::string body = gen_pass(P, pl.ops.data() + P.op_base, P.nmats, M, RB, back, c128);
+        std::string body = gen_pass(P, pl.ops.data() + P.op_base, P.nmats, M, RB, back, c128, pl.dir == 5);
         uint64_t h = jit::fnv(body);
         auto it = uniq.find(h);
         if (it == uniq.end()) {
@@ -1560,7 +1679,8 @@ void launch_jit(V* psi, V* adj, Step& st, FusedPlan& pl, double* gpart, int64_t 
     const int per_sm = pipe ? 1 : ctas_per_sm(BACK, T);
     int64_t grid = std::min<int64_t>(static_cast<int64_t>(P.ntiles), static_cast<int64_t>(num_sms()) * per_sm);
     if (BACK) grid = std::min<int64_t>(grid, gcols);
-    double bytes = static_cast<double>(P.ntiles) * (int64_t{1} << pl.M) * sizeof(V) * (BACK ? 4.0 : 2.0);
+    // algorithmic bytes: ψ in/out (forward); ψ, φ̄ in/out (reverse); checkpointed reverse: ψ in, φ̄ in/out
+    double bytes = static_cast<double>(P.ntiles) * (int64_t{1} << pl.M) * sizeof(V) * (BACK ? (pl.dir == 5 ? 3.0 : 4.0) : 2.0);
     int gbase = P.grad_base;
     alignas(64) unsigned char tmp[128] = {0}, tma[128] = {0};
     if (pipe && tma_enabled()) {
@@ -1607,7 +1727,9 @@ int batch_bits(int64_t B) {
 }
 
 std::shared_ptr<FusedPlan> build_host_plan(const Program& p, const DevState& s, int dir);
+std::shared_ptr<FusedPlan> build_mirror_plan(const Program& p, const FusedPlan& rev);
 bool refresh_values(FusedPlan& pl, const Program& p);
+void finalize_plan(FusedPlan& pl, const DevState& s, int dir);
 
 std::shared_ptr<FusedPlan> get_plan(std::vector<std::shared_ptr<FusedPlan>>& cache, const Program& p,
                                     const DevState& s, int dir) {
@@ -1623,12 +1745,20 @@ std::shared_ptr<FusedPlan> get_plan(std::vector<std::shared_ptr<FusedPlan>>& cac
                                [&](const std::shared_ptr<FusedPlan>& c) { return c->dir == dir && c->B == s.B; }),
                 cache.end());
     auto pl = build_host_plan(p, s, dir);
+    finalize_plan(*pl, s, dir);
+    cache.push_back(pl);
+    return pl;
+}
+
+// JIT kernels and device tables of a freshly planned plan.
+void finalize_plan(FusedPlan& plr, const DevState& s, int dir) {
+    FusedPlan* pl = &plr;
     const int M = pl->M, RB = pl->RB;
     const bool default_geo = M == (dir == 2 ? kBwdM : kFwdM) && RB == (dir == 2 ? kBwdRB : kFwdRB);
     if (!jit::enabled() && !default_geo) raise(QBG_ERR_UNSUPPORTED, "fused: non-default tile geometry needs the JIT");
     if (jit::enabled()) {
         try {
-            jit_prepare(*pl, M, RB, dir == 2, s.dtype == QBG_C128);
+            jit_prepare(*pl, M, RB, dir == 2 || dir == 5, s.dtype == QBG_C128);
         } catch (const Error& e) {
             static bool warned = false;
             const char* strict = std::getenv("QBG_JIT_STRICT");
@@ -1653,8 +1783,6 @@ std::shared_ptr<FusedPlan> get_plan(std::vector<std::shared_ptr<FusedPlan>>& cac
         pl->d_ptr = upload(pl->csr_ptr);
         pl->d_idx = upload(pl->csr_idx);
     }
-    cache.push_back(pl);
-    return pl;
 }
 
 // The realised program as the planner's fused gate list (dir 0 forward, 1 adjoint, 2 reverse).
@@ -1666,9 +1794,11 @@ std::vector<PG> plan_gates(const Program& p, int dir) {
         PG g;
         if (dir == 0) {
             g.g = &p.real[q].u;
+            g.src.push_back(static_cast<int>(q));
         } else {
             const RealOp& r = p.real[N - 1 - q];
             g.g = &r.udag;
+            g.src.push_back(static_cast<int>(N - 1 - q));
             if (dir == 2 && r.param >= 0) {
                 g.k = &r.k;
                 g.param = r.param;
@@ -1679,12 +1809,31 @@ std::vector<PG> plan_gates(const Program& p, int dir) {
     return fuse_runs(std::move(gs), dir == 2);
 }
 
+// The gate list of a checkpoint mirror plan: each segment's program ops in forward order, runs
+// fused within the segment only.  seg_begin (optional) receives each segment's first gate.
+std::vector<PG> mirror_gates(const Program& p, const std::vector<std::vector<int>>& part, std::vector<int>* seg_begin) {
+    std::vector<PG> out;
+    for (const auto& seg : part) {
+        if (seg_begin) seg_begin->push_back(static_cast<int>(out.size()));
+        std::vector<PG> gs;
+        for (int i : seg) {
+            PG g;
+            g.g = &p.real[static_cast<size_t>(i)].u;
+            g.src.push_back(i);
+            gs.push_back(std::move(g));
+        }
+        for (PG& g : fuse_runs(std::move(gs), false)) out.push_back(std::move(g));
+    }
+    if (seg_begin) seg_begin->push_back(static_cast<int>(out.size()));
+    return out;
+}
+
 // New θ on a program whose plan exists: when the fused gate list keeps its structure (pg_sig),
 // the passes, ops and specialised kernels stay; only the matrix values, the cross-gradient
 // matrices and the kernels' matrix parameters are rewritten (no plan_passes, no JIT lookup).
 // Returns false when the structure changed (the caller rebuilds).
 bool refresh_values(FusedPlan& pl, const Program& p) {
-    std::vector<PG> gates = plan_gates(p, pl.dir);
+    std::vector<PG> gates = pl.dir == 4 ? mirror_gates(p, pl.part, nullptr) : plan_gates(p, pl.dir == 5 ? 2 : pl.dir);
     if (gates.size() != pl.sig.size()) return false;
     for (size_t i = 0; i < gates.size(); ++i)
         if (pg_sig(gates[i]) != pl.sig[i]) return false;
@@ -1733,6 +1882,65 @@ bool refresh_values(FusedPlan& pl, const Program& p) {
     return true;
 }
 
+std::atomic<uint64_t> g_plan_serial{0};
+
+// The forward mirror (dir 4) of a checkpointed reverse plan (dir 5): one segment per reverse step,
+// in reverse order, applying the same program ops in forward order on the same tile qubits, so the
+// state after segment k is exactly the ψ the matching reverse pass reads as its checkpoint.
+std::shared_ptr<FusedPlan> build_mirror_plan(const Program& p, const FusedPlan& rev) {
+    auto pl = std::make_shared<FusedPlan>();
+    pl->version = p.version;
+    pl->B = rev.B;
+    pl->dtype = rev.dtype;
+    pl->n = rev.n;
+    pl->dir = 4;
+    pl->serial = ++g_plan_serial;
+    pl->mirror_of = rev.serial;
+    for (size_t r = rev.steps.size(); r-- > 0;) {
+        const Step& st = rev.steps[r];
+        std::vector<int> src;
+        uint64_t Q = 0;
+        if (st.tile) {
+            for (int gi : st.members) src.insert(src.end(), rev.gates[gi].src.begin(), rev.gates[gi].src.end());
+            for (int k = 0; k < st.pass.mq; ++k) Q |= uint64_t{1} << st.pass.qpos[k];
+        } else {
+            src = rev.gates[st.single].src;
+        }
+        std::sort(src.begin(), src.end());
+        pl->part.push_back(std::move(src));
+        pl->part_q.push_back(Q);
+    }
+    std::vector<int> seg_begin;
+    pl->gates = mirror_gates(p, pl->part, &seg_begin);
+    pl->sig.reserve(pl->gates.size());
+    for (const PG& g : pl->gates) pl->sig.push_back(pg_sig(g));
+    const int nb = batch_bits(rev.B);
+    const Geo g = geo_for(0);
+    pl->M = rev.M;
+    pl->RB = g.RB;
+    for (size_t k = 0; k < pl->part.size(); ++k) {
+        pl->seg_steps.push_back(static_cast<int>(pl->steps.size()));
+        std::vector<int> sel;
+        for (int gi = seg_begin[k]; gi < seg_begin[k + 1]; ++gi) sel.push_back(gi);
+        if (pl->part_q[k] == 0) {  // a single-gate reverse step: the same gate alone
+            for (int gi : sel) {
+                Step st;
+                st.single = gi;
+                st.seg = static_cast<int>(k);
+                pl->steps.push_back(st);
+            }
+            continue;
+        }
+        while (!sel.empty()) {
+            const size_t first = pl->steps.size();
+            sel = emit_pass(*pl, pl->M, pl->RB, nb, false, g.coal, pl->part_q[k], sel);
+            for (size_t i = first; i < pl->steps.size(); ++i) pl->steps[i].seg = static_cast<int>(k);
+        }
+    }
+    pl->seg_steps.push_back(static_cast<int>(pl->steps.size()));
+    return pl;
+}
+
 // The planner alone (no device, no JIT): used by get_plan and by the host-only preview.
 std::shared_ptr<FusedPlan> build_host_plan(const Program& p, const DevState& s, int dir) {
     auto pl = std::make_shared<FusedPlan>();
@@ -1741,14 +1949,15 @@ std::shared_ptr<FusedPlan> build_host_plan(const Program& p, const DevState& s, 
     pl->dtype = s.dtype;
     pl->n = s.n;
     pl->dir = dir;
-    pl->gates = plan_gates(p, dir);
+    pl->serial = ++g_plan_serial;
+    pl->gates = plan_gates(p, dir == 5 ? 2 : dir);
     pl->sig.reserve(pl->gates.size());
     for (const PG& g : pl->gates) pl->sig.push_back(pg_sig(g));
     const int nb = batch_bits(s.B);
-    const Geo g = geo_for(dir);
+    const Geo g = geo_for(dir == 5 ? 2 : dir);
     pl->M = g.M;
     pl->RB = g.RB;
-    plan_passes(*pl, g.M, g.RB, nb, dir == 2, g.coal);
+    plan_passes(*pl, g.M, g.RB, nb, dir >= 2, g.coal, dir == 5);
     // per-gate fallback steps with a scalar gradient get their own component rows
     for (auto& st : pl->steps)
         if (!st.tile && pl->gates[st.single].k) {
@@ -1801,22 +2010,29 @@ void run_forward(const DevState& s, FusedPlan& pl, const void* src) {
     }
 }
 
+// arena (checkpointed plans, dir 5): reverse step r reads ψ from checkpoint r instead of psi
 template <typename V>
-void run_backward(const DevState& psi, const DevState& adj, FusedPlan& pl, double* d_grads) {
+void run_backward(const DevState& psi, const DevState& adj, FusedPlan& pl, double* d_grads, char* arena = nullptr) {
     const int64_t cols = static_cast<int64_t>(num_sms()) * 8;
     const int64_t total = pl.ncomps;
     double* part = static_cast<double*>(scratch(std::max<int64_t>(1, total) * cols * sizeof(double), 13));
     if (total) QBG_CUDA(cudaMemsetAsync(part, 0, total * cols * sizeof(double), stream()));
-    for (auto& st : pl.steps) {
+    for (size_t r = 0; r < pl.steps.size(); ++r) {
+        Step& st = pl.steps[r];
+        DevState ps = psi;
+        if (arena) ps.ptr = arena + r * psi.bytes();
         if (st.tile) {
             if (st.jk >= 0)
-                launch_jit<V, true>(static_cast<V*>(psi.ptr), static_cast<V*>(adj.ptr), st, pl, part, cols);
+                launch_jit<V, true>(static_cast<V*>(ps.ptr), static_cast<V*>(adj.ptr), st, pl, part, cols);
+            else if (!arena)
+                launch_interp(pl.dtype, true, ps.ptr, adj.ptr, st.pass, pl.d_ops, pl.d_mats, part, cols);
             else
-                launch_interp(pl.dtype, true, psi.ptr, adj.ptr, st.pass, pl.d_ops, pl.d_mats, part, cols);
+                raise(QBG_ERR_INTERNAL, "fused: a checkpointed pass without its specialised kernel");
         } else {
+            // (per-gate step; with checkpoints its uncompute of ψ only consumes checkpoint r)
             const PG& g = pl.gates[st.single];
             int used = 0;
-            launch_gate_back(psi, adj, g.gate(), g.k, g.k ? part + st.single_comp * cols : nullptr, cols, &used);
+            launch_gate_back(ps, adj, g.gate(), g.k, g.k ? part + st.single_comp * cols : nullptr, cols, &used);
         }
     }
     if (total) {
@@ -1849,13 +2065,97 @@ bool fused_backward(const DevState& psi, const DevState& adj, Program& p, double
     return true;
 }
 
+// ---- checkpointed expect' (dir 4 forward mirror, dir 5 reverse) ---------------------------------
+// The forward passes write the state after every reverse pass's segment (out of place, into an
+// arena of checkpoints); each reverse pass then reads its ψ instead of uncomputing it.  Same HBM
+// traffic per step as the uncompute design (3S + 3S per pass pair instead of 2S + 4S), 36% less
+// FP64 in the reverse passes, and the caller's register is never modified.
+namespace {
+bool ckpt_enabled() {  // QBG_CKPT=0: the uncompute design (A/B)
+    static const bool on = pipeline_enabled() && env_int("QBG_CKPT", 1) != 0;
+    return on;
+}
+
+std::shared_ptr<FusedPlan> get_mirror(Program& p, const DevState& s, const FusedPlan& rev) {
+    for (auto& c : p.plans)
+        if (c->dir == 4 && c->B == s.B && c->dtype == s.dtype && c->n == s.n && c->mirror_of == rev.serial &&
+            (c->version == p.version || refresh_values(*c, p)))
+            return c;
+    p.plans.erase(std::remove_if(p.plans.begin(), p.plans.end(),
+                                 [&](const std::shared_ptr<FusedPlan>& c) { return c->dir == 4 && c->B == s.B; }),
+                  p.plans.end());
+    auto pl = build_mirror_plan(p, rev);
+    finalize_plan(*pl, s, 4);
+    p.plans.push_back(pl);
+    return pl;
+}
+
+template <typename V>
+void run_ckpt_forward(const DevState& in, FusedPlan& fw, char* arena) {
+    const size_t nseg = fw.part.size(), sb = in.bytes();
+    const void* cur = in.ptr;
+    for (size_t k = 0; k < nseg; ++k) {
+        DevState d = in;
+        d.ptr = arena + (nseg - 1 - k) * sb;  // checkpoint of reverse step nseg-1-k
+        bool placed = false;
+        for (int i = fw.seg_steps[k]; i < fw.seg_steps[k + 1]; ++i) {
+            Step& st = fw.steps[i];
+            if (!placed && st.tile && st.jk >= 0) {  // out of place: previous checkpoint -> this one
+                launch_jit<V, false>(static_cast<V*>(const_cast<void*>(cur)), static_cast<V*>(d.ptr), st, fw, nullptr, 0);
+                placed = true;
+                continue;
+            }
+            if (!placed) {
+                QBG_CUDA(cudaMemcpyAsync(d.ptr, cur, sb, cudaMemcpyDeviceToDevice, stream()));
+                placed = true;
+            }
+            if (st.tile && st.jk >= 0)
+                launch_jit<V, false>(static_cast<V*>(d.ptr), nullptr, st, fw, nullptr, 0);
+            else if (st.tile)
+                launch_interp(fw.dtype, false, d.ptr, nullptr, st.pass, fw.d_ops, fw.d_mats, nullptr, 0);
+            else
+                launch_gate(d, fw.gates[st.single].gate());
+        }
+        if (!placed) QBG_CUDA(cudaMemcpyAsync(d.ptr, cur, sb, cudaMemcpyDeviceToDevice, stream()));
+        cur = d.ptr;
+    }
+}
+}  // namespace
+
+int64_t fused_ckpt_states(Program& p, const DevState& s) {
+    if (!ckpt_enabled() || !fusable(s, geo_for(2).M)) return 0;
+    auto rev = get_plan(p.plans, p, s, 5);
+    for (auto& st : rev->steps)
+        if (st.tile && st.jk < 0) return 0;  // (JIT unavailable: the interpreter has no checkpointed pass)
+    return static_cast<int64_t>(rev->steps.size());
+}
+
+void fused_ckpt_forward(const DevState& in, Program& p, void* arena) {
+    auto rev = get_plan(p.plans, p, in, 5);
+    auto fw = get_mirror(p, in, *rev);
+    if (in.dtype == QBG_C128)
+        run_ckpt_forward<double2>(in, *fw, static_cast<char*>(arena));
+    else
+        run_ckpt_forward<float2>(in, *fw, static_cast<char*>(arena));
+}
+
+void fused_ckpt_backward(const DevState& adj, Program& p, void* arena, double* d_grads) {
+    auto rev = get_plan(p.plans, p, adj, 5);
+    if (adj.dtype == QBG_C128)
+        run_backward<double2>(adj, adj, *rev, d_grads, static_cast<char*>(arena));
+    else
+        run_backward<float2>(adj, adj, *rev, d_grads, static_cast<char*>(arena));
+}
+
 void fused_stats(const Program& p, int64_t* f, int64_t* b) {
     *f = 0;
     *b = 0;
+    bool ck = false;
+    for (auto& c : p.plans) ck |= c->dir == 5;
     for (auto& c : p.plans) {
         int64_t steps = static_cast<int64_t>(c->steps.size());
-        if (c->dir == 0) *f = steps;
-        if (c->dir == 2) *b = steps;
+        if (c->dir == (ck ? 4 : 0)) *f = steps;
+        if (c->dir == (ck ? 5 : 2)) *b = steps;
     }
 }
 
@@ -1872,7 +2172,14 @@ std::string fused_plan_preview(const Program& p, int64_t B, int dtype) {
     s.dtype = dtype;
     std::vector<std::shared_ptr<FusedPlan>> v;
     if (fusable(s, geo_for(0).M)) v.push_back(build_host_plan(p, s, 0));
-    if (fusable(s, geo_for(2).M)) v.push_back(build_host_plan(p, s, 2));
+    if (fusable(s, geo_for(2).M)) {
+        v.push_back(build_host_plan(p, s, 2));
+        if (env_int("QBG_CKPT", 1) != 0) {  // the checkpointed pair expect' runs when the checkpoints fit
+            auto rev = build_host_plan(p, s, 5);
+            v.push_back(build_mirror_plan(p, *rev));
+            v.push_back(rev);
+        }
+    }
     return plans_text(v);
 }
 
@@ -2201,6 +2508,13 @@ int64_t fused_jit_check(const Program& p, const Observable* o, int64_t B, int dt
         auto pl = build_host_plan(p, s, 2);
         jit_prepare(*pl, pl->M, pl->RB, true, dtype == QBG_C128, true);
         count += static_cast<int64_t>(pl->steps.size());
+        if (ckpt_enabled()) {  // the checkpointed pair (expect' when its checkpoints fit)
+            auto rev = build_host_plan(p, s, 5);
+            jit_prepare(*rev, rev->M, rev->RB, true, dtype == QBG_C128, true);
+            auto fw = build_mirror_plan(p, *rev);
+            jit_prepare(*fw, fw->M, fw->RB, false, dtype == QBG_C128, true);
+            count += static_cast<int64_t>(rev->steps.size() + fw->steps.size());
+        }
     }
     if (o && !o->terms.empty() && s.n >= kSeedM - batch_bits(B)) {
         for (bool energy_only : {false, true}) {  // expect' (φ̄ = Oψ) and expect (energies only)

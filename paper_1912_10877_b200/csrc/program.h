@@ -48,6 +48,12 @@ bool fused_backward(const DevState& psi, const DevState& adj, Program& p, double
 bool fused_obs_apply(const DevState& psi, const DevState& phi, Observable& o, double* d_energy /* B or null */);
 // passes of the most recently built forward / backward plans (0 when unfused)
 void fused_stats(const Program& p, int64_t* fwd, int64_t* bwd);
+// checkpointed expect' (fused.cu): the number of full-state checkpoints the program needs on s (0:
+// unavailable, use fused_forward / fused_backward); the forward writes them into arena (checkpoint 0
+// = the output state), the reverse pass reads them
+int64_t fused_ckpt_states(Program& p, const DevState& s);
+void fused_ckpt_forward(const DevState& in, Program& p, void* arena);
+void fused_ckpt_backward(const DevState& adj, Program& p, void* arena, double* d_grads /* nparams, += */);
 std::string fused_plan_info(const Program& p);  // human-readable pass/stage layout
 // Host-only planner run (no device): forward + reverse plans for a 2^n x B register.
 std::string fused_plan_preview(const Program& p, int64_t B, int dtype);
