@@ -1208,6 +1208,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         s << SYNC;
     };
     bool ex = true, ey = back;  // the states a gate op acts on (x = ψ, y = φ̄; checkpointed: φ̄ only)
+    std::string cfix;           // statistics of a lane-flipped register slot: per-lane component fix-up
     auto emit_op = [&](const DOp& op) {
             const int o = op.mat;
             std::ostringstream ctl;
@@ -1349,7 +1350,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                 }
                 case G_CROSS1: {
                     s << "{ double c[8] = {0, 0, 0, 0, 0, 0, 0, 0}; if (" << cond << ") gcross1<V, R, " << int(op.a)
-                      << ">(x, y, c); const double v = warp_sum8(c, lane); sg_acc(&sg[(" << op.gslot
+                      << ">(x, y, c); " << cfix << "const double v = warp_sum8(c, lane); sg_acc(&sg[(" << op.gslot
                       << " + (lane >> 2)) * " << CS << " + warp], v, (lane & 3) == 0); }\n";
                     break;
                 }
@@ -1361,8 +1362,8 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                         call = "gcrossd_u<V, R>(x, y, c, (tid >> " + std::to_string(op.a) + ") & 1);";
                     else
                         call = "gcrossd_u<V, R>(x, y, c, (int)((outer >> " + std::to_string(op.a) + ") & 1ull));";
-                    s << "{ double c[4] = {0, 0, 0, 0}; if (" << cond << ") " << call
-                      << " const double v = warp_sum4(c, lane); sg_acc(&sg[(" << op.gslot
+                    s << "{ double c[4] = {0, 0, 0, 0}; if (" << cond << ") " << call << " " << cfix
+                      << "const double v = warp_sum4(c, lane); sg_acc(&sg[(" << op.gslot
                       << " + (lane >> 3)) * " << CS << " + warp], v, (lane & 7) == 0); }\n";
                     break;
                 }
@@ -1374,7 +1375,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                     }
                     s << "{ double c[4] = {0, 0, 0, 0}; if (" << cond << ") " << "gcrossh1"
                       << "<V, R, " << int(op.a)
-                      << ">(x, y, c); const double v = warp_sum4(c, lane); sg_acc(&sg[(" << op.gslot
+                      << ">(x, y, c); " << cfix << "const double v = warp_sum4(c, lane); sg_acc(&sg[(" << op.gslot
                       << " + (lane >> 3)) * " << CS << " + warp], v, (lane & 7) == 0); }\n";
                     break;
                 }
@@ -1414,30 +1415,142 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         // that hold statistics from the last to the first (the tile arrives in the last stage's
         // layout); then φ̄ alone is uncomputed through the stages in order.  ψ is neither
         // uncomputed nor stored: 28 instead of 44 FP64 instructions per element pair and rotation run.
-        std::vector<int> vis;
-        for (int st = P.nstages - 1; st >= 0; --st)
-            for (int i = P.st[st].op_begin; i < P.st[st].op_end; ++i)
-                if (is_stat(ops[i])) {
-                    vis.push_back(st);
-                    break;
-                }
-        int cur = 0;
-        if (!vis.empty()) {
-            cur = P.nstages - 1;
-            for (int j = 0; j < R; ++j)
-                s << "x[" << j << "] = sx[SI(linL | " << loff(SL, j) << "u)]; y[" << j << "] = sy[SI(linL | "
-                  << loff(SL, j) << "u)];\n";
-        } else {
-            for (int j = 0; j < R; ++j) s << "y[" << j << "] = sy[SI(lin0 | " << loff(S0, j) << "u)];\n";
-        }
-        if (P.nstages > 1) s << SYNC;  // the transposes overwrite the slot
-        for (int st : vis) {
-            if (st != cur) {
-                transpose(cur, st, true, true);
-                cur = st;
+        // The statistics need no stage layout of the uncompute: their qubits are grouped RB at a time,
+        // and each group reads ψ and φ̄ from the tile's linear image in the slot (read-only, no
+        // transposes) with its own register layout.  Bank conflicts: the local bits below nlow
+        // select the 16-B bank group; those in thread bits take lanes 0.., those in register bits are
+        // XOR-ed per lane with a lane bit whose own local bit is high ("flipped" slots), so the 8
+        // lanes of every quarter warp hit 8 distinct groups.  A flipped slot swaps the roles of its
+        // qubit's values 0 and 1 in that lane: fixed up on the statistic before the warp reduction.
+        struct StatOp {
+            DOp op;
+            int lbit;  // the run qubit's local bit (-1: a tile-outer bit)
+        };
+        std::vector<StatOp> rops, dops;  // runs needing a register slot / diagonal runs
+        bool generic = false;            // other gradient ops (controlled generators): stage layouts
+        for (int st = 0; st < P.nstages; ++st)
+            for (int i = P.st[st].op_begin; i < P.st[st].op_end; ++i) {
+                const DOp& op = ops[i];
+                if (!is_stat(op)) continue;
+                const DStage& S = P.st[st];
+                if (op.creg_mask || op.cthr_mask || op.ctile_mask) generic = true;
+                if (op.code == G_CROSSH || op.code == G_CROSS1)
+                    rops.push_back({op, S.lreg[op.a]});
+                else if (op.code == G_CROSSD)
+                    dops.push_back({op, op.b == LOC_REG ? S.lreg[op.a] : op.b == LOC_THR ? S.lthr[op.a] : -1});
+                else
+                    generic = true;
             }
-            for (int i = P.st[st].op_begin; i < P.st[st].op_end; ++i)
-                if (is_stat(ops[i])) emit_op(ops[i]);
+        int cur = 0;
+        if (!generic) {
+            const int nlow = c128 ? 3 : 4;
+            const int ngroups = rops.empty() ? (dops.empty() ? 0 : 1) : static_cast<int>((rops.size() + RB - 1) / RB);
+            for (int g = 0; g < ngroups; ++g) {
+                std::vector<int> rb;  // register slot k -> local bit
+                for (size_t r = static_cast<size_t>(g) * RB; r < rops.size() && rb.size() < static_cast<size_t>(RB); ++r)
+                    rb.push_back(rops[r].lbit);
+                auto in_rb = [&](int b) { return std::find(rb.begin(), rb.end(), b) != rb.end(); };
+                for (int b = M - 1; b >= nlow && static_cast<int>(rb.size()) < RB; --b)
+                    if (!in_rb(b)) rb.push_back(b);
+                for (int b = 0; b < M && static_cast<int>(rb.size()) < RB; ++b)
+                    if (!in_rb(b)) rb.push_back(b);
+                std::vector<int> th;  // thread bit p -> local bit: the low ones first
+                for (int b = 0; b < nlow; ++b)
+                    if (!in_rb(b)) th.push_back(b);
+                for (int b = nlow; b < M; ++b)
+                    if (!in_rb(b)) th.push_back(b);
+                if (static_cast<int>(th.size()) != W) raise(QBG_ERR_INTERNAL, "jit: statistics group layout");
+                uint32_t w[kMaxW];
+                for (int p = 0; p < W; ++p) w[p] = 1u << th[p];
+                int flip_lane[kMaxR];  // lane bit XOR-ed into register slot k (-1: none)
+                std::fill(flip_lane, flip_lane + kMaxR, -1);
+                int nextp = 0;
+                while (nextp < nlow && nextp < W && th[nextp] < nlow) ++nextp;
+                for (int k = 0; k < RB; ++k)
+                    if (rb[k] < nlow && nextp < nlow && nextp < W) {
+                        flip_lane[k] = nextp;
+                        w[nextp] ^= 1u << rb[k];
+                        ++nextp;
+                    }
+                auto lo = [&](int j) {
+                    uint32_t o = 0;
+                    for (int k = 0; k < RB; ++k)
+                        if ((j >> k) & 1) o |= 1u << rb[k];
+                    return o;
+                };
+                s << "{ const unsigned lg = " << tid_sum(w, W, true) << ";\n";
+                for (int j = 0; j < R; ++j)
+                    s << "x[" << j << "] = sx[SI(lg ^ " << lo(j) << "u)]; y[" << j << "] = sy[SI(lg ^ " << lo(j) << "u)];\n";
+                auto fix = [&](int k, int code) -> std::string {
+                    if (flip_lane[k] < 0) return std::string();
+                    const std::string f = "((tid >> " + std::to_string(flip_lane[k]) + ") & 1)";
+                    if (code == G_CROSSH)
+                        return "{ const bool f = " + f + "; const double t = c[0]; c[0] = f ? c[1] : t; c[1] = f ? t : c[1]; "
+                               "c[3] = f ? -c[3] : c[3]; } ";
+                    if (code == G_CROSSD) return "{ const bool f = " + f + "; const double t = c[0]; c[0] = f ? c[1] : t; c[1] = f ? t : c[1]; } ";
+                    std::string r = "{ const bool f = " + f + ";";  // G_CROSS1: C_uv <-> C_(1-u)(1-v)
+                    for (int pr : {0, 1, 2, 3}) {
+                        const int a0 = pr < 2 ? pr : pr + 2, b0 = pr < 2 ? pr + 6 : pr + 2;
+                        r += " { const double t = c[" + std::to_string(a0) + "]; c[" + std::to_string(a0) + "] = f ? c[" +
+                             std::to_string(b0) + "] : t; c[" + std::to_string(b0) + "] = f ? t : c[" + std::to_string(b0) + "]; }";
+                    }
+                    return r + " } ";
+                };
+                for (size_t r = static_cast<size_t>(g) * RB; r < rops.size() && r < static_cast<size_t>(g + 1) * RB; ++r) {
+                    DOp o2 = rops[r].op;
+                    o2.a = static_cast<uint8_t>(r - static_cast<size_t>(g) * RB);
+                    cfix = fix(o2.a, o2.code);
+                    emit_op(o2);
+                }
+                if (g == 0)
+                    for (const StatOp& d : dops) {
+                        DOp o2 = d.op;
+                        cfix.clear();
+                        if (d.lbit >= 0) {
+                            const int k = static_cast<int>(std::find(rb.begin(), rb.end(), d.lbit) - rb.begin());
+                            if (k < RB) {
+                                o2.b = LOC_REG;
+                                o2.a = static_cast<uint8_t>(k);
+                                cfix = fix(k, G_CROSSD);
+                            } else {
+                                o2.b = LOC_THR;
+                                o2.a = static_cast<uint8_t>(std::find(th.begin(), th.end(), d.lbit) - th.begin());
+                            }
+                        }
+                        emit_op(o2);
+                    }
+                cfix.clear();
+                s << "}\n";
+            }
+            for (int j = 0; j < R; ++j) s << "y[" << j << "] = sy[SI(lin0 | " << loff(S0, j) << "u)];\n";
+            if (P.nstages > 1) s << SYNC;  // the transposes overwrite the slot
+        } else {
+            // generic: the stages that hold statistics, from the last (the tile arrives in the last
+            // stage's linear layout) to the first, transposing ψ and φ̄ between them
+            std::vector<int> vis;
+            for (int st = P.nstages - 1; st >= 0; --st)
+                for (int i = P.st[st].op_begin; i < P.st[st].op_end; ++i)
+                    if (is_stat(ops[i])) {
+                        vis.push_back(st);
+                        break;
+                    }
+            if (!vis.empty()) {
+                cur = P.nstages - 1;
+                for (int j = 0; j < R; ++j)
+                    s << "x[" << j << "] = sx[SI(linL | " << loff(SL, j) << "u)]; y[" << j << "] = sy[SI(linL | "
+                      << loff(SL, j) << "u)];\n";
+            } else {
+                for (int j = 0; j < R; ++j) s << "y[" << j << "] = sy[SI(lin0 | " << loff(S0, j) << "u)];\n";
+            }
+            if (P.nstages > 1) s << SYNC;  // the transposes overwrite the slot
+            for (int st : vis) {
+                if (st != cur) {
+                    transpose(cur, st, true, true);
+                    cur = st;
+                }
+                for (int i = P.st[st].op_begin; i < P.st[st].op_end; ++i)
+                    if (is_stat(ops[i])) emit_op(ops[i]);
+            }
         }
         ex = false;
         for (int st = 0; st < P.nstages; ++st) {
