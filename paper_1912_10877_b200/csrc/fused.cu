@@ -559,27 +559,35 @@ std::vector<int> emit_pass(FusedPlan& pl, int M, int RB, int nb, bool backward, 
         // Stages with lookahead: a stage takes every pending gate whose non-diagonal targets fit
         // its register set and that commutes with the gates it passes over (same rule as the
         // pass selection), so a CNOT ring and its rotation runs share stages.
+        // The register set of a stage is seeded: besides the plain scan (the set grows with the
+        // gates in order), the targets of any one or two of the first pending gates seed it, and the
+        // stage that takes the most gates wins — a CNOT chain's next target then gets its register
+        // before the rotation runs fill the set (fewer stages, i.e. transposes, per pass).
         std::vector<StagePlan> stages;
         {
-            std::vector<int> pending = sel;
-            while (!pending.empty()) {
-                StagePlan cur;
-                std::vector<int> left;
+            auto need_of = [&](int gi) {
+                const Gate& g = pl.gates[gi].gate();
+                uint32_t need = 0;
+                if (!is_diagonal(g))
+                    for (int q = 0; q < g.t; ++q) need |= 1u << tg.local[g.tbit[q]];
+                // a permutation (CNOT, Toffoli, controlled SWAP) whose controls are register bits is
+                // a compile-time register rename; a control on a thread bit would make it a
+                // runtime conditional swap of the whole register tile (128 moves for 2 x 16 c128)
+                // (measured: forward passes gain ~2%; reverse passes lose more to the extra
+                // stages than the moves cost next to the FP64 work, so forward only)
+                if (g.kind == QBG_MAT_PERMUTATION && !backward && perm_ctrl_regs())
+                    for (int q = 0; q < 64; ++q)
+                        if (((g.cmask >> q) & 1) && tg.local[q] >= 0) need |= 1u << tg.local[q];
+                return need;
+            };
+            auto scan = [&](uint32_t S0, const std::vector<int>& pending, StagePlan& cur, std::vector<int>& left) {
+                cur = StagePlan{};
+                cur.S = S0;
+                left.clear();
                 uint64_t bnd = 0, ball = 0;
                 for (int gi : pending) {
                     const PG& pg = pl.gates[gi];
-                    const Gate& g = pg.gate();
-                    uint32_t need = 0;
-                    if (!is_diagonal(g))
-                        for (int q = 0; q < g.t; ++q) need |= 1u << tg.local[g.tbit[q]];
-                    // a permutation (CNOT, Toffoli, controlled SWAP) whose controls are register bits is
-                    // a compile-time register rename; a control on a thread bit would make it a
-                    // runtime conditional swap of the whole register tile (128 moves for 2 x 16 c128)
-                    // (measured: forward passes gain ~2%; reverse passes lose more to the extra
-                    // stages than the moves cost next to the FP64 work, so forward only)
-                    if (g.kind == QBG_MAT_PERMUTATION && !backward && perm_ctrl_regs())
-                        for (int q = 0; q < 64; ++q)
-                            if (((g.cmask >> q) & 1) && tg.local[q] >= 0) need |= 1u << tg.local[q];
+                    const uint32_t need = need_of(gi);
                     bool conflict = (pg.nd() & ball) | (pg.all() & bnd);
                     if (!conflict && __builtin_popcount(cur.S | need) <= R) {
                         cur.S |= need;
@@ -590,8 +598,32 @@ std::vector<int> emit_pass(FusedPlan& pl, int M, int RB, int nb, bool backward, 
                         left.push_back(gi);
                     }
                 }
-                stages.push_back(cur);
-                pending = left;
+            };
+            static const int seeds = env_int("QBG_STAGE_SEEDS", 16);  // (0: the plain scan; A/B)
+            std::vector<int> pending = sel;
+            while (!pending.empty()) {
+                StagePlan best, c;
+                std::vector<int> bleft, l;
+                scan(0, pending, best, bleft);
+                std::vector<uint32_t> cand;  // target sets of the first pending gates
+                for (int gi : pending) {
+                    if (static_cast<int>(cand.size()) >= seeds) break;
+                    const uint32_t nd = need_of(gi);
+                    if (nd && __builtin_popcount(nd) <= R && std::find(cand.begin(), cand.end(), nd) == cand.end())
+                        cand.push_back(nd);
+                }
+                for (size_t i = 0; i < cand.size(); ++i)
+                    for (size_t j = i; j < cand.size(); ++j) {
+                        const uint32_t S0 = cand[i] | cand[j];
+                        if (__builtin_popcount(S0) > R) continue;
+                        scan(S0, pending, c, l);
+                        if (c.gates.size() > best.gates.size()) {
+                            best = c;
+                            bleft = l;
+                        }
+                    }
+                stages.push_back(best);
+                pending = bleft;
             }
         }
         if (static_cast<int>(stages.size()) > kMaxStages - 2) {
@@ -611,8 +643,17 @@ std::vector<int> emit_pass(FusedPlan& pl, int M, int RB, int nb, bool backward, 
             return S;
         };
         for (auto& s : stages) s.S = fill(s.S);
-        if (stages.front().S & C) stages.insert(stages.begin(), StagePlan{fill(0), {}});
-        if (stages.back().S & C) stages.push_back(StagePlan{fill(0), {}});
+        // The first stage's layout reads the tile, the last one's writes it.  Without the pipeline
+        // these are global accesses and must be coalesced (no low bit in registers).  Pipelined, the
+        // producer moves the tile and the consumers read / write its linear image in shared
+        // memory: one low bit in registers is a 2-way bank conflict on that access — cheaper than
+        // an extra stage (a transpose).  The reverse pass's consumers store to global memory.
+        auto needs_extra = [&](uint32_t S, bool store) {
+            if (!pipeline_enabled() || (store && backward)) return (S & C) != 0;
+            return __builtin_popcount(S & C) >= 2;
+        };
+        if (needs_extra(stages.front().S, false)) stages.insert(stages.begin(), StagePlan{fill(0), {}});
+        if (needs_extra(stages.back().S, true)) stages.push_back(StagePlan{fill(0), {}});
 
         Step step;
         step.tile = true;
@@ -651,12 +692,11 @@ std::vector<int> emit_pass(FusedPlan& pl, int M, int RB, int nb, bool backward, 
                 // three bits of distinct (bit mod 3) so the swizzled 16-B accesses of a quarter
                 // warp hit 8 distinct bank groups
                 bool used[3] = {false, false, false};
-                if ((sp.S & C) == 0)
-                    for (int b = 0; b < 32 && order.size() < 3; ++b)
-                        if ((C >> b) & 1) {
-                            order.push_back(b);
-                            used[b % 3] = true;
-                        }
+                for (int b = 0; b < 32 && order.size() < 3; ++b)
+                    if (((C >> b) & 1) && !((sp.S >> b) & 1) && !used[b % 3]) {
+                        order.push_back(b);
+                        used[b % 3] = true;
+                    }
                 for (int b : avail)
                     if (!used[b % 3] && order.size() < 3 &&
                         std::find(order.begin(), order.end(), b) == order.end()) {
