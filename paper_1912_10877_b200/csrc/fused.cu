@@ -1536,11 +1536,33 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                     }
                     return r + " } ";
                 };
-                for (size_t r = static_cast<size_t>(g) * RB; r < rops.size() && r < static_cast<size_t>(g + 1) * RB; ++r) {
-                    DOp o2 = rops[r].op;
-                    o2.a = static_cast<uint8_t>(r - static_cast<size_t>(g) * RB);
-                    cfix = fix(o2.a, o2.code);
-                    emit_op(o2);
+                const size_t r0 = static_cast<size_t>(g) * RB, r1 = std::min(rops.size(), r0 + RB);
+                bool herm = r1 - r0 >= 2 && RB == 4;
+                for (size_t r = r0; r < r1; ++r) herm = herm && rops[r].op.code == G_CROSSH;
+                if (herm) {
+                    // the group's Hermitian runs together: one pass over the pairs per slot, one
+                    // 16-component warp reduction (lane l: run ((l >> 1) & 15) >> 2, component l/2 & 3)
+                    const int nk = static_cast<int>(r1 - r0);
+                    s << "{ double c[16]; gstat_group<V, R, " << nk << ">(x, y, c);\n";
+                    for (int k = 0; k < nk; ++k) {
+                        std::string fx = fix(k, G_CROSSH);
+                        for (size_t at = fx.find("c["); at != std::string::npos; at = fx.find("c[", at + 2)) {
+                            const size_t e = fx.find(']', at);
+                            const int ci = std::stoi(fx.substr(at + 2, e - at - 2));
+                            fx.replace(at, e - at + 1, "c[" + std::to_string(4 * k + ci) + "]");
+                        }
+                        s << fx;
+                    }
+                    s << "const double v = warp_sum16(c, lane); const int m = (lane >> 1) & 15, rr = m >> 2; const int gs = ";
+                    for (int k = 0; k < nk; ++k) s << "rr == " << k << " ? " << rops[r0 + k].op.gslot << " : ";
+                    s << "0; sg_acc(&sg[(gs + (m & 3)) * " << CS << " + warp], v, (lane & 1) == 0 && rr < " << nk << "); }\n";
+                } else {
+                    for (size_t r = r0; r < r1; ++r) {
+                        DOp o2 = rops[r].op;
+                        o2.a = static_cast<uint8_t>(r - r0);
+                        cfix = fix(o2.a, o2.code);
+                        emit_op(o2);
+                    }
                 }
                 if (g == 0)
                     for (const StatOp& d : dops) {

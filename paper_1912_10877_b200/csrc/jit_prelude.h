@@ -351,6 +351,65 @@ __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
+// Hermitian cross statistics of the runs on register slots 0..NK-1 together (the checkpointed
+// reverse pass's statistics groups): c[4k .. 4k+3] = Im C00, Im C11, Im(C01 + C10), Re(C01 - C10)
+// of slot k, zero for k >= NK.  The diagonal parts are sums of the per-element Im(conj(a) p), shared
+// by the slots; the off-diagonal accumulators alternate between two halves (8-deep FMA chains).
+template <class V, int R, int NK>
+__device__ __forceinline__ void gstat_group(const V* p, const V* a, double* c) {
+  typedef typename RT<V>::T T;
+  T d[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) d[j] = fma((T)a[j].x, (T)p[j].y, -((T)a[j].y * (T)p[j].x));
+  T t[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) t[j] = d[j];
+#pragma unroll
+  for (int w = R / 2; w >= 1; w >>= 1)
+#pragma unroll
+    for (int i = 0; i < w; ++i) t[i] += t[i + w];
+  const T tot = t[0];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (k >= NK) {
+      c[4 * k] = 0.0; c[4 * k + 1] = 0.0; c[4 * k + 2] = 0.0; c[4 * k + 3] = 0.0;
+      continue;
+    }
+    T s0[2] = {0, 0}, i01[2] = {0, 0}, i10[2] = {0, 0}, r01[2] = {0, 0}, r10[2] = {0, 0};
+    int h = 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      if (j & (1 << k)) continue;
+      const int j1 = j | (1 << k);
+      const T a0x = a[j].x, a0y = a[j].y, a1x = a[j1].x, a1y = a[j1].y;
+      const T p0x = p[j].x, p0y = p[j].y, p1x = p[j1].x, p1y = p[j1].y;
+      s0[h] += d[j];
+      i01[h] = fma(a0x, p1y, fma(-a0y, p1x, i01[h]));
+      i10[h] = fma(a1x, p0y, fma(-a1y, p0x, i10[h]));
+      r01[h] = fma(a0x, p1x, fma(a0y, p1y, r01[h]));
+      r10[h] = fma(a1x, p0x, fma(a1y, p0y, r10[h]));
+      h ^= 1;
+    }
+    const T sz = s0[0] + s0[1];
+    c[4 * k] = (double)sz;
+    c[4 * k + 1] = (double)(tot - sz);
+    c[4 * k + 2] = (double)((i01[0] + i01[1]) + (i10[0] + i10[1]));
+    c[4 * k + 3] = (double)((r01[0] + r01[1]) - (r10[0] + r10[1]));
+  }
+}
+// 16 values per lane -> lane l holds the warp total of component (l >> 1) & 15 (16 shuffles)
+__device__ __forceinline__ double warp_sum16(double* v, int lane) {
+#pragma unroll
+  for (int o = 16, n = 8; o >= 2; o >>= 1, n >>= 1) {
+    const bool hi = lane & o;
+#pragma unroll
+    for (int k = 0; k < n; ++k) {
+      const double send = hi ? v[k] : v[k + n], keep = hi ? v[k + n] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
 // 8 values over the warp by halving exchanges; lane 4c ends with the sum of component c
 // 4 values per lane -> lane l holds the warp total of component (l >> 3) & 3
 __device__ __forceinline__ double warp_sum4(double* v, int lane) {
