@@ -128,6 +128,14 @@ int qbg_set_stream(void* stream);
 int qbg_synchronize(void);
 /* Fusion switch: 1 (default) = tiled multi-gate passes, 0 = one kernel per gate. */
 int qbg_set_fusion(int32_t enabled);
+/* expect' design: 1 (default) = checkpointed (the forward passes keep the state after every
+   reverse segment, the reverse passes read it instead of uncomputing it; used when those
+   checkpoints fit in device memory, the register is left unmodified), 0 = uncompute (two extra
+   full states at most, the register is uncomputed back to the input when in place). */
+int qbg_set_checkpointing(int32_t enabled);
+/* Upper bound on the device memory the checkpoints may take (bytes; -1, the default: whatever is
+   free less a reserve of max(4 GiB, 1/16 of the device)).  Above it expect' uncomputes. */
+int qbg_set_checkpoint_limit(int64_t bytes);
 /* Kernel for dense 3..5-qubit gates (register.hpp:371-384 as one GEMM over all bases):
    1 (default) FP64 tensor cores, DMMA m8n8k4 (complex64 is widened to FP64 and rounded once);
    2 complex64 on tcgen05 kind::tf32 with a 3-piece operand split (faster; the tensor cores' fp32

@@ -23,6 +23,19 @@ def set_fusion(enabled: bool) -> None:
     lib().qbg_set_fusion(1 if enabled else 0)
 
 
+def set_checkpointing(enabled: bool) -> None:
+    """expect' design: checkpointed (default; the forward passes keep the state after every reverse
+    segment, the reverse passes read it — used when the checkpoints fit in device memory) or
+    uncompute (the reverse passes uncompute ψ alongside φ̄)."""
+    lib().qbg_set_checkpointing(1 if enabled else 0)
+
+
+def set_checkpoint_limit(nbytes: int) -> None:
+    """Upper bound on the device memory expect's checkpoints may take (-1: free memory less a
+    reserve); above it the uncompute design runs."""
+    lib().qbg_set_checkpoint_limit(int(nbytes))
+
+
 DENSE_PATHS = {"cuda": 0, "fp64-tensor": 1, "tf32-tensor": 2}
 
 

@@ -71,7 +71,7 @@ def lib() -> ctypes.CDLL:
         "qbg_shard_unpack": (c_int32, [P, P, c_int32, c_uint64, c_int64, c_int64, P]),
         "qbg_buffer_alloc": (c_int32, [c_int64, POINTER(P)]), "qbg_buffer_free": (c_int32, [P]),
         "qbg_set_stream": (c_int32, [P]), "qbg_synchronize": (c_int32, []),
-        "qbg_set_fusion": (c_int32, [c_int32]), "qbg_set_dense_path": (c_int32, [c_int32]), "qbg_profile_enable": (c_int32, [c_int32]),
+        "qbg_set_fusion": (c_int32, [c_int32]), "qbg_set_checkpointing": (c_int32, [c_int32]), "qbg_set_checkpoint_limit": (c_int32, [c_int64]), "qbg_set_dense_path": (c_int32, [c_int32]), "qbg_profile_enable": (c_int32, [c_int32]),
         "qbg_profile_reset": (c_int32, []), "qbg_profile_report": (c_int32, [c_char_p, c_int64]),
         "qbg_launch_count": (c_uint64, []), "qbg_launch_count_reset": (c_int32, []),
         "qbg_rng_create": (c_int32, [c_uint64, POINTER(P)]), "qbg_rng_destroy": (c_int32, [P]),

@@ -56,7 +56,9 @@ def obs_apply(obs: Block, reg: Register, out: Register | None = None) -> Registe
 
 def expect_grad(obs: Block, pair, want_state_grad: bool = False, inplace: bool = False) -> GradResult:
     """expect'(O, reg => circuit).  ``inplace`` runs on ``reg`` itself (it
-    is uncomputed back to the input up to rounding) and saves one full-state copy.
+    is uncomputed back to the input up to rounding) and saves one full-state copy.  With the
+    checkpointed design (default when its checkpoints fit, see set_checkpointing) the register is
+    never modified, in place or not.
     ``obs`` may be an MMD loss (Listing 12: expect'(mmd, zero_state(n)=>circuit))."""
     from .mmd import MMD, mmd_grad
     if isinstance(obs, MMD):

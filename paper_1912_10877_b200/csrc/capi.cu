@@ -151,6 +151,7 @@ struct CkptArena {
     void* ptr = nullptr;
     size_t bytes = 0, state_bytes = 0;
 } g_ckpt;
+std::atomic<int64_t> g_ckpt_limit{-1};  // qbg_set_checkpoint_limit (bytes; -1: free memory less a reserve)
 
 void ws_free(DevState& d) {
     if (!d.ptr) return;
@@ -179,6 +180,8 @@ void ckpt_free() {
 // (max(4 GiB, 1/16 of the device)) — the caller then runs the uncompute design
 void* ckpt_get(int64_t k, const DevState& s) {
     const size_t need = static_cast<size_t>(k) * s.bytes();
+    const int64_t lim = g_ckpt_limit.load();
+    if (lim >= 0 && need > static_cast<size_t>(lim)) return nullptr;
     if (g_ckpt.ptr && g_ckpt.bytes >= need) {
         g_ckpt.state_bytes = std::max(g_ckpt.state_bytes, s.bytes());
         return g_ckpt.ptr;
@@ -644,6 +647,14 @@ int qbg_set_dense_path(int32_t path) {
 }
 int qbg_set_fusion(int32_t on) {
     g_fusion = on != 0;
+    return QBG_OK;
+}
+int qbg_set_checkpointing(int32_t on) {
+    fused_set_checkpointing(on != 0);
+    return QBG_OK;
+}
+int qbg_set_checkpoint_limit(int64_t bytes) {
+    g_ckpt_limit.store(bytes < 0 ? -1 : bytes);
     return QBG_OK;
 }
 int qbg_profile_enable(int32_t on) {

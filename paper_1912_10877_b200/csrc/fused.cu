@@ -2246,9 +2246,10 @@ bool fused_backward(const DevState& psi, const DevState& adj, Program& p, double
 // traffic per step as the uncompute design (3S + 3S per pass pair instead of 2S + 4S), 36% less
 // FP64 in the reverse passes, and the caller's register is never modified.
 namespace {
+std::atomic<bool> g_ckpt_on{true};  // qbg_set_checkpointing
 bool ckpt_enabled() {  // QBG_CKPT=0: the uncompute design (A/B)
     static const bool on = pipeline_enabled() && env_int("QBG_CKPT", 1) != 0;
-    return on;
+    return on && g_ckpt_on.load();
 }
 
 std::shared_ptr<FusedPlan> get_mirror(Program& p, const DevState& s, const FusedPlan& rev) {
@@ -2296,6 +2297,8 @@ void run_ckpt_forward(const DevState& in, FusedPlan& fw, char* arena) {
     }
 }
 }  // namespace
+
+void fused_set_checkpointing(bool on) { g_ckpt_on.store(on); }
 
 int64_t fused_ckpt_states(Program& p, const DevState& s) {
     if (!ckpt_enabled() || !fusable(s, geo_for(2).M)) return 0;

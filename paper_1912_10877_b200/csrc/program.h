@@ -54,6 +54,7 @@ void fused_stats(const Program& p, int64_t* fwd, int64_t* bwd);
 int64_t fused_ckpt_states(Program& p, const DevState& s);
 void fused_ckpt_forward(const DevState& in, Program& p, void* arena);
 void fused_ckpt_backward(const DevState& adj, Program& p, void* arena, double* d_grads /* nparams, += */);
+void fused_set_checkpointing(bool on);  // qbg_set_checkpointing (default on unless QBG_CKPT=0)
 std::string fused_plan_info(const Program& p);  // human-readable pass/stage layout
 // Host-only planner run (no device): forward + reverse plans for a 2^n x B register.
 std::string fused_plan_preview(const Program& p, int64_t B, int dtype);
