@@ -13,11 +13,12 @@ def test_plan_preview_25q_metric_workload():
     c = qb.variational_circuit(25, 10)
     qb.dispatch(c, "random")
     t = qb.compile_block(c).plan_preview()
-    fwd, bwd = t.split("plan dir=2")
-    nf = len(re.findall(r"tile Q=", fwd))
-    nb = len(re.findall(r"tile Q=", bwd))
-    # the fusion planner must cover 1025 gates in far fewer passes than gates
-    assert 0 < nf <= 40 and 0 < nb <= 45, (nf, nb)
+    plans = {int(m.group(1)): body for m, body in zip(re.finditer(r"plan dir=(\d)", t), re.split(r"plan dir=\d[^\n]*\n", t)[1:])}
+    npass = {d: len(re.findall(r"tile Q=", body)) for d, body in plans.items()}
+    # the fusion planner must cover 1025 gates in far fewer passes than gates: forward (0), reverse
+    # (2), and the checkpointed pair — reverse (5) and its forward mirror (4, >= one pass per segment)
+    assert 0 < npass[0] <= 40 and 0 < npass[2] <= 45, npass
+    assert 0 < npass[5] <= 40 and npass[4] >= npass[5], npass
     assert "single gate" not in t  # every gate of the variational circuit tiles
     # every tile holds the three low (coalescing) qubits
     assert all(q.startswith("0,1,2,") for q in re.findall(r"tile Q=([\d,]+)", t))
