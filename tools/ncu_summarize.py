@@ -2,6 +2,7 @@
 
     python tools/ncu_summarize.py launches <launches.csv>          # per-kernel share of device time
     python tools/ncu_summarize.py traffic <report.ncu-rep> <name>   # dram bytes per launch -> json
+    python tools/ncu_summarize.py mix <sass.csv> <label>             # executed instructions per opcode
 """
 import collections
 import csv
@@ -43,17 +44,39 @@ def traffic(rep, name):
     res = {}
     for r in rows[2:]:
         d = dict(zip(hdr, r))
-        rd = float(d["dram__bytes_read.sum"].replace(",", ""))
-        wr = float(d["dram__bytes_write.sum"].replace(",", ""))
-        unit_r = rows[1][hdr.index("dram__bytes_read.sum")]
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit_r, 1)
-        res = {name: (rd + wr) * scale, "dram_read_bytes": rd * scale, "dram_write_bytes": wr * scale,
+        units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        rd = float(d["dram__bytes_read.sum"].replace(",", "")) * units.get(rows[1][hdr.index("dram__bytes_read.sum")], 1)
+        wr = float(d["dram__bytes_write.sum"].replace(",", "")) * units.get(rows[1][hdr.index("dram__bytes_write.sum")], 1)
+        res = {name: rd + wr, "dram_read_bytes": rd, "dram_write_bytes": wr,
                "duration": d.get("gpu__time_duration.sum"), "kernel": d.get("Kernel Name", "")[:80]}
     print(json.dumps(res))
+
+
+def mix(path, label):
+    rows = list(csv.reader(open(path)))
+    hdr = next(r for r in rows if r and r[0] == "Address")
+    ie = hdr.index("Instructions Executed")
+    cnt = collections.Counter()
+    for r in rows:
+        if len(r) <= ie or not r[0].startswith("0x"):
+            continue
+        toks = r[1].split()
+        if not toks:
+            continue
+        op = toks[1] if toks[0].startswith("@") and len(toks) > 1 else toks[0]
+        cnt[op.split(".")[0]] += int(float(r[ie] or 0))
+    tot = sum(cnt.values())
+    print(f"{label}: {tot} warp instructions executed")
+    for op, v in cnt.most_common(16):
+        print(f"{op:12s} {v:12d} {100 * v / tot:5.1f}%")
+    fp64 = sum(cnt[o] for o in ("DFMA", "DMUL", "DADD"))
+    print(f"FP64 (DFMA + DMUL + DADD): {100 * fp64 / tot:.1f}%")
 
 
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2])
+    elif sys.argv[1] == "mix":
+        mix(sys.argv[2], sys.argv[3])
     else:
         traffic(sys.argv[2], sys.argv[3])
