@@ -116,6 +116,14 @@ int pipe_slots(bool back, int M, bool c128, int ngrad, int nwt) {
     while (n > 2 && n * tile + cells + 128 > 220 * 1024) --n;
     return n;
 }
+// Checkpointed reverse passes: the slot (ψ and φ̄ tiles) is needed only until the statistics and the
+// read of φ̄ are done; φ̄'s transposes then use a private scratch tile of the consumer group, and the
+// slot is released at once, so the next tile loads during the whole uncompute sweep.  One slot per
+// consumer group (QBG_CK_SCRATCH=0: the shared ring, slot held to the end of the tile; A/B).
+bool ck_scratch() {
+    static const bool on = env_int("QBG_CK_SCRATCH", 1) != 0;
+    return on;
+}
 // Specialised-kernel defaults (measured on B200, 25q apply+grad, tools/sweep.py logs in
 // profiles/): forward 2^11-element tiles of 128 threads x 16 registers, 3 CTAs/SM; reverse
 // 2^11 x 2 states of 128 threads x 2x16, 2 CTAs/SM.  The interpreter keeps (12,4) / (11,3).
@@ -992,7 +1000,8 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
     const int NG = pipe ? consumer_groups(back) : 1;
     const int NWT = NG * NW;  // consumer warps
     const int CS = NWT + 1;   // gradient cell stride (odd: the lanes of a warp_sum hit distinct banks)
-    const int nbuf = pipe ? pipe_slots(back, M, c128, P.ngrad, NWT) : 1;
+    const bool scr = ck && ck_scratch();  // φ̄ scratch per group, early slot release (see ck_scratch)
+    const int nbuf = !pipe ? 1 : scr ? NG : pipe_slots(back, M, c128, P.ngrad, NWT);
     // who writes the results: with a deep ring the producer drains each computed slot to global
     // memory (consumers only compute); with a shallow one (reverse pass: 3 slots of 2 states) the
     // drain would delay the refill, so the consumers store from registers and release the slot
@@ -1036,7 +1045,9 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         s << "#define GI(e) (e)\n#define SI(e) (e)\n";
     }
     s << "extern __shared__ __align__(128) unsigned char smraw[];\n";
-    const size_t cells_off = nbuf * tile_bytes;
+    if (pstore && scr) raise(QBG_ERR_INTERNAL, "jit: a checkpointed pass drains no slot");
+    const size_t scr_off = nbuf * tile_bytes;
+    const size_t cells_off = scr_off + (scr ? static_cast<size_t>(NG) * (elem << M) : 0);
     const size_t bar_off = (cells_off + (back ? static_cast<size_t>(P.ngrad) * CS * 8 : 0) + 15) & ~size_t{15};
     if (pipe) {
         s << "V* ring = (V*)smraw;\n";
@@ -1148,6 +1159,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             if (inc > L) s << "reg_alloc<" << std::min(inc, 248) << ">();\n";
         }
         s << "const int cg = tid_all / " << TH << ", tid = tid_all & " << TH - 1 << ";\n";
+        if (scr) s << "V* const scr = (V*)(smraw + " << scr_off << ") + (size_t)cg * " << (1 << M) << "u;\n";
         if (back) s << "const int warp = cg * " << NW << " + (tid >> 5), lane = tid & 31;\n";
     } else if (back) {
         s << "for (int i = tid; i < " << P.ngrad * CS << "; i += " << TH << ") sg[i] = 0.0;\n" << SYNC;
@@ -1231,18 +1243,19 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         }
     }
     // register tile <-> shared memory: written with stage a's layout, read back with stage b's
+    std::string ybuf = "sy";  // where φ̄'s transposes go (checkpointed, after the slot release: scr)
     auto transpose = [&](int a, int b, bool tx, bool ty) {
         const DStage& Sa = P.st[a];
         const DStage& Sb = P.st[b];
         for (int j = 0; j < R; ++j) {
             if (tx) s << "sx[SI(st" << a << " ^ " << soff(Sa, j) << "u)] = x[" << j << "];";
-            if (ty) s << " sy[SI(st" << a << " ^ " << soff(Sa, j) << "u)] = y[" << j << "];";
+            if (ty) s << " " << ybuf << "[SI(st" << a << " ^ " << soff(Sa, j) << "u)] = y[" << j << "];";
             s << "\n";
         }
         s << SYNC;
         for (int j = 0; j < R; ++j) {
             if (tx) s << "x[" << j << "] = sx[SI(st" << b << " ^ " << soff(Sb, j) << "u)];";
-            if (ty) s << " y[" << j << "] = sy[SI(st" << b << " ^ " << soff(Sb, j) << "u)];";
+            if (ty) s << " y[" << j << "] = " << ybuf << "[SI(st" << b << " ^ " << soff(Sb, j) << "u)];";
             s << "\n";
         }
         s << SYNC;
@@ -1614,6 +1627,12 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                     if (is_stat(ops[i])) emit_op(ops[i]);
             }
         }
+        if (scr) {
+            // every read of the slot is done: release it (the producer refills it during the sweep)
+            if (use_tma) s << "fence_proxy_async();\n";
+            s << SYNC << "if (tid == 0) mbar_arrive(done + slot);\n";
+            ybuf = "scr";
+        }
         ex = false;
         for (int st = 0; st < P.nstages; ++st) {
             bool any = false;
@@ -1659,7 +1678,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             s << "\n";
         }
         if (exp_mode == 1 || exp_mode == 5 || exp_mode == 6) s << "}\n";
-        if (pipe) {
+        if (pipe && !scr) {
             if (use_tma) s << "fence_proxy_async();\n";
             s << SYNC << "if (tid == 0) mbar_arrive(done + slot);\n";
         }
@@ -1781,8 +1800,11 @@ void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128, bool check_
         const int nwt = (pipeline_enabled() ? consumer_groups(back) : 1) * NW;
         const size_t cells = back ? static_cast<size_t>(P.ngrad) * (nwt + 1) * 8 : 0;
         if (pipeline_enabled()) {
-            const int nbuf = pipe_slots(back, M, c128, P.ngrad, nwt);
-            st.smem = ((nbuf * tile_bytes + cells + 15) & ~size_t{15}) + 2 * nbuf * 8;
+            const bool scr = pl.dir == 5 && ck_scratch();
+            const int ng = consumer_groups(back);
+            const int nbuf = scr ? ng : pipe_slots(back, M, c128, P.ngrad, nwt);
+            const size_t scratch = scr ? static_cast<size_t>(ng) * (elem << M) : 0;
+            st.smem = ((nbuf * tile_bytes + scratch + cells + 15) & ~size_t{15}) + 2 * nbuf * 8;
         } else {
             st.smem = (P.nstages > 1 || back ? tile_bytes : 0) + cells;
         }
