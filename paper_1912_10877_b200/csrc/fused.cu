@@ -2566,6 +2566,12 @@ std::string gen_seed(const SPass& sp, const std::vector<SGroup>& groups, const s
             s << "acc[" << k << "] = phi[tb + " << goff(static_cast<uint32_t>(k) << TB) << "ll];\n";
     }
     s << "__syncthreads();\n";
+    // real coefficients (every Hermitian Pauli sum with i^{nY} folded in, e.g. heisenberg): the
+    // per-element update is a real scale-accumulate, 2 FMA instead of a complex one's 4
+    bool real = true;
+    for (int gi = sp.g0; gi < sp.g1; ++gi)
+        for (int t = groups[gi].term_begin; t < groups[gi].term_end; ++t) real = real && terms[t].cim == 0.0;
+    const char* WT = real ? "RT<V>::T" : "V";
     int tix = 0;
     for (int gi = sp.g0; gi < sp.g1; ++gi) {
         const SGroup& g = groups[gi];
@@ -2576,27 +2582,40 @@ std::string gen_seed(const SPass& sp, const std::vector<SGroup>& groups, const s
         int hi = 0;
         std::vector<uint32_t> hs;
         for (auto& [h, ts] : byh) {
-            s << "V W" << hi << " = mk<V>(0, 0);\n";
+            s << WT << " W" << hi << " = " << (real ? "0" : "mk<V>(0, 0)") << ";\n";
             for (int t : ts) {
                 const STerm& st = terms[t];
                 const int pidx = tix + (t - g.term_begin);
                 s << "{ const int par = (__popc((tid ^ " << xlow << "u) & " << (st.zloc & (T - 1)) << "u) + __popcll(outer & "
-                  << hex(st.zout) << ")) & 1; const V c = mk<V>(pm.m[" << 2 * pidx << "], pm.m[" << 2 * pidx + 1
-                  << "]); W" << hi << " = par ? mk<V>(W" << hi << ".x - c.x, W" << hi << ".y - c.y) : mk<V>(W" << hi
-                  << ".x + c.x, W" << hi << ".y + c.y); }\n";
+                  << hex(st.zout) << ")) & 1; ";
+                if (real)
+                    s << "const RT<V>::T c = pm.m[" << 2 * pidx << "]; W" << hi << " = par ? W" << hi << " - c : W" << hi
+                      << " + c; }\n";
+                else
+                    s << "const V c = mk<V>(pm.m[" << 2 * pidx << "], pm.m[" << 2 * pidx + 1 << "]); W" << hi
+                      << " = par ? mk<V>(W" << hi << ".x - c.x, W" << hi << ".y - c.y) : mk<V>(W" << hi << ".x + c.x, W" << hi
+                      << ".y + c.y); }\n";
             }
             hs.push_back(h);
             ++hi;
         }
         for (int k = 0; k < R; ++k) {
             const uint32_t kk = static_cast<uint32_t>(k) ^ xhigh;
-            s << "{ const V v = sp[(tid ^ " << xlow << "u) + " << (kk << TB) << "u]; V cf = mk<V>(0, 0);";
-            for (size_t h = 0; h < hs.size(); ++h) {
-                const bool neg = __builtin_popcount(kk & hs[h]) & 1;
-                s << " cf = mk<V>(cf.x " << (neg ? "-" : "+") << " W" << h << ".x, cf.y " << (neg ? "-" : "+") << " W" << h
-                  << ".y);";
+            s << "{ const V v = sp[(tid ^ " << xlow << "u) + " << (kk << TB) << "u]; ";
+            if (real) {
+                s << "RT<V>::T cf = 0;";
+                for (size_t h = 0; h < hs.size(); ++h)
+                    s << " cf " << ((__builtin_popcount(kk & hs[h]) & 1) ? "-" : "+") << "= W" << h << ";";
+                s << " acc[" << k << "] = mk<V>(fma(cf, v.x, acc[" << k << "].x), fma(cf, v.y, acc[" << k << "].y)); }\n";
+            } else {
+                s << "V cf = mk<V>(0, 0);";
+                for (size_t h = 0; h < hs.size(); ++h) {
+                    const bool neg = __builtin_popcount(kk & hs[h]) & 1;
+                    s << " cf = mk<V>(cf.x " << (neg ? "-" : "+") << " W" << h << ".x, cf.y " << (neg ? "-" : "+") << " W" << h
+                      << ".y);";
+                }
+                s << " acc[" << k << "] = cfma(acc[" << k << "], cf, v); }\n";
             }
-            s << " acc[" << k << "] = cfma(acc[" << k << "], cf, v); }\n";
         }
         s << "}\n";
         tix += g.term_end - g.term_begin;
