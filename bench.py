@@ -47,6 +47,8 @@ def parse():
                     help="qubits per GPU of the sharded state (33: 128 GiB per B200; n = this + log2 N)")
     ap.add_argument("--sharded-depth", type=int, default=2)
     ap.add_argument("--sharded-steps", type=int, default=3)
+    ap.add_argument("--sharded-timeout", type=float, default=420.0,
+                    help="seconds after which a stuck sharded measurement is reported as an error")
     return ap.parse_args()
 
 
@@ -467,7 +469,7 @@ def main():
                     "fp64": fp64_roofline(top, per_launch_ms) if args.dtype == "c128" else None,
                     "per_gate_convention": per_gate_roofline(top, per_launch_ms, G, S, peak),
                     "kernels": [{k2: (round(v, 6) if isinstance(v, float) else v) for k2, v in kk.items()}
-                                for kk in kernels[:8]]}
+                                for kk in kernels[:16]]}
         # whole-step HBM throughput: every kernel's algorithmic bytes of one step over the step time
         step_bytes = sum(k["bytes"] for k in kernels) / 2
         roofline["step"] = {"hbm_gbs": step_bytes / (ms / 1e3) / 1e9, "frac": step_bytes / (ms / 1e3) / 1e9 / peak,
@@ -490,33 +492,47 @@ def main():
                "cpu_model": cb.cpu_model(), "job_seconds_extrapolated": r["job_seconds_extrapolated"],
                "extrapolation_check": cpu_validation()}
 
-    sharded = None
     prog_stats = prog.stats()
+    line = {
+        "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (zero_state, θ ~ U(0,2π) from Rng(42+rank))",
+        "config": workload_config(args),
+        "hbm_gbs_algorithmic": hbm_alg, "hbm_frac_algorithmic": hbm_alg / peak,
+        "hbm_note": "hbm_*_algorithmic use the per-gate convention (2S per gate per state pass, SURVEY 8(d)): "
+                    "> 1 because fusion applies ~34 gates per HBM pass; the real HBM rates are "
+                    "roofline.achieved (dominant kernel) and roofline.step (whole step)",
+        "energy": float(res.energies[0]),
+        "fusion": not args.no_fusion, "prog_stats": prog_stats,
+        "e2e": e2e, "gpu_launches": launches, "clocks": ck, "roofline": roofline, "cpu_baseline": cpu,
+        "sharded_state": None,
+    }
+
     if not args.no_sharded and args.dtype == "c128":
         del reg, prog
         import gc
         gc.collect()
         L.qbg_release_workspace()
+        # The sharded measurement is a secondary key of the metric line: a watchdog on every rank
+        # makes sure a stuck exchange can never swallow the line (rank 0 prints it, all ranks exit).
+        import threading
+
+        def _watchdog():
+            if rank == 0:
+                line["sharded_state"] = {"error": f"timed out after {args.sharded_timeout} s"}
+                print(json.dumps(line), flush=True)
+            os._exit(0)
+
+        wd = threading.Timer(args.sharded_timeout, _watchdog)
+        wd.daemon = True
+        wd.start()
         try:
-            sharded = sharded_weak_scaling(args, rank, world, pg)
+            line["sharded_state"] = sharded_weak_scaling(args, rank, world, pg)
         except Exception as e:  # reported, never fatal to the metric line
-            sharded = {"error": f"{type(e).__name__}: {e}"[:300]}
+            line["sharded_state"] = {"error": f"{type(e).__name__}: {e}"[:300]}
+        wd.cancel()
 
     if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": world, "steps": args.steps,
-            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (zero_state, θ ~ U(0,2π) from Rng(42+rank))",
-            "config": workload_config(args),
-            "hbm_gbs_algorithmic": hbm_alg, "hbm_frac_algorithmic": hbm_alg / peak,
-            "hbm_note": "hbm_*_algorithmic use the per-gate convention (2S per gate per state pass, SURVEY 8(d)): "
-                        "> 1 because fusion applies ~34 gates per HBM pass; the real HBM rates are "
-                        "roofline.achieved (dominant kernel) and roofline.step (whole step)",
-            "energy": float(res.energies[0]),
-            "fusion": not args.no_fusion, "prog_stats": prog_stats,
-            "e2e": e2e, "gpu_launches": launches, "clocks": ck, "roofline": roofline, "cpu_baseline": cpu,
-            "sharded_state": sharded,
-        }
         print(json.dumps(line), flush=True)
     if pg is not None:
         pg.barrier()

@@ -30,6 +30,7 @@
 #include <fstream>
 #include <map>
 #include <mutex>
+#include <set>
 #include <unordered_map>
 #include <memory>
 
@@ -1201,7 +1202,8 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         return o;
     };
     // diagnostics only (QBG_EXP): 1 = no global traffic (synthetic tile, stores never taken),
-    // 2 = no gate ops (pure load / transpose / store) — splits a pass into compute and memory time
+    // 2 = no gate ops (pure load / transpose / store) — splits a pass into compute and memory time;
+    // checkpointed reverse passes: 4 = no transposes, 7 = no statistics, 8 = no uncompute ops
     const int exp_mode = env_int("QBG_EXP", 0);
     if (!pipe) {
         s << "pdl_wait();\n";
@@ -1457,6 +1459,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             }
     };
     auto is_stat = [](const DOp& op) { return op.code >= G_DENSE1; };
+    int cur = 0;  // checkpointed pass: the stage layout the registers hold at the store
     if (!ck) {
         for (int st = 0; st < P.nstages; ++st) {
             const DStage& S = P.st[st];
@@ -1495,10 +1498,10 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                 else
                     generic = true;
             }
-        int cur = 0;
         if (!generic) {
             const int nlow = c128 ? 3 : 4;
-            const int ngroups = rops.empty() ? (dops.empty() ? 0 : 1) : static_cast<int>((rops.size() + RB - 1) / RB);
+            int ngroups = rops.empty() ? (dops.empty() ? 0 : 1) : static_cast<int>((rops.size() + RB - 1) / RB);
+            if (exp_mode == 7) ngroups = 0;  // (diagnostics: checkpointed pass without its statistics)
             for (int g = 0; g < ngroups; ++g) {
                 std::vector<int> rb;  // register slot k -> local bit
                 for (size_t r = static_cast<size_t>(g) * RB; r < rops.size() && rb.size() < static_cast<size_t>(RB); ++r)
@@ -1644,11 +1647,11 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             for (int i = P.st[st].op_begin; i < P.st[st].op_end; ++i) any |= !is_stat(ops[i]);
             if (!any && st != P.nstages - 1) continue;
             if (st != cur) {
-                transpose(cur, st, false, true);
+                if (exp_mode != 4) transpose(cur, st, false, true);  // (QBG_EXP=4: no transposes)
                 cur = st;
             }
             for (int i = P.st[st].op_begin; i < P.st[st].op_end; ++i)
-                if (!is_stat(ops[i])) emit_op(ops[i]);
+                if (!is_stat(ops[i]) && exp_mode != 8) emit_op(ops[i]);  // (QBG_EXP=8: no uncompute)
         }
     }
     if (pstore) {
@@ -1873,6 +1876,20 @@ void jit_prepare(FusedPlan& pl, int M, int RB, bool back, bool c128, bool check_
 }
 
 // ---- execution ---------------------------------------------------------------------------------
+// Profiling label of a tile pass.  QBG_PROF_KERNELS=1 (diagnostics) splits the fused_fwd /
+// fused_bwd totals of qbg_profile_report by pass structure: "<kind>:<stages>s<ops>o" plus the
+// per-stage op counts, so one bench run times each pass type without a profiler.
+const char* prof_name(const char* kind, const Step& st) {
+    static const bool on = env_int("QBG_PROF_KERNELS", 0) != 0;
+    if (!on) return kind;
+    static std::mutex mu;
+    static std::set<std::string> names;  // node-based: c_str() pointers stay valid
+    std::string n = std::string(kind) + ":" + std::to_string(st.pass.nstages) + "s" + std::to_string(st.pass.nops) + "o[";
+    for (int k = 0; k < st.pass.nstages; ++k)
+        n += std::to_string(st.pass.st[k].op_end - st.pass.st[k].op_begin) + (k + 1 < st.pass.nstages ? " " : "]");
+    std::lock_guard<std::mutex> lk(mu);
+    return names.insert(n).first->c_str();
+}
 template <typename V, bool BACK>
 void launch_jit(V* psi, V* adj, Step& st, FusedPlan& pl, double* gpart, int64_t gcols) {
     const int T = 1 << (pl.M - pl.RB);
@@ -1900,7 +1917,7 @@ void launch_jit(V* psi, V* adj, Step& st, FusedPlan& pl, double* gpart, int64_t 
         }
     }
     void* args[] = {&psi, &adj, &gpart, &gcols, &gbase, st.blob.data(), tmp, tma};
-    LaunchScope ls(BACK ? "fused_bwd" : "fused_fwd", bytes, st.flops);
+    LaunchScope ls(prof_name(BACK ? "fused_bwd" : "fused_fwd", st), bytes, st.flops);
     jit::launch(pl.jk[st.jk], static_cast<unsigned>(grid), pipe ? consumer_groups(BACK) * T + kProducerThreads : T, st.smem,
                 args);
     static const bool sync_each = env_int("QBG_SYNC_EACH", 0) != 0;  // diagnostics: localise a failing pass
