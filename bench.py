@@ -508,35 +508,41 @@ def main():
         "sharded_state": None,
     }
 
+    # The sharded measurement is a secondary key of the metric line: a watchdog on every rank
+    # makes sure a stuck exchange (or a peer stuck in NCCL after another rank failed) can never
+    # swallow the line or hang the job: rank 0 prints the line once, every rank exits.
+    import threading
+    printed = threading.Event()
+
+    def emit():
+        if rank == 0 and not printed.is_set():
+            printed.set()
+            print(json.dumps(line), flush=True)
+
+    def _watchdog():
+        if line["sharded_state"] is None and not args.no_sharded:
+            line["sharded_state"] = {"error": f"timed out after {args.sharded_timeout} s"}
+        emit()
+        os._exit(0)
+
+    wd = threading.Timer(args.sharded_timeout, _watchdog)
+    wd.daemon = True
+    wd.start()
     if not args.no_sharded and args.dtype == "c128":
         del reg, prog
         import gc
         gc.collect()
         L.qbg_release_workspace()
-        # The sharded measurement is a secondary key of the metric line: a watchdog on every rank
-        # makes sure a stuck exchange can never swallow the line (rank 0 prints it, all ranks exit).
-        import threading
-
-        def _watchdog():
-            if rank == 0:
-                line["sharded_state"] = {"error": f"timed out after {args.sharded_timeout} s"}
-                print(json.dumps(line), flush=True)
-            os._exit(0)
-
-        wd = threading.Timer(args.sharded_timeout, _watchdog)
-        wd.daemon = True
-        wd.start()
         try:
             line["sharded_state"] = sharded_weak_scaling(args, rank, world, pg)
         except Exception as e:  # reported, never fatal to the metric line
             line["sharded_state"] = {"error": f"{type(e).__name__}: {e}"[:300]}
-        wd.cancel()
 
-    if rank == 0:
-        print(json.dumps(line), flush=True)
+    emit()
     if pg is not None:
         pg.barrier()
         pg.destroy_process_group()
+    wd.cancel()
 
 
 if __name__ == "__main__":

@@ -1203,7 +1203,8 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
     };
     // diagnostics only (QBG_EXP): 1 = no global traffic (synthetic tile, stores never taken),
     // 2 = no gate ops (pure load / transpose / store) — splits a pass into compute and memory time;
-    // checkpointed reverse passes: 4 = no transposes, 7 = no statistics, 8 = no uncompute ops
+    // checkpointed reverse passes: 4 = no transposes, 7 = no statistics, 8 = no uncompute ops,
+    // 9 = at most two statistics groups, 10 = slot released before the statistics
     const int exp_mode = env_int("QBG_EXP", 0);
     if (!pipe) {
         s << "pdl_wait();\n";
@@ -1502,6 +1503,11 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             const int nlow = c128 ? 3 : 4;
             int ngroups = rops.empty() ? (dops.empty() ? 0 : 1) : static_cast<int>((rops.size() + RB - 1) / RB);
             if (exp_mode == 7) ngroups = 0;  // (diagnostics: checkpointed pass without its statistics)
+            if (exp_mode == 9) ngroups = std::min(ngroups, 2);  // (diagnostics: at most two groups)
+            if (exp_mode == 10 && scr) {  // (diagnostics: slot released before the statistics; wrong results)
+                if (use_tma) s << "fence_proxy_async();\n";
+                s << "if (tid == 0) mbar_arrive(done + slot);\n";
+            }
             for (int g = 0; g < ngroups; ++g) {
                 std::vector<int> rb;  // register slot k -> local bit
                 for (size_t r = static_cast<size_t>(g) * RB; r < rops.size() && rb.size() < static_cast<size_t>(RB); ++r)
@@ -1638,7 +1644,8 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         if (scr) {
             // every read of the slot is done: release it (the producer refills it during the sweep)
             if (use_tma) s << "fence_proxy_async();\n";
-            s << SYNC << "if (tid == 0) mbar_arrive(done + slot);\n";
+            s << SYNC;
+            if (exp_mode != 10 || generic) s << "if (tid == 0) mbar_arrive(done + slot);\n";
             ybuf = "scr";
         }
         ex = false;
@@ -2422,6 +2429,22 @@ std::string plans_text(const std::vector<std::shared_ptr<FusedPlan>>& plans) {
             s << " stages=" << P.nstages << " ops=" << P.nops << " [";
             for (int k = 0; k < P.nstages; ++k) s << P.st[k].op_end - P.st[k].op_begin << (k + 1 < P.nstages ? " " : "");
             s << "] comps=" << P.ngrad << " smem=" << st.smem << "\n";
+            static const bool verbose = env_int("QBG_PREVIEW_OPS", 0) != 0;  // diagnostics: stage layouts, ops
+            if (verbose)
+                for (int k = 0; k < P.nstages; ++k) {
+                    const DStage& S = P.st[k];
+                    s << "    stage " << k << " reg=";
+                    for (int r = 0; r < kMaxR && r < 4; ++r) s << int(S.lreg[r]) << (r < 3 ? "," : "");
+                    s << " ops:";
+                    for (int i = S.op_begin; i < S.op_end; ++i) {
+                        const DOp& o = c->ops[P.op_base + i];
+                        s << " " << int(o.code) << "(" << int(o.a) << "," << int(o.b) << ")";
+                        if (o.creg_mask) s << "r" << o.creg_mask;
+                        if (o.cthr_mask) s << "t" << o.cthr_mask;
+                        if (o.ctile_mask) s << "g";
+                    }
+                    s << "\n";
+                }
         }
     }
     return s.str();
