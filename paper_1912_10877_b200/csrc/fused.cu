@@ -438,6 +438,8 @@ bool pg_grad(const PG& g) { return !g.run.empty() || g.k != nullptr; }
 
 std::vector<int> emit_pass(FusedPlan& pl, int M, int RB, int nb, bool backward, int coal, uint64_t Q,
                            const std::vector<int>& sel);
+bool tma_box_ok(const DPass& P, int M);  // the tile is a <= 5-D TMA box (complex128)
+bool tma_enabled();
 
 // Greedy pass construction (see fused.h): a gate joins the pass when it does not conflict with
 // any gate already passed over and its non-diagonal targets fit in the tile qubit set.
@@ -559,8 +561,77 @@ std::vector<int> emit_pass(FusedPlan& pl, int M, int RB, int nb, bool backward, 
     const int max_mats = jit::enabled() ? kMaxMatsJit : kMaxMats;
     std::vector<int> back;
     {
-        // ---- stages ----
         TileGeom tg = geom(M, RB, nb, Q, pl.B);
+        // ---- permutation folding (DPass::nfold) ----
+        // Forward passes (plans 0, 4): the CNOT / X gates that can be hoisted to the pass start
+        // (every gate before them that stays a stage op touches other qubits) become the affine
+        // map of the stage-0 slot read.  Checkpointed reverse passes (plan 5): the ones that can
+        // sink to the pass end become the map of the scratch write feeding the tile's TMA store.
+        // They then need no register stage: a CNOT ring otherwise costs a register slot per stage
+        // for its next target.
+        DPass probe{};
+        probe.mq = mq;
+        probe.nb = nb;
+        {
+            int k = 0;
+            for (int q = 0; q < 64; ++q)
+                if ((Q >> q) & 1) probe.qpos[k++] = static_cast<uint8_t>(q);
+        }
+        probe.B = pl.B;
+        probe.nchunks = pl.B >> nb;
+        probe.ntiles = (uint64_t{1} << (n - mq)) * static_cast<uint64_t>(probe.nchunks);
+        // the reverse pass stores through its scratch tile with one TMA tensor store
+        const bool rstore_tma = backward && pl.dir == 5 && pipeline_enabled() && jit::enabled() && ck_scratch() &&
+                                tma_enabled() && pl.dtype == QBG_C128 && tma_box_ok(probe, M);
+        static const bool fold_env = env_int("QBG_FOLD", 1) != 0;  // (0: CNOTs stay stage ops; A/B)
+        const bool fold_on = fold_env && jit::enabled() && pipeline_enabled() && M <= kMaxFoldM &&
+                             (backward ? rstore_tma : (pl.dir == 0 || pl.dir == 4));
+        std::vector<int> folded;  // application order
+        std::vector<int> work = sel;
+        if (fold_on) {
+            auto foldable = [&](const PG& pg) {
+                const Gate& g = pg.gate();
+                if (pg.k || !pg.run.empty() || g.kind != QBG_MAT_PERMUTATION || g.t != 1 || popc(g.cmask) > 1) return false;
+                const bool x1 = g.perm[0] == 1 && g.m[0].re == 1 && g.m[0].im == 0 && g.m[1].re == 1 && g.m[1].im == 0;
+                return x1 && tg.local[g.tbit[0]] >= 0;
+            };
+            uint64_t blocked = 0;
+            std::vector<int> keep;
+            std::vector<uint64_t> outer_ctl;
+            auto take = [&](int gi) {
+                const PG& pg = pl.gates[gi];
+                if (!foldable(pg) || (pg.all() & blocked)) return false;
+                const uint64_t cm = pg.gate().cmask;
+                if (cm && tg.local[__builtin_ctzll(cm)] < 0 &&
+                    std::find(outer_ctl.begin(), outer_ctl.end(), cm) == outer_ctl.end()) {
+                    if (static_cast<int>(outer_ctl.size()) >= kMaxFoldOuter) return false;
+                    outer_ctl.push_back(cm);
+                }
+                return true;
+            };
+            if (!backward) {
+                for (int gi : sel) {
+                    if (take(gi)) folded.push_back(gi);
+                    else {
+                        blocked |= pl.gates[gi].all();
+                        keep.push_back(gi);
+                    }
+                }
+            } else {
+                for (size_t i = sel.size(); i-- > 0;) {
+                    const int gi = sel[i];
+                    if (take(gi)) folded.push_back(gi);
+                    else {
+                        blocked |= pl.gates[gi].all();
+                        keep.push_back(gi);
+                    }
+                }
+                std::reverse(folded.begin(), folded.end());
+                std::reverse(keep.begin(), keep.end());
+            }
+            work.swap(keep);
+        }
+        // ---- stages ----
         const int R = RB, Wn = M - RB;
         struct StagePlan {
             uint32_t S = 0;  // local register bits
@@ -610,7 +681,7 @@ std::vector<int> emit_pass(FusedPlan& pl, int M, int RB, int nb, bool backward, 
                 }
             };
             static const int seeds = env_int("QBG_STAGE_SEEDS", 16);  // (0: the plain scan; A/B)
-            std::vector<int> pending = sel;
+            std::vector<int> pending = work;
             while (!pending.empty()) {
                 StagePlan best, c;
                 std::vector<int> bleft, l;
@@ -640,6 +711,8 @@ std::vector<int> emit_pass(FusedPlan& pl, int M, int RB, int nb, bool backward, 
             for (size_t s = kMaxStages - 2; s < stages.size(); ++s)
                 back.insert(back.end(), stages[s].gates.begin(), stages[s].gates.end());
             stages.resize(kMaxStages - 2);
+            // a sunk gate must not overtake a deferred one: the reverse pass keeps none
+            if (backward) back.insert(back.end(), folded.begin(), folded.end()), folded.clear();
             std::sort(back.begin(), back.end());
         }
         // coalescing lane bits of the load / store layouts: the batch bits and the low qubits
@@ -658,10 +731,35 @@ std::vector<int> emit_pass(FusedPlan& pl, int M, int RB, int nb, bool backward, 
         // producer moves the tile and the consumers read / write its linear image in shared
         // memory: one low bit in registers is a 2-way bank conflict on that access — cheaper than
         // an extra stage (a transpose).  The reverse pass's consumers store to global memory.
+        // (A checkpointed reverse pass with a TMA tensor store writes its tile to the scratch in
+        // the linear layout first, like the forward's drain.)
         auto needs_extra = [&](uint32_t S, bool store) {
-            if (!pipeline_enabled() || (store && backward)) return (S & C) != 0;
+            if (!pipeline_enabled() || (store && backward && !rstore_tma)) return (S & C) != 0;
             return __builtin_popcount(S & C) >= 2;
         };
+        if (stages.empty()) stages.push_back(StagePlan{fill(0), {}});  // every gate folded
+        // Before adding a layout-only stage, try to move the offending first / last stage inward
+        // past stages whose gates all commute with its own (disjoint qubits): a pass of rotation
+        // runs whose CNOTs are folded then needs no extra transpose for its low-qubit runs.
+        auto commute = [&](const StagePlan& a, const StagePlan& b) {
+            for (int ga : a.gates)
+                for (int gb : b.gates)
+                    if (pl.gates[ga].all() & pl.gates[gb].all()) return false;
+            return true;
+        };
+        const int ns = static_cast<int>(stages.size());
+        if (ns >= 3 && needs_extra(stages.front().S, false)) {
+            int best = -1;
+            for (int p = 1; p <= ns - 2 && commute(stages[0], stages[p]); ++p)
+                if (!needs_extra(stages[1].S, false)) best = p;
+            if (best > 0) std::rotate(stages.begin(), stages.begin() + 1, stages.begin() + best + 1);
+        }
+        if (ns >= 3 && needs_extra(stages.back().S, true)) {
+            int best = -1;
+            for (int p = ns - 2; p >= 1 && commute(stages[ns - 1], stages[p]); --p)
+                if (!needs_extra(stages[ns - 2].S, true)) best = p;
+            if (best > 0) std::rotate(stages.begin() + best, stages.end() - 1, stages.end());
+        }
         if (needs_extra(stages.front().S, false)) stages.insert(stages.begin(), StagePlan{fill(0), {}});
         if (needs_extra(stages.back().S, true)) stages.push_back(StagePlan{fill(0), {}});
 
@@ -888,6 +986,41 @@ std::vector<int> emit_pass(FusedPlan& pl, int M, int RB, int nb, bool backward, 
         if (P.nops > kMaxOps || P.nmats > max_mats || P.ngrad > kMaxComps)
             raise(QBG_ERR_INTERNAL, "fused plan: pass exceeds its shared-memory budget");
         for (const StagePlan& sp : stages) step.members.insert(step.members.end(), sp.gates.begin(), sp.gates.end());
+        step.members.insert(step.members.end(), folded.begin(), folded.end());
+        std::sort(step.members.begin(), step.members.end());
+        // the fold map: forward F = C_1 ∘ … ∘ C_m (slot address of the element a register holds),
+        // reverse F = D_m ∘ … ∘ D_1 (where the element lands); both built by right composition
+        // F ← F ∘ G of an X / CNOT G: l ↦ l ⊕ [control = v] e_t (G is an involution)
+        if (!folded.empty()) {
+            P.nfold = static_cast<int>(folded.size());
+            for (int k = 0; k < kMaxFoldM; ++k) P.fcol[k] = k < M ? 1u << k : 0u;
+            auto rcompose = [&](const Gate& g) {
+                const uint32_t ct = P.fcol[tg.local[g.tbit[0]]];
+                if (g.cmask == 0) {
+                    P.fd ^= ct;
+                    return;
+                }
+                const int q = __builtin_ctzll(g.cmask);
+                if (!((g.cval >> q) & 1)) P.fd ^= ct;  // control on 0: [l_c = 0] = l_c ⊕ 1
+                const int c = tg.local[q];
+                if (c >= 0) {
+                    P.fcol[c] ^= ct;
+                    return;
+                }
+                int i = 0;
+                while (i < P.nfo && P.foq[i] != q) ++i;
+                if (i == P.nfo) {
+                    P.foq[i] = static_cast<uint8_t>(q);
+                    P.fow[i] = 0;
+                    ++P.nfo;
+                }
+                P.fow[i] ^= ct;
+            };
+            if (!backward)
+                for (int gi : folded) rcompose(pl.gates[gi].gate());
+            else
+                for (size_t i = folded.size(); i-- > 0;) rcompose(pl.gates[folded[i]].gate());
+        }
         pl.ncomps += ncomp;
         pl.steps.push_back(step);
         pl.tile_passes++;
@@ -991,6 +1124,10 @@ bool tma_layout(const DPass& P, int M, bool c128, std::vector<TmaDim>& dims) {
     }
     return dims.size() <= 5;
 }
+bool tma_box_ok(const DPass& P, int M) {
+    std::vector<TmaDim> dims;
+    return tma_layout(P, M, true, dims);
+}
 
 std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, bool back, bool c128, bool ck = false) {
     const int R = 1 << RB, W = M - RB, TH = 1 << W, NW = TH / 32;
@@ -1016,6 +1153,11 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
     std::vector<TmaDim> td;
     const bool use_tma = pipe && tma_enabled() && tma_layout(P, M, c128, td);
     const bool tstore = use_tma && tma_store_enabled();  // (used where the producer drains: pstore)
+    // checkpointed reverse pass: the consumers store φ̄ by a TMA tensor store from their scratch
+    // (emit_pass plans the last stage for it: rstore_tma)
+    const bool rstore = ck && scr && use_tma;
+    if (P.nfold && (!pipe || (back && !rstore)))
+        raise(QBG_ERR_INTERNAL, "jit: folded permutations need the pipelined load (forward) or the TMA store (reverse)");
     auto tma_coords = [&](const std::string& outer, const std::string& tile) {
         std::ostringstream co;
         for (size_t d = 0; d < td.size(); ++d) {
@@ -1195,6 +1337,26 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             if ((j >> k) & 1) o |= 1u << S.lreg[k];
         return o;
     };
+    // the fold map (DPass::nfold) of a local offset, and the per-thread / per-tile parts of a
+    // folded stage-0 read (forward) or scratch write (reverse)
+    auto fmap = [&](uint32_t l) {
+        uint32_t o = 0;
+        for (int k = 0; k < M; ++k)
+            if ((l >> k) & 1) o ^= P.nfold ? P.fcol[k] : 1u << k;
+        return o;
+    };
+    auto fthr = [&](const DStage& S) {
+        uint32_t w[kMaxW];
+        for (int p = 0; p < W; ++p) w[p] = fmap(1u << S.lthr[p]);
+        return tid_sum(w, W, true);
+    };
+    auto ftile = [&]() {
+        std::ostringstream o;
+        o << (P.nfold ? P.fd : 0u) << "u";
+        for (int i = 0; i < P.nfo; ++i)
+            o << " ^ (((outer >> " << int(P.foq[i]) << ") & 1ull) ? " << P.fow[i] << "u : 0u)";
+        return o.str();
+    };
     auto soff = [&](const DStage& S, int j) {
         uint32_t o = 0;
         for (int k = 0; k < RB; ++k)
@@ -1237,6 +1399,9 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
                 if (exp_mode == 5 || exp_mode == 6) {  // (diagnostics: synthetic tile, no slot reads / global stores)
                     s << "x[" << j << "] = mk<V>((double)(tid + " << j << ") * 1e-3, (double)tile * 1e-9);";
                     if (back) s << " y[" << j << "] = mk<V>((double)(tid - " << j << ") * 1e-3, 1e-9);";
+                } else if (P.nfold && !back) {  // folded permutations: the affine slot address
+                    if (j == 0) s << "const unsigned lin0f = (" << fthr(S0) << ") ^ (" << ftile() << ");\n";
+                    s << "x[" << j << "] = sx[SI(lin0f ^ " << fmap(loff(S0, j)) << "u)];";
                 } else {
                     s << "x[" << j << "] = sx[SI(lin0 | " << loff(S0, j) << "u)];";
                     if (back) s << " y[" << j << "] = sy[SI(lin0 | " << loff(S0, j) << "u)];";
@@ -1642,8 +1807,10 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
             }
         }
         if (scr) {
-            // every read of the slot is done: release it (the producer refills it during the sweep)
-            if (use_tma) s << "fence_proxy_async();\n";
+            // every read of the slot is done: release it (the producer refills it during the sweep).
+            // With the TMA store, the group's previous store must have read the scratch before the
+            // sweep writes it again (it had the whole statistics phase to do so).
+            if (use_tma) s << "fence_proxy_async();\nif (tid == 0) tma_wait_read0();\n";
             s << SYNC;
             if (exp_mode != 10 || generic) s << "if (tid == 0) mbar_arrive(done + slot);\n";
             ybuf = "scr";
@@ -1687,10 +1854,21 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         s << SYNC << "if (tid == 0) mbar_arrive(done + slot);\n";
     } else {
         if (exp_mode == 1 || exp_mode == 5 || exp_mode == 6) s << "if (outer == ~0ull) {\n";
-        for (int j = 0; j < R; ++j) {
-            if (!ck) s << (back ? "psi" : "outp") << "[GI(tb + gL + " << goff(SL, j) << "ll)] = x[" << j << "];";
-            if (back) s << " adj[GI(tb + gL + " << goff(SL, j) << "ll)] = y[" << j << "];";
-            s << "\n";
+        if (rstore) {
+            // checkpointed reverse pass: φ̄ into the group's scratch in the tile's linear (TMA box)
+            // layout — through the fold map when the pass ends with folded permutations — then one
+            // TMA tensor store by one thread
+            const DStage& SC = P.st[cur];
+            s << "{ const unsigned linS = (" << fthr(SC) << ") ^ (" << ftile() << ");\n";
+            for (int j = 0; j < R; ++j) s << "scr[SI(linS ^ " << fmap(loff(SC, j)) << "u)] = y[" << j << "];\n";
+            s << "}\nfence_proxy_async();\n" << SYNC;
+            s << "if (tid == 0) {\ntma_store" << td.size() << "(&tma, scr, " << tma_coords("outer", "tile") << ");\ntma_commit();\n}\n";
+        } else {
+            for (int j = 0; j < R; ++j) {
+                if (!ck) s << (back ? "psi" : "outp") << "[GI(tb + gL + " << goff(SL, j) << "ll)] = x[" << j << "];";
+                if (back) s << " adj[GI(tb + gL + " << goff(SL, j) << "ll)] = y[" << j << "];";
+                s << "\n";
+            }
         }
         if (exp_mode == 1 || exp_mode == 5 || exp_mode == 6) s << "}\n";
         if (pipe && !scr) {
@@ -1699,6 +1877,7 @@ std::string gen_pass(const DPass& P, const DOp* ops, int nmats, int M, int RB, b
         }
     }
     s << "}\n";  // tile loop
+    if (rstore) s << "if (tid == 0) tma_wait0();\n";
     if (back) {
         if (pipe)
             s << "group_bar<" << NG * TH << ">(" << 1 + NG << ");\nconst int tc = tid_all;\n";
@@ -1777,6 +1956,14 @@ uint64_t pass_key(const DPass& P, const DOp* ops, int M, int RB, bool back, bool
         mix(S.gthr, sizeof(int64_t) * W);
         mix(S.lreg, static_cast<size_t>(RB));
         mix(S.lthr, static_cast<size_t>(W));
+    }
+    mixv(P.nfold);
+    if (P.nfold) {
+        mix(P.fcol, sizeof(uint32_t) * M);
+        mixv(P.fd);
+        mixv(P.nfo);
+        mix(P.foq, static_cast<size_t>(P.nfo));
+        mix(P.fow, sizeof(uint32_t) * P.nfo);
     }
     mix(ops, sizeof(DOp) * static_cast<size_t>(P.nops));
     return h;

@@ -56,6 +56,8 @@ struct DOp {
 static_assert(sizeof(DOp) == 48, "DOp layout");
 
 constexpr int kMaxR = 5;
+constexpr int kMaxFoldM = 16;     // local index bits a fold map covers
+constexpr int kMaxFoldOuter = 8;  // outer-controlled folded gates per pass (distinct controls)
 constexpr int kMaxW = 10;
 constexpr int kMaxStages = 12;
 
@@ -84,6 +86,17 @@ struct DPass {
     int32_t nmats;
     int32_t grad_base; // first gradient component of the pass (row of the partials buffer)
     DStage st[kMaxStages];
+    // Folded permutation gates (specialised pipelined kernels only): the CNOT / X gates at the
+    // start of a forward pass (at the end of a checkpointed reverse pass) are not register-stage
+    // ops but an affine map F of the tile's local index, applied to the slot address of the
+    // stage-0 read (forward) or of the write that feeds the tile's TMA store (reverse):
+    //   F(l) = XOR_k l_k fcol[k]  ^  fd  ^  XOR_i outer_bit(foq[i]) fow[i]
+    int32_t nfold;      // folded gates (0: none)
+    int32_t nfo;        // outer-controlled terms
+    uint32_t fcol[kMaxFoldM];
+    uint32_t fd;
+    uint8_t foq[kMaxFoldOuter];   // global qubit of an outer control
+    uint32_t fow[kMaxFoldOuter];  // its local mask
 };
 
 // Observable seed pass: groups of Pauli terms sharing one local X mask.
