@@ -1415,11 +1415,17 @@ void grad_driver(qbg_reg* r, Program& p, int32_t inplace, qbg_reg* state_grad, d
     // after every reverse segment in an arena, the reverse passes read ψ instead of uncomputing it;
     // the caller's register is not modified (in place or not, it ends as it started)
     if (g_fusion) {
-        const int64_t k = fused_ckpt_states(p, r->s);
+        int64_t k = fused_ckpt_states(p, r->s);
         void* arena = k > 0 ? ckpt_get(k, r->s) : nullptr;
+        if (arena && !(fused_ckpt_forward(r->s, p, arena, k) && fused_ckpt_sync(p, r->s, k))) {
+            // the program's structure changed with θ: the plans are rebuilt, run the forward again
+            k = fused_ckpt_states(p, r->s);
+            arena = k > 0 ? ckpt_get(k, r->s) : nullptr;
+            if (arena && !(fused_ckpt_forward(r->s, p, arena, k) && fused_ckpt_sync(p, r->s, k)))
+                raise(QBG_ERR_INTERNAL, "expect': checkpointed plans inconsistent after a rebuild");
+        }
         if (arena) {
             Nvtx nv("qbg.expect_grad.checkpointed");
-            fused_ckpt_forward(r->s, p, arena);
             DevState psi = r->s;
             psi.ptr = arena;  // checkpoint 0: the output state
             double* e = static_cast<double*>(scratch(r->s.B * sizeof(double), 10));

@@ -333,6 +333,7 @@ struct Step {
     std::vector<char> blob;      // its matrix parameter (PM<T, 2*nmats>)
     size_t smem = 0;
     double flops = 0;            // algorithmic FP64 flops of one launch (pass_flops)
+    int msrc_begin = 0, msrc_end = 0;  // its matrices' entries in FusedPlan::msrc (refresh_segment)
 };
 
 }  // namespace
@@ -356,6 +357,7 @@ struct FusedPlan {
     std::vector<std::vector<int>> part;
     std::vector<uint64_t> part_q;      // tile qubits of a segment's passes (0: a single-gate step)
     std::vector<int> seg_steps;        // first step of each segment (+ end)
+    std::vector<int> seg_gates;        // first fused gate of each segment (+ end)
     uint64_t serial = 0, mirror_of = 0;
     int64_t ncomps = 0;
     std::vector<jit::Kernel> jk;
@@ -780,6 +782,7 @@ std::vector<int> emit_pass(FusedPlan& pl, int M, int RB, int nb, bool backward, 
         P.ntiles = (uint64_t{1} << (n - mq)) * static_cast<uint64_t>(P.nchunks);
         P.op_base = static_cast<int>(pl.ops.size());
         P.mat_base = static_cast<int>(pl.mats.size());
+        step.msrc_begin = static_cast<int>(pl.msrc.size());
         P.grad_base = static_cast<int>(pl.ncomps);
         int ncomp = 0;
         for (int s = 0; s < P.nstages; ++s) {
@@ -985,6 +988,7 @@ std::vector<int> emit_pass(FusedPlan& pl, int M, int RB, int nb, bool backward, 
         P.ngrad = ncomp;
         if (P.nops > kMaxOps || P.nmats > max_mats || P.ngrad > kMaxComps)
             raise(QBG_ERR_INTERNAL, "fused plan: pass exceeds its shared-memory budget");
+        step.msrc_end = static_cast<int>(pl.msrc.size());
         for (const StagePlan& sp : stages) step.members.insert(step.members.end(), sp.gates.begin(), sp.gates.end());
         step.members.insert(step.members.end(), folded.begin(), folded.end());
         std::sort(step.members.begin(), step.members.end());
@@ -2295,6 +2299,39 @@ bool refresh_values(FusedPlan& pl, const Program& p) {
     return true;
 }
 
+// The values-only refresh of one segment of a mirror plan (dir 4): its fused gates, matrices and
+// kernel parameters, so the checkpointed forward can launch segment k while the host refreshes
+// segment k + 1.  False when the segment's structure changed (the caller rebuilds the plans).
+bool refresh_segment(FusedPlan& pl, const Program& p, size_t k) {
+    std::vector<PG> gs = mirror_gates(p, {pl.part[k]}, nullptr);
+    const int g0 = pl.seg_gates[k], g1 = pl.seg_gates[k + 1];
+    if (static_cast<int>(gs.size()) != g1 - g0) return false;
+    for (size_t i = 0; i < gs.size(); ++i)
+        if (pg_sig(gs[i]) != pl.sig[g0 + i]) return false;
+    for (size_t i = 0; i < gs.size(); ++i) pl.gates[g0 + i] = std::move(gs[i]);
+    const bool c128 = pl.dtype == QBG_C128;
+    for (int si = pl.seg_steps[k]; si < pl.seg_steps[k + 1]; ++si) {
+        Step& st = pl.steps[si];
+        if (!st.tile) continue;
+        size_t at = static_cast<size_t>(st.pass.mat_base);
+        for (int m = st.msrc_begin; m < st.msrc_end; ++m) {
+            const MatSrc& ms = pl.msrc[m];
+            const Gate& g = pl.gates[ms.gi].gate();
+            std::vector<cdbl> v = ms.what == MS_G ? g.m : dense_of(g);  // (mirror plans: no K matrices)
+            if (at + v.size() > pl.mats.size()) raise(QBG_ERR_INTERNAL, "fused plan: segment refresh out of range");
+            std::copy(v.begin(), v.end(), pl.mats.begin() + static_cast<std::ptrdiff_t>(at));
+            at += v.size();
+        }
+        if (at != static_cast<size_t>(st.pass.mat_base + st.pass.nmats))
+            raise(QBG_ERR_INTERNAL, "fused plan: segment refresh does not match the plan layout");
+        fill_blob(st, pl.mats, c128);
+        if (st.jk < 0 && st.pass.nmats)  // interpreter kernels read the device table
+            QBG_CUDA(cudaMemcpyAsync(pl.d_mats + st.pass.mat_base, pl.mats.data() + st.pass.mat_base,
+                                     st.pass.nmats * sizeof(cdbl), cudaMemcpyHostToDevice, stream()));
+    }
+    return true;
+}
+
 std::atomic<uint64_t> g_plan_serial{0};
 
 // The forward mirror (dir 4) of a checkpointed reverse plan (dir 5): one segment per reverse step,
@@ -2325,6 +2362,7 @@ std::shared_ptr<FusedPlan> build_mirror_plan(const Program& p, const FusedPlan& 
     }
     std::vector<int> seg_begin;
     pl->gates = mirror_gates(p, pl->part, &seg_begin);
+    pl->seg_gates = seg_begin;
     pl->sig.reserve(pl->gates.size());
     for (const PG& g : pl->gates) pl->sig.push_back(pg_sig(g));
     const int nb = batch_bits(rev.B);
@@ -2505,10 +2543,11 @@ std::shared_ptr<FusedPlan> get_mirror(Program& p, const DevState& s, const Fused
 }
 
 template <typename V>
-void run_ckpt_forward(const DevState& in, FusedPlan& fw, char* arena) {
+bool run_ckpt_forward(const DevState& in, FusedPlan& fw, char* arena, const Program* refresh = nullptr) {
     const size_t nseg = fw.part.size(), sb = in.bytes();
     const void* cur = in.ptr;
     for (size_t k = 0; k < nseg; ++k) {
+        if (refresh && !refresh_segment(fw, *refresh, k)) return false;
         DevState d = in;
         d.ptr = arena + (nseg - 1 - k) * sb;  // checkpoint of reverse step nseg-1-k
         bool placed = false;
@@ -2533,26 +2572,69 @@ void run_ckpt_forward(const DevState& in, FusedPlan& fw, char* arena) {
         if (!placed) QBG_CUDA(cudaMemcpyAsync(d.ptr, cur, sb, cudaMemcpyDeviceToDevice, stream()));
         cur = d.ptr;
     }
+    if (refresh) {
+        if (!fw.mats.empty())  // the whole device table at once (only interpreter kernels read it)
+            QBG_CUDA(cudaMemcpyAsync(fw.d_mats, fw.mats.data(), fw.mats.size() * sizeof(cdbl), cudaMemcpyHostToDevice,
+                                     stream()));
+        fw.version = refresh->version;
+    }
+    return true;
 }
 }  // namespace
 
 void fused_set_checkpointing(bool on) { g_ckpt_on.store(on); }
 
+// A new θ rewrites the values of both plans (refresh_values: the program's fused gates, their
+// signatures, matrices and gradient matrices — host work of a few hundred µs per plan).  The
+// reverse plan's refresh is deferred until the forward passes are queued (fused_ckpt_sync), so it
+// overlaps them instead of delaying the step's first launch; the step count and the segments the
+// forward needs are structure, which a value refresh never changes.
+namespace {
+std::shared_ptr<FusedPlan> peek_plan(Program& p, const DevState& s, int dir) {
+    for (auto& c : p.plans)
+        if (c->dir == dir && c->B == s.B && c->dtype == s.dtype && c->n == s.n) return c;
+    return nullptr;
+}
+std::shared_ptr<FusedPlan> find_mirror(Program& p, const DevState& s, const FusedPlan& rev) {
+    for (auto& c : p.plans)
+        if (c->dir == 4 && c->B == s.B && c->dtype == s.dtype && c->n == s.n && c->mirror_of == rev.serial) return c;
+    return nullptr;
+}
+}  // namespace
+
 int64_t fused_ckpt_states(Program& p, const DevState& s) {
     if (!ckpt_enabled() || !fusable(s, geo_for(2).M)) return 0;
-    auto rev = get_plan(p.plans, p, s, 5);
+    auto rev = peek_plan(p, s, 5);
+    if (!rev) rev = get_plan(p.plans, p, s, 5);
     for (auto& st : rev->steps)
         if (st.tile && st.jk < 0) return 0;  // (JIT unavailable: the interpreter has no checkpointed pass)
     return static_cast<int64_t>(rev->steps.size());
 }
 
-void fused_ckpt_forward(const DevState& in, Program& p, void* arena) {
-    auto rev = get_plan(p.plans, p, in, 5);
-    auto fw = get_mirror(p, in, *rev);
-    if (in.dtype == QBG_C128)
-        run_ckpt_forward<double2>(in, *fw, static_cast<char*>(arena));
-    else
-        run_ckpt_forward<float2>(in, *fw, static_cast<char*>(arena));
+bool fused_ckpt_forward(const DevState& in, Program& p, void* arena, int64_t k) {
+    auto rev = peek_plan(p, in, 5);
+    if (!rev) rev = get_plan(p.plans, p, in, 5);
+    auto fw = find_mirror(p, in, *rev);
+    auto run = [&](FusedPlan& f, const Program* refresh) {
+        return in.dtype == QBG_C128 ? run_ckpt_forward<double2>(in, f, static_cast<char*>(arena), refresh)
+                                    : run_ckpt_forward<float2>(in, f, static_cast<char*>(arena), refresh);
+    };
+    // a new θ on a known structure: each segment is refreshed right before its passes are queued
+    static const bool lazy = env_int("QBG_LAZY_REFRESH", 1) != 0;  // (0: the whole plan first; A/B)
+    if (fw && fw->version != p.version && !fw->seg_gates.empty() && lazy && run(*fw, &p)) return true;
+    if (!fw || !(fw->version == p.version || refresh_values(*fw, p))) {
+        // first use, or the program's structure changed with θ: the reverse plan first
+        rev = get_plan(p.plans, p, in, 5);
+        if (static_cast<int64_t>(rev->steps.size()) != k) return false;
+        fw = get_mirror(p, in, *rev);
+    }
+    return run(*fw, nullptr);
+}
+
+bool fused_ckpt_sync(Program& p, const DevState& s, int64_t k) {
+    auto rev = get_plan(p.plans, p, s, 5);  // refresh (or rebuild: a new serial)
+    auto fw = find_mirror(p, s, *rev);
+    return fw && fw->version == p.version && static_cast<int64_t>(rev->steps.size()) == k;
 }
 
 void fused_ckpt_backward(const DevState& adj, Program& p, void* arena, double* d_grads) {

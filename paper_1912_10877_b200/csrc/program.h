@@ -52,7 +52,11 @@ void fused_stats(const Program& p, int64_t* fwd, int64_t* bwd);
 // unavailable, use fused_forward / fused_backward); the forward writes them into arena (checkpoint 0
 // = the output state), the reverse pass reads them
 int64_t fused_ckpt_states(Program& p, const DevState& s);
-void fused_ckpt_forward(const DevState& in, Program& p, void* arena);
+// false: the program's structure changed with θ (plans rebuilt); the caller sizes the arena again
+bool fused_ckpt_forward(const DevState& in, Program& p, void* arena, int64_t k);
+// after the forward is queued: brings the reverse plan up to date; false if the forward just run
+// used segments of a stale structure (the caller runs the forward again)
+bool fused_ckpt_sync(Program& p, const DevState& s, int64_t k);
 void fused_ckpt_backward(const DevState& adj, Program& p, void* arena, double* d_grads /* nparams, += */);
 void fused_set_checkpointing(bool on);  // qbg_set_checkpointing (default on unless QBG_CKPT=0)
 std::string fused_plan_info(const Program& p);  // human-readable pass/stage layout
