@@ -2697,7 +2697,9 @@ std::string plans_text(const std::vector<std::shared_ptr<FusedPlan>>& plans) {
             for (int k = 0; k < P.mq; ++k) s << int(P.qpos[k]) << (k + 1 < P.mq ? "," : "");
             s << " stages=" << P.nstages << " ops=" << P.nops << " [";
             for (int k = 0; k < P.nstages; ++k) s << P.st[k].op_end - P.st[k].op_begin << (k + 1 < P.nstages ? " " : "");
-            s << "] comps=" << P.ngrad << " smem=" << st.smem << "\n";
+            s << "] comps=" << P.ngrad << " smem=" << st.smem;
+            if (P.nfold) s << " fold=" << P.nfold;
+            s << "\n";
             static const bool verbose = env_int("QBG_PREVIEW_OPS", 0) != 0;  // diagnostics: stage layouts, ops
             if (verbose)
                 for (int k = 0; k < P.nstages; ++k) {

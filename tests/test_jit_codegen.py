@@ -67,3 +67,19 @@ def test_random_circuit_kernels_generate_and_compile(n, seed):
     k = ctypes.c_int64()
     check(lib().qbg_jit_check(p._h, o._h, 1, 0, ctypes.byref(k)))
     assert k.value > 0
+
+
+def test_folded_checkpoint_plans_25q():
+    """Permutation folding: in the checkpointed pair of the 25q/d10 bench workload
+    every CNOT of the ring folds into the load / store maps, so each pass holds rotation runs only
+    (33 + 33 passes, 77 + 77 stages; 128 + 128 without folding)."""
+    c = qb.variational_circuit(25, 10)
+    qb.dispatch(c, "random")
+    t = qb.compile_block(c).plan_preview()
+    for d in (4, 5):
+        i = t.index(f"plan dir={d}")
+        j = t.find("plan dir", i + 5)
+        body = t[i:j if j > 0 else None]
+        assert len(re.findall("tile Q", body)) == 33, d
+        assert sum(int(x) for x in re.findall(r"stages=(\d+)", body)) <= 80, d
+        assert len(re.findall(r"fold=\d+", body)) >= 30, d  # the ring's CNOTs, in (almost) every pass
