@@ -2180,6 +2180,17 @@ void finalize_plan(FusedPlan& plr, const DevState& s, int dir) {
             static bool warned = false;
             const char* strict = std::getenv("QBG_JIT_STRICT");
             if (strict && strict[0] == '1') throw;
+            // the interpreter kernels know neither folded permutations nor the JIT-only stage ops:
+            // such a plan must not fall back silently
+            for (const auto& st : pl->steps) {
+                if (!st.tile) continue;
+                bool jit_only = st.pass.nfold != 0;
+                for (int i = 0; i < st.pass.nops && !jit_only; ++i) {
+                    const uint8_t c = pl->ops[st.pass.op_base + i].code;
+                    jit_only = c == OP_DENSE3 || c == OP_DENSE4 || c == G_CROSSH;
+                }
+                if (jit_only) throw;
+            }
             if (!warned) std::fprintf(stderr, "qbg: JIT specialisation failed, using the interpreter kernels: %s\n", e.what());
             warned = true;
             for (auto& st : pl->steps) st.jk = -1;
