@@ -186,11 +186,14 @@ void* ckpt_get(int64_t k, const DevState& s) {
         g_ckpt.state_bytes = std::max(g_ckpt.state_bytes, s.bytes());
         return g_ckpt.ptr;
     }
-    ckpt_free();
     ensure_device();
     size_t fr = 0, tot = 0;
     QBG_CUDA(cudaMemGetInfo(&fr, &tot));
     const size_t reserve = std::max<size_t>(size_t{4} << 30, tot / 16);
+    // (a request that cannot fit leaves the current arena alone)
+    if (need + reserve > fr + g_ckpt.bytes) return nullptr;
+    ckpt_free();
+    QBG_CUDA(cudaMemGetInfo(&fr, &tot));
     if (need + reserve > fr) return nullptr;
     void* p = nullptr;
     if (cudaMalloc(&p, need) != cudaSuccess) {
