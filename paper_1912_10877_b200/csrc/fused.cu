@@ -3021,7 +3021,9 @@ void run_seed(const DevState& psi, const DevState& phi, FusedPlan& pl, double* d
             double* ep = epart + (pl.energy_only ? static_cast<int64_t>(k) * per_pass : 0);
             void* args[] = {&pp, &qq, &ep, pl.sblob[k].data()};
             int64_t grid = std::min<int64_t>(static_cast<int64_t>(sp.ntiles), static_cast<int64_t>(num_sms()) * 2);
-            LaunchScope ls("seed", (pl.energy_only ? 1.0 : sp.first ? 2.0 : 3.0) * psi.bytes());
+            static const bool by_pass = env_int("QBG_PROF_KERNELS", 0) != 0;  // (diagnostics: see prof_name)
+            const char* nm = !by_pass ? "seed" : sp.first ? "seed:first" : sp.last ? "seed:last" : "seed:mid";
+            LaunchScope ls(nm, (pl.energy_only ? 1.0 : sp.first ? 2.0 : 3.0) * psi.bytes());
             jit::launch(pl.jk[pl.sjk[k]], static_cast<unsigned>(grid), 256, psi.elem() << kSeedM, args);
         }
     } else {
