@@ -2847,6 +2847,7 @@ std::shared_ptr<FusedPlan> make_seed_plan(const Observable& o, const DevState& s
 // terms with equal k-part Z mask are pre-summed per thread.
 // energy_only: every pass starts from zero and contributes Re Σ conj(ψ_l) (O_pass ψ)_l to the energy
 // directly (the groups' contributions are independent), so φ is never written.
+bool seed_tma(const SPass& sp, bool c128, std::vector<TmaDim>& td);
 std::string gen_seed(const SPass& sp, const std::vector<SGroup>& groups, const std::vector<STerm>& terms, bool c128,
                      bool energy_only) {
     constexpr int M = kSeedM, TB = 8, T = 1 << TB, R = 1 << (M - TB);
@@ -2854,12 +2855,19 @@ std::string gen_seed(const SPass& sp, const std::vector<SGroup>& groups, const s
     std::ostringstream s;
     int nterm = 0;
     for (int gi = sp.g0; gi < sp.g1; ++gi) nterm += groups[gi].term_end - groups[gi].term_begin;
-    s << "extern \"C\" __global__ void __launch_bounds__(" << T << ", " << kSeedMinB << ") __NAME__(const " << (c128 ? "c128" : "c64")
-      << "* __restrict__ psi, " << (c128 ? "c128" : "c64")
+    // Pipelined seed (complex128, tile a <= 5-D TMA box): one persistent CTA per SM, the ψ tile
+    // double-buffered in shared memory and loaded by TMA one tile ahead, so the next tile's load
+    // overlaps this tile's Pauli terms (the plain loop loads, synchronises, computes, stores).
+    std::vector<TmaDim> td;
+    const bool tpipe = seed_tma(sp, c128, td);
+    const size_t tile_bytes = static_cast<size_t>(c128 ? 16 : 8) << M;
+    s << "extern \"C\" __global__ void __launch_bounds__(" << T << ", " << (tpipe ? 1 : kSeedMinB) << ") __NAME__(const "
+      << (c128 ? "c128" : "c64") << "* __restrict__ psi, " << (c128 ? "c128" : "c64")
       << "* __restrict__ phi, double* __restrict__ epart, const __grid_constant__ PM<" << (c128 ? "double" : "float")
-      << ", " << std::max(2, 2 * nterm) << "> pm) {\n";
+      << ", " << std::max(2, 2 * nterm) << "> pm" << (tpipe ? ", const __grid_constant__ TMap tmp" : "") << ") {\n";
     s << "typedef " << (c128 ? "c128" : "c64") << " V;\nconst int tid = threadIdx.x;\n";
-    s << "extern __shared__ __align__(16) unsigned char smraw[];\nV* sp = (V*)smraw;\n__shared__ double red[" << T << "];\n";
+    s << "extern __shared__ __align__(128) unsigned char smraw[];\n__shared__ double red[" << T << "];\n";
+    if (!tpipe) s << "V* sp = (V*)smraw;\n";
     // element offset of local index l: batch bits, then tile qubits
     auto goff = [&](uint32_t l) {
         int64_t e = l & (bc - 1);
@@ -2872,27 +2880,61 @@ std::string gen_seed(const SPass& sp, const std::vector<SGroup>& groups, const s
     for (int p = 0; p < TB; ++p) wt[p] = goff(1u << p);
     s << "const i64 gt = " << tid_sum(wt, TB, false) << ";\n";
     s << "V acc[" << R << "];\n";
-    s << "pdl_wait();\n";  // launched with programmatic stream serialisation (jit::launch)
-    s << "for (u64 tile = blockIdx.x; tile < " << sp.ntiles << "ull; tile += gridDim.x) {\n";
+    // the tile's outer index (tile qubits deposited as zero bits) and batch chunk
+    s << "auto geo = [&](u64 tile, u64& outer, u64& c) {\n";
     if (sp.nchunks == 1)
-        s << "const u64 o = tile; const u64 c = 0;\n";
+        s << "const u64 o = tile; c = 0;\n";
     else
-        s << "const u64 o = tile / " << sp.nchunks << "ull; const u64 c = tile - o * " << sp.nchunks << "ull;\n";
-    s << "u64 outer = o;\n";
+        s << "const u64 o = tile / " << sp.nchunks << "ull; c = tile - o * " << sp.nchunks << "ull;\n";
+    s << "outer = o;\n";
     for (int k = 0; k < sp.mq; ++k) {
         int p = sp.qpos[k];
         s << "outer = ((outer >> " << p << ") << " << p + 1 << ") | (outer & " << hex((uint64_t{1} << p) - 1) << ");\n";
     }
-    s << "const i64 tb = (i64)outer * " << sp.B << "ll + (i64)c * " << bc << "ll + gt;\n";
-    s << "__syncthreads();\n";
-    for (int k = 0; k < R; ++k) s << "sp[tid + " << k * T << "] = psi[tb + " << goff(static_cast<uint32_t>(k) << TB) << "ll];\n";
-    for (int k = 0; k < R; ++k) {
-        if (sp.first || energy_only)
-            s << "acc[" << k << "] = mk<V>(0, 0);\n";
-        else
-            s << "acc[" << k << "] = phi[tb + " << goff(static_cast<uint32_t>(k) << TB) << "ll];\n";
+    s << "};\n";
+    if (tpipe) {
+        std::ostringstream co;  // TMA coordinates of a tile (outer, c), tma_layout's dimension order
+        for (size_t d = 0; d < td.size(); ++d) {
+            if (td[d].coord == 0) co << "0";
+            else if (td[d].coord == 1) co << "(int)c2";
+            else co << "(int)((o2 >> " << td[d].shift << ") & " << td[d].mask << "ull)";
+            if (d + 1 < td.size()) co << ", ";
+        }
+        s << "V* const sb = (V*)smraw;\nunsigned long long* const fb = (unsigned long long*)(smraw + " << 2 * tile_bytes << ");\n";
+        s << "if (tid == 0) { mbar_init(fb, 1); mbar_init(fb + 1, 1); }\n__syncthreads();\n";
+        s << "pdl_wait();\n";
+        s << "auto issue = [&](u64 t2, unsigned b2) { u64 o2, c2; geo(t2, o2, c2); mbar_arrive_tx(fb + b2, " << tile_bytes
+          << "u); tma_load" << td.size() << "(sb + b2 * " << (1u << M) << "u, &tmp, fb + b2, " << co.str() << "); };\n";
+        s << "if (tid == 0 && blockIdx.x < " << sp.ntiles << "ull) issue(blockIdx.x, 0u);\n";
+        s << "u64 it = 0;\n";
+        s << "for (u64 tile = blockIdx.x; tile < " << sp.ntiles << "ull; tile += gridDim.x, ++it) {\n";
+        s << "const unsigned b = (unsigned)(it & 1);\n";
+        // the other buffer was last read in the previous iteration (fenced and synchronised)
+        s << "if (tid == 0 && tile + gridDim.x < " << sp.ntiles << "ull) issue(tile + gridDim.x, b ^ 1u);\n";
+        s << "u64 outer, c; geo(tile, outer, c);\n";
+        s << "const i64 tb = (i64)outer * " << sp.B << "ll + (i64)c * " << bc << "ll + gt;\n";
+        for (int k = 0; k < R; ++k) {
+            if (sp.first || energy_only)
+                s << "acc[" << k << "] = mk<V>(0, 0);\n";
+            else
+                s << "acc[" << k << "] = phi[tb + " << goff(static_cast<uint32_t>(k) << TB) << "ll];\n";
+        }
+        s << "mbar_wait(fb + b, (unsigned)(it >> 1) & 1u);\nconst V* sp = sb + b * " << (1u << M) << "u;\n";
+    } else {
+        s << "pdl_wait();\n";  // launched with programmatic stream serialisation (jit::launch)
+        s << "for (u64 tile = blockIdx.x; tile < " << sp.ntiles << "ull; tile += gridDim.x) {\n";
+        s << "u64 outer, c; geo(tile, outer, c);\n";
+        s << "const i64 tb = (i64)outer * " << sp.B << "ll + (i64)c * " << bc << "ll + gt;\n";
+        s << "__syncthreads();\n";
+        for (int k = 0; k < R; ++k) s << "sp[tid + " << k * T << "] = psi[tb + " << goff(static_cast<uint32_t>(k) << TB) << "ll];\n";
+        for (int k = 0; k < R; ++k) {
+            if (sp.first || energy_only)
+                s << "acc[" << k << "] = mk<V>(0, 0);\n";
+            else
+                s << "acc[" << k << "] = phi[tb + " << goff(static_cast<uint32_t>(k) << TB) << "ll];\n";
+        }
+        s << "__syncthreads();\n";
     }
-    s << "__syncthreads();\n";
     // real coefficients (every Hermitian Pauli sum with i^{nY} folded in, e.g. heisenberg): the
     // per-element update is a real scale-accumulate, 2 FMA instead of a complex one's 4
     bool real = true;
@@ -2958,8 +3000,24 @@ std::string gen_seed(const SPass& sp, const std::vector<SGroup>& groups, const s
         s << "if (tid < " << bc << ") { double t = 0.0; for (int m = tid; m < " << T << "; m += " << bc
           << ") t += red[m]; epart[tile * " << bc << "ull + tid] = t; }\n";
     }
+    // (pipelined: every read of this buffer retired before the next TMA write into it)
+    if (tpipe) s << "fence_proxy_async();\n__syncthreads();\n";
     s << "}\n}\n";
     return s.str();
+}
+
+// Whether a seed pass runs pipelined (TMA double buffer): complex128 tiles that are a TMA box.
+bool seed_tma(const SPass& sp, bool c128, std::vector<TmaDim>& td) {
+    static const bool on = env_int("QBG_SEED_TMA", 1) != 0;  // (0: the plain tile loop; A/B)
+    if (!on || !c128 || !tma_enabled()) return false;
+    DPass probe{};
+    probe.mq = sp.mq;
+    probe.nb = sp.nb;
+    std::memcpy(probe.qpos, sp.qpos, sizeof(probe.qpos));
+    probe.B = sp.B;
+    probe.nchunks = sp.nchunks;
+    probe.ntiles = sp.ntiles;
+    return tma_layout(probe, kSeedM, true, td);
 }
 
 void seed_jit_prepare(FusedPlan& pl, bool c128, bool check_only) {
@@ -3019,12 +3077,26 @@ void run_seed(const DevState& psi, const DevState& phi, FusedPlan& pl, double* d
             const void* pp = psi.ptr;
             void* qq = phi.ptr;
             double* ep = epart + (pl.energy_only ? static_cast<int64_t>(k) * per_pass : 0);
-            void* args[] = {&pp, &qq, &ep, pl.sblob[k].data()};
-            int64_t grid = std::min<int64_t>(static_cast<int64_t>(sp.ntiles), static_cast<int64_t>(num_sms()) * 2);
+            alignas(64) unsigned char tmp[128] = {0};
+            std::vector<TmaDim> td;
+            const bool tpipe = seed_tma(sp, psi.dtype == QBG_C128, td);
+            if (tpipe) {
+                uint64_t sz[5], stv[5];
+                uint32_t bx[5];
+                for (size_t d = 0; d < td.size(); ++d) {
+                    sz[d] = td[d].size;
+                    stv[d] = td[d].stride;
+                    bx[d] = td[d].box;
+                }
+                jit::encode_tensor_map(tmp, const_cast<void*>(pp), static_cast<int>(td.size()), sz, stv, bx);
+            }
+            void* args[] = {&pp, &qq, &ep, pl.sblob[k].data(), tmp};
+            int64_t grid = std::min<int64_t>(static_cast<int64_t>(sp.ntiles), static_cast<int64_t>(num_sms()) * (tpipe ? 1 : 2));
             static const bool by_pass = env_int("QBG_PROF_KERNELS", 0) != 0;  // (diagnostics: see prof_name)
             const char* nm = !by_pass ? "seed" : sp.first ? "seed:first" : sp.last ? "seed:last" : "seed:mid";
             LaunchScope ls(nm, (pl.energy_only ? 1.0 : sp.first ? 2.0 : 3.0) * psi.bytes());
-            jit::launch(pl.jk[pl.sjk[k]], static_cast<unsigned>(grid), 256, psi.elem() << kSeedM, args);
+            jit::launch(pl.jk[pl.sjk[k]], static_cast<unsigned>(grid), 256,
+                        tpipe ? 2 * (psi.elem() << kSeedM) + 16 : psi.elem() << kSeedM, args);
         }
     } else {
         for (auto& sp : pl.spasses)
